@@ -1,0 +1,129 @@
+"""Seeded parity cases shared by tests/golden/make_golden.py and the tests.
+
+Every input is regenerated from its seed here, so the committed golden files
+only hold the reference's OUTPUTS (hashes, seam columns, run boundaries,
+dp_passes). Case shapes follow the reference's own tests (pkg/tests/*.py):
+tiny maps for the DP/label/batch invariants, small streams for the buffer,
+small clips for every pipeline mode and axis combination.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+
+def sha(a) -> str:
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def fhex(x) -> str:
+    return float(x).hex()
+
+
+def luma_table_frame() -> np.ndarray:
+    """All 2^24 RGB triples as one (4096, 4096, 3) frame (r major)."""
+    v = np.arange(1 << 24, dtype=np.uint32)
+    return np.stack([(v >> 16) & 255, (v >> 8) & 255, v & 255], -1).astype(np.uint8).reshape(4096, 4096, 3)
+
+
+# ------------------------------------------------------------------ energy cases
+def energy_case(seed: int):
+    rng = np.random.default_rng(1000 + seed)
+    h, w = int(rng.integers(3, 41)), int(rng.integers(3, 41))
+    curr = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    prev = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    return curr, prev
+
+
+ENERGY_SEEDS = list(range(12))
+
+
+# ------------------------------------------------------------------ DP / batch cases
+def map_case(seed: int, hmax=20, wmax=20):
+    rng = np.random.default_rng(2000 + seed)
+    h, w = int(rng.integers(1, hmax + 1)), int(rng.integers(1, wmax + 1))
+    kind = seed % 3
+    if kind == 0:
+        m = rng.uniform(0, 255, size=(h, w))
+    elif kind == 1:  # integer-valued (gradient-like) with many ties
+        m = rng.integers(0, 4, size=(h, w)).astype(np.float64)
+    else:            # uniform-like means of motion energies
+        m = rng.uniform(0, 255, size=(h, w)) / 3.0
+    return m
+
+
+MAP_SEEDS = list(range(40))
+
+
+def carve_case(seed: int):
+    rng = np.random.default_rng(3000 + seed)
+    h, w = int(rng.integers(3, 30)), int(rng.integers(4, 48))
+    frame = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    target = int(rng.integers(1, w))
+    energy = None
+    if seed % 2 == 0:
+        energy = rng.uniform(0, 255, size=(h, w)) / float(rng.integers(1, 7))
+    return frame, target, energy
+
+
+CARVE_SEEDS = list(range(16))
+
+
+# ------------------------------------------------------------------ buffer streams
+def stream_case(seed: int):
+    """Energy-map streams in the style of test_buffering.py:158-179 (drift + upheavals)."""
+    rng = np.random.default_rng(4000 + seed)
+    h, w = int(rng.integers(3, 24)), int(rng.integers(3, 24))
+    base = rng.uniform(20, 120, size=(h, w))
+    maps = []
+    for k in range(40):
+        jump = 120.0 if rng.random() < 0.1 else 0.0
+        maps.append(np.clip(base + rng.uniform(-6, 6, size=(h, w)) + jump, 0, 255))
+    return maps
+
+
+STREAM_SEEDS = list(range(8))
+
+
+# ------------------------------------------------------------------ small clips
+def small_clip(seed: int, t=10, h=24, w=32, gray=False, motion=2, rects=3):
+    """Moving rectangles on a noisy gradient, small enough for the reference in seconds."""
+    rng = np.random.default_rng(5000 + seed)
+    x = np.round(255.0 * np.arange(w) / (w - 1))
+    frames = []
+    params = [(rng.integers(0, 256, 3), int(rng.integers(3, max(4, h // 2))), int(rng.integers(3, max(4, w // 2))),
+               int(rng.integers(0, h)), int(rng.integers(0, w)),
+               int(rng.integers(-motion, motion + 1)), int(rng.integers(-motion, motion + 1))) for _ in range(rects)]
+    for k in range(t):
+        img = np.empty((h, w, 3)); img[:] = x[None, :, None]
+        for col, rh, rw, y0, x0, vy, vx in params:
+            img[np.ix_((y0 + vy * k + np.arange(rh)) % h, (x0 + vx * k + np.arange(rw)) % w)] = col
+        img += rng.normal(0, 4, size=img.shape)
+        f = np.clip(np.rint(img), 0, 255).astype(np.uint8)
+        frames.append(f[:, :, 0].copy() if gray else f)
+    return frames
+
+
+# name -> (clip kwargs, config kwargs)
+CLIP_CASES = {
+    "buf_w": (dict(seed=0), dict(target_width=24, mode="buffered")),
+    "buf_h": (dict(seed=1), dict(target_height=17, mode="buffered")),
+    "buf_wh": (dict(seed=2), dict(target_width=25, target_height=19, mode="buffered")),
+    "buf_wh_hf": (dict(seed=3), dict(target_width=25, target_height=19, mode="buffered", height_first=True)),
+    "buf_gray": (dict(seed=4, gray=True), dict(target_width=20, mode="buffered")),
+    "buf_fast": (dict(seed=5, motion=6, t=14), dict(target_width=22, mode="buffered")),
+    "buf_maxlen3": (dict(seed=6, t=11), dict(target_width=26, mode="buffered", max_len=3)),
+    "buf_alpha": (dict(seed=7, t=12), dict(target_width=23, mode="buffered", alpha=0.05)),
+    "buf_w1": (dict(seed=8, t=4, h=9, w=8), dict(target_width=1, mode="buffered")),
+    "buf_tall": (dict(seed=9, t=6, h=70, w=20), dict(target_width=11, mode="buffered")),
+    "buf_wide": (dict(seed=10, t=6, h=5, w=90), dict(target_width=40, mode="buffered")),
+    "buf_weights": (dict(seed=11), dict(target_width=24, mode="buffered", w_motion=0.25, w_grad=0.75)),
+    "scpl_w": (dict(seed=12, t=6), dict(target_width=24, mode="scpl")),
+    "scpl_wh": (dict(seed=13, t=5), dict(target_width=27, target_height=20, mode="scpl")),
+    "raw_w": (dict(seed=14, t=4), dict(target_width=26, mode="raw")),
+    "raw_h": (dict(seed=15, t=3), dict(target_height=20, mode="raw")),
+    "buf_single": (dict(seed=16, t=1), dict(target_width=20, mode="buffered")),
+}
