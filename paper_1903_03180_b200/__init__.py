@@ -1,0 +1,23 @@
+"""B200-native (sm_100a) buffered SCPL video retargeting -- a drop-in for `vidcarve` 0.1.0.
+
+Same public names as the reference package (pkg/src/vidcarve/__init__.py:9-68) for the
+retargeting path; the compute runs in libscpl.so (include/scpl.h) with no CPU fallback.
+Out of scope: media I/O, CLI, plots and the bench corpus helpers.
+"""
+
+from .batching import SeamBatch, batch_carve, default_energy, label_parents, remove_batch, select_batch
+from .buffering import BufferPolicy, FixedRun, SpatioTemporalBuffer, threshold
+from .energy import MAXVAL, gradient_energy, motion_energy, to_luma
+from .pipeline import (MODES, RetargetConfig, RunMetrics, replay_batches, retarget_image, retarget_video,
+                       retarget_video_tensor)
+from .seams import DpTables, Seam, cumulative_energy, min_seam, remove_seam, trace_columns, transpose
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "MAXVAL", "MODES", "BufferPolicy", "DpTables", "FixedRun", "RetargetConfig", "RunMetrics", "Seam",
+    "SeamBatch", "SpatioTemporalBuffer", "batch_carve", "cumulative_energy", "default_energy",
+    "gradient_energy", "label_parents", "min_seam", "motion_energy", "remove_batch", "remove_seam",
+    "replay_batches", "retarget_image", "retarget_video", "retarget_video_tensor", "select_batch",
+    "threshold", "to_luma", "trace_columns", "transpose",
+]

@@ -1,0 +1,553 @@
+// C-ABI (include/scpl.h) and the native orchestrator of the buffered SCPL path.
+//
+// retarget_video (pipeline.py:92-137) runs here, on the host side of the .so:
+//   1. energy codes for every frame                       (K1, one streaming pass)
+//   2. the spatio-temporal buffer scan                    (K2 chunks + exact host decision
+//      against the caller's phi table, buffering.py:93-138)
+//   3. per carved axis (width first unless height_first, pipeline.py:192-193):
+//        per run: representative luma plane + index map (+ uniform map on the first
+//        carved axis, K3), then the carve loop batched across all runs (K4-K7),
+//        then the replay gather of every frame of the run (K8)
+//   4. RunMetrics.dp_passes = total DP passes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/scpl.h"
+#include "scpl_common.cuh"
+#include "scpl_kernels.h"
+
+using namespace scpl;
+
+namespace scpl {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace scpl
+
+struct PwPlan {
+  int2* leaves = nullptr;
+  PwVnode* vnodes = nullptr;
+  int nleaves = 0;
+};
+
+struct scpl_ctx {
+  int device = 0;
+  int num_sms = 148;
+  double* h_asde = nullptr;  // pinned
+  int h_asde_cap = 0;
+  std::map<long, PwPlan> plans;
+};
+
+namespace {
+
+// stream-ordered device buffer
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  DBuf() = default;
+  DBuf(size_t bytes, cudaStream_t s) : st(s) {
+    if (bytes) SCPL_CUDA(cudaMallocAsync(&p, bytes, s));
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    p = o.p;
+    st = o.st;
+    o.p = nullptr;
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+template <class F>
+int guarded(scpl_ctx* ctx, F&& f) {
+  try {
+    if (ctx) SCPL_CUDA(cudaSetDevice(ctx->device));
+    f();
+    return 0;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return 2;
+  }
+}
+
+const PwPlan& plan_for(scpl_ctx* ctx, long N) {
+  auto it = ctx->plans.find(N);
+  if (it != ctx->plans.end()) return it->second;
+  std::vector<int2> leaves;
+  std::vector<PwVnode> vnodes;
+  build_pairwise_plan(N, leaves, vnodes);
+  PwPlan p;
+  p.nleaves = (int)leaves.size();
+  SCPL_CUDA(cudaMalloc(&p.leaves, sizeof(int2) * leaves.size()));
+  SCPL_CUDA(cudaMalloc(&p.vnodes, sizeof(PwVnode) * vnodes.size()));
+  SCPL_CUDA(cudaMemcpy(p.leaves, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice));
+  SCPL_CUDA(cudaMemcpy(p.vnodes, vnodes.data(), sizeof(PwVnode) * vnodes.size(), cudaMemcpyHostToDevice));
+  return ctx->plans.emplace(N, p).first->second;
+}
+
+double* pinned_asde(scpl_ctx* ctx, int n) {
+  if (ctx->h_asde_cap < n) {
+    if (ctx->h_asde) cudaFreeHost(ctx->h_asde);
+    ctx->h_asde = nullptr;
+    SCPL_CUDA(cudaMallocHost(&ctx->h_asde, sizeof(double) * n));
+    ctx->h_asde_cap = n;
+  }
+  return ctx->h_asde;
+}
+
+// ------------------------------------------------------------------ buffer scan
+// SpatioTemporalBuffer.push/flush over the whole clip (buffering.py:93-138).
+std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* codes, int T, int H, int W,
+                                             const scpl_video_params& P, cudaStream_t st) {
+  std::vector<std::pair<int, int>> runs;
+  if (T == 0) return runs;
+  const long N = (long)H * W;
+  const PwPlan& plan = plan_for(ctx, N);
+  int spec = P.spec_len > 0 ? P.spec_len : 8;
+  DBuf ck(sizeof(double) * 2 * N, st);
+  DBuf leafsum(sizeof(double) * spec * plan.nleaves, st);
+  DBuf asde_d(sizeof(double) * spec, st);
+  double* h = pinned_asde(ctx, spec);
+  int s = 0, n_acc = 1;
+  bool init = true;
+  while (true) {
+    int remaining = T - (s + n_acc);
+    if (remaining == 0) {
+      runs.push_back({s, n_acc});
+      break;
+    }
+    if (n_acc >= P.max_len) {  // the next push would exceed the cap: flush (buffering.py:119)
+      runs.push_back({s, n_acc});
+      s += n_acc;
+      n_acc = 1;
+      init = true;
+      continue;
+    }
+    int L = std::min(spec, std::min(remaining, P.max_len - n_acc));
+    launch_window_stats(codes, N, plan.leaves, plan.nleaves, s, n_acc, L, 1, init ? 1 : 0, P.w_motion,
+                        P.w_grad, ck.as<double>(), ck.as<double>() + N, leafsum.as<double>(), plan.vnodes,
+                        asde_d.as<double>(), st);
+    SCPL_CUDA(cudaMemcpyAsync(h, asde_d.p, sizeof(double) * L, cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaStreamSynchronize(st));
+    int breach = -1;
+    for (int c = 0; c < L; ++c) {
+      int n = n_acc + c + 1;
+      if (!(h[c] <= P.phi[n])) {  // asde <= threshold(n) and n <= max_len (buffering.py:119)
+        breach = c;
+        break;
+      }
+    }
+    if (breach < 0) {
+      n_acc += L;
+      init = false;
+    } else {
+      runs.push_back({s, n_acc + breach});
+      s = s + n_acc + breach;
+      n_acc = 1;
+      init = true;
+    }
+  }
+  return runs;
+}
+
+// ------------------------------------------------------------------ carve driver
+struct CarveSlab {
+  DBuf mem;
+  std::vector<RunCarve> runs;
+  DBuf runs_d;
+  int rows = 0, stride = 0;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// allocate per-run planes for `nruns` carves of rows x cols; with_U adds an fp64 plane
+void carve_alloc(CarveSlab& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
+                 cudaStream_t st) {
+  const int nblk = std::max(1, (rows - 1 + kBlockRows - 1) / kBlockRows);
+  const size_t plane = (size_t)rows * cols;
+  size_t per = align256(plane) * 2 + align256(plane * 2) * 2 + align256((size_t)nblk * cols * 4) +
+               align256((size_t)nblk * cols) + align256((size_t)nblk * cols * 2) + align256((size_t)cols * 8) +
+               (with_U ? align256(plane * 8) : 0) +
+               (dbg ? align256((size_t)cols * 8) + align256((size_t)cols * 2) + align256((size_t)cols * 4) : 0);
+  S.mem = DBuf(per * nruns, st);
+  S.rows = rows;
+  S.stride = cols;
+  S.runs.assign(nruns, RunCarve{});
+  uint8_t* base = S.mem.as<uint8_t>();
+  for (int r = 0; r < nruns; ++r) {
+    uint8_t* p = base + per * r;
+    RunCarve& R = S.runs[r];
+    auto take = [&](size_t bytes) {
+      uint8_t* q = p;
+      p += align256(bytes);
+      return q;
+    };
+    R.rows = rows;
+    R.stride = cols;
+    R.target = target;
+    R.kmax = kmax;
+    R.luma = take(plane);
+    R.grad = take(plane);
+    R.idx = reinterpret_cast<int16_t*>(take(plane * 2));
+    R.rem = reinterpret_cast<int16_t*>(take(plane * 2));
+    R.pw = reinterpret_cast<uint32_t*>(take((size_t)nblk * cols * 4));
+    R.delta = reinterpret_cast<int8_t*>(take((size_t)nblk * cols));
+    R.col_end = reinterpret_cast<int16_t*>(take((size_t)nblk * cols * 2));
+    R.lastce = reinterpret_cast<double*>(take((size_t)cols * 8));
+    R.U = with_U ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
+    if (dbg) {
+      R.dbg_costs = reinterpret_cast<double*>(take((size_t)cols * 8));
+      R.dbg_cols = reinterpret_cast<int16_t*>(take((size_t)cols * 2));
+      R.dbg_sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
+    }
+    R.width = cols;
+    R.done = cols <= target;
+  }
+}
+
+// run every carve in S to completion; on_iter(iteration) is called after each pass's
+// host sync when given (forces one pass per sync)
+template <class F>
+void carve_run_all(CarveSlab& S, cudaStream_t st, F&& on_iter, bool per_iter_sync) {
+  const int nruns = (int)S.runs.size();
+  if (nruns == 0) return;
+  S.runs_d = DBuf(sizeof(RunCarve) * nruns, st);
+  SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, S.runs.data(), sizeof(RunCarve) * nruns, cudaMemcpyHostToDevice, st));
+  RunCarve* rd = S.runs_d.as<RunCarve>();
+  bool any_U = false;
+  for (auto& R : S.runs) any_U |= R.U != nullptr;
+  int it = 0;
+  const int burst = per_iter_sync ? 1 : 8;
+  while (true) {
+    for (int k = 0; k < burst; ++k, ++it) {
+      launch_carve_gradient(rd, nruns, S.rows, S.stride, it == 0 ? 1 : 0, st);
+      if (it == 0 && any_U) launch_carve_dp(rd, nruns, true, S.stride, st);
+      launch_carve_dp(rd, nruns, false, S.stride, st);
+      launch_carve_select(rd, nruns, S.stride, S.rows, st);
+      launch_carve_compact(rd, nruns, S.rows, st);
+    }
+    SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(RunCarve) * nruns, cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaStreamSynchronize(st));
+    if (per_iter_sync) on_iter(it - 1);
+    bool all = true;
+    for (auto& R : S.runs) all &= R.done != 0;
+    if (all) break;
+  }
+}
+
+}  // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+int scpl_version(void) { return 1; }
+const char* scpl_last_error(void) { return g_err.c_str(); }
+
+int scpl_create(int device, scpl_ctx** out) {
+  return guarded(nullptr, [&] {
+    SCPL_ARG(out != nullptr, "out is NULL");
+    int n = 0;
+    SCPL_CUDA(cudaGetDeviceCount(&n));
+    SCPL_ARG(device >= 0 && device < n, "no such CUDA device");
+    SCPL_CUDA(cudaSetDevice(device));
+    auto* c = new scpl_ctx();
+    c->device = device;
+    SCPL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    *out = c;
+  });
+}
+
+void scpl_destroy(scpl_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (auto& kv : ctx->plans) {
+    cudaFree(kv.second.leaves);
+    cudaFree(kv.second.vnodes);
+  }
+  if (ctx->h_asde) cudaFreeHost(ctx->h_asde);
+  delete ctx;
+}
+
+int scpl_to_luma(scpl_ctx* ctx, const uint8_t* pixels, long npx, int channels, uint8_t* luma_out, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
+    launch_luma(pixels, npx, channels, luma_out, (cudaStream_t)stream);
+  });
+}
+
+int scpl_gradient_energy(scpl_ctx* ctx, const uint8_t* luma, int h, int w, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(h >= 3 && w >= 3, "frame too small for 3x3 Sobel");
+    launch_sobel_f64(luma, h, w, out, (cudaStream_t)stream);
+  });
+}
+
+int scpl_energy_codes(scpl_ctx* ctx, const uint8_t* frames, const uint8_t* prev, int T, int h, int w,
+                      int channels, uint16_t* codes, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
+    SCPL_ARG(h >= 3 && w >= 3, "frame too small for 3x3 Sobel");
+    launch_codes(frames, prev, T, h, w, channels, codes, ctx->num_sms, (cudaStream_t)stream);
+  });
+}
+
+int scpl_decode_energy(scpl_ctx* ctx, const uint16_t* codes, int T, int h, int w, int first_pure, double w_motion,
+                       double w_grad, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    launch_decode(codes, (long)h * w, T, first_pure, w_motion, w_grad, out, (cudaStream_t)stream);
+  });
+}
+
+int scpl_window_asde(scpl_ctx* ctx, const uint16_t* codes, int T, int h, int w, int start, int n_acc, int count,
+                     double w_motion, double w_grad, double* state, int init, double* asde_out, void* stream) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    SCPL_ARG(count >= 1 && n_acc >= 1 && start >= 0 && start + n_acc + count <= T, "window out of range");
+    SCPL_ARG(!init || n_acc == 1, "init requires n_acc == 1");
+    const long N = (long)h * w;
+    const PwPlan& plan = plan_for(ctx, N);
+    DBuf leafsum(sizeof(double) * count * plan.nleaves, st);
+    DBuf asde_d(sizeof(double) * count, st);
+    launch_window_stats(codes, N, plan.leaves, plan.nleaves, start, n_acc, count, 1, init, w_motion, w_grad,
+                        state, state + N, leafsum.as<double>(), plan.vnodes, asde_d.as<double>(), st);
+    SCPL_CUDA(cudaMemcpyAsync(asde_out, asde_d.p, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int scpl_uniform_energy(scpl_ctx* ctx, const uint16_t* codes, int h, int w, int start, int n, double w_motion,
+                        double w_grad, int transposed, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(n >= 1, "empty run");
+    launch_uniform(codes, h, w, start, n, 1, w_motion, w_grad, transposed, out, (cudaStream_t)stream);
+  });
+}
+
+int scpl_replay(scpl_ctx* ctx, const uint8_t* in, int T, int h, int w, int channels, const int16_t* index,
+                int stride, int target, int transposed, uint8_t* out, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
+    launch_replay(in, out, T, h, w, channels, index, stride, target, transposed, (cudaStream_t)stream);
+  });
+}
+
+int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int channels, int target,
+                     const double* energy, int kmax, int16_t* index_out, int* n_batches, int* batch_sizes,
+                     int16_t* batch_cols, double* batch_costs, int16_t* offsets, void* stream) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
+    SCPL_ARG(target >= 1, "target width must be >= 1");
+    SCPL_ARG(target <= w, "target width exceeds frame width");
+    SCPL_ARG(h >= 1 && w >= 1, "empty frame");
+    CarveSlab S;
+    carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, st);
+    RunCarve& R = S.runs[0];
+    launch_carve_setup_luma(frame, h, w, channels, 0, R.luma, R.idx, st);
+    if (energy) SCPL_CUDA(cudaMemcpyAsync(const_cast<double*>(R.U), energy, sizeof(double) * h * w,
+                                          cudaMemcpyDeviceToDevice, st));
+    int removed = 0;
+    std::vector<int16_t> rem;
+    carve_run_all(
+        S, st,
+        [&](int) {
+          if (!offsets) return;
+          const RunCarve& Rh = S.runs[0];
+          int b = Rh.b;
+          rem.resize((size_t)h * b);
+          SCPL_CUDA(cudaMemcpy(rem.data(), Rh.rem, sizeof(int16_t) * h * b, cudaMemcpyDeviceToHost));
+          for (int s = 0; s < b; ++s)
+            for (int i = 0; i < h; ++i) offsets[(size_t)(removed + s) * h + i] = rem[(size_t)i * b + s];
+          removed += b;
+        },
+        true);
+    const RunCarve& Rh = S.runs[0];
+    *n_batches = Rh.iters;
+    SCPL_CUDA(cudaMemcpyAsync(batch_sizes, Rh.dbg_sizes, sizeof(int) * Rh.iters, cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaMemcpyAsync(batch_cols, Rh.dbg_cols, sizeof(int16_t) * Rh.nremoved, cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(
+        cudaMemcpyAsync(batch_costs, Rh.dbg_costs, sizeof(double) * Rh.nremoved, cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaMemcpy2DAsync(index_out, sizeof(int16_t) * target, Rh.idx, sizeof(int16_t) * w,
+                                sizeof(int16_t) * target, h, cudaMemcpyDeviceToDevice, st));
+    SCPL_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int w, int channels,
+                        const scpl_video_params* params, uint8_t* out, scpl_video_result* result, void* stream) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    SCPL_ARG(params != nullptr && result != nullptr, "params/result is NULL");
+    const scpl_video_params P = *params;
+    SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
+    SCPL_ARG(h >= 3 && w >= 3, "frame too small to carve");
+    SCPL_ARG(P.target_width >= 1 && P.target_width <= w, "target width out of range");
+    SCPL_ARG(P.target_height >= 1 && P.target_height <= h, "target height out of range");
+    SCPL_ARG(P.mode >= 0 && P.mode <= 2, "unknown mode");
+    SCPL_ARG(P.max_len >= 1, "max_len must be >= 1");
+    SCPL_ARG(P.mode != 2 || P.phi != nullptr, "phi table required for buffered mode");
+    result->dp_passes = 0;
+    result->n_runs = 0;
+    if (T <= 0) return;
+    const int C = channels;
+    const int tw = P.target_width, th = P.target_height;
+
+    // 1. energy codes (not needed by raw mode: gradient only)
+    DBuf codes;
+    if (P.mode != 0) {
+      codes = DBuf(sizeof(uint16_t) * (size_t)T * h * w, st);
+      launch_codes(frames, nullptr, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, st);
+    }
+    // 2. runs
+    std::vector<std::pair<int, int>> runs;
+    if (P.mode == 2) {
+      runs = buffer_scan(ctx, codes.as<uint16_t>(), T, h, w, P, st);
+    } else {
+      for (int t = 0; t < T; ++t) runs.push_back({t, 1});
+    }
+    result->n_runs = (int)runs.size();
+    if (result->run_start && result->run_len)
+      for (size_t r = 0; r < runs.size(); ++r) {
+        result->run_start[r] = runs[r].first;
+        result->run_len[r] = runs[r].second;
+      }
+
+    // 3. phases (pipeline.py:192-193, 246-277)
+    std::vector<int> phases;  // 0 width, 1 height
+    for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
+      if (ax == 0 && tw < w) phases.push_back(0);
+      if (ax == 1 && th < h) phases.push_back(1);
+    }
+    if (phases.empty()) {
+      SCPL_CUDA(cudaMemcpyAsync(out, frames, (size_t)T * h * w * C, cudaMemcpyDeviceToDevice, st));
+      SCPL_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+    const uint8_t* cur = frames;
+    int curH = h, curW = w;
+    DBuf tmp;
+    long dp = 0;
+    for (size_t ph = 0; ph < phases.size(); ++ph) {
+      const bool height = phases[ph] == 1;
+      const int rows = height ? curW : curH, cols = height ? curH : curW;
+      const int target = height ? th : tw;
+      const bool with_U = (ph == 0) && P.mode != 0;
+      CarveSlab S;
+      carve_alloc(S, (int)runs.size(), rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false, st);
+      const size_t fbytes = (size_t)curH * curW * C;
+      for (size_t r = 0; r < runs.size(); ++r) {
+        RunCarve& R = S.runs[r];
+        launch_carve_setup_luma(cur + fbytes * runs[r].first, curH, curW, C, height ? 1 : 0, R.luma, R.idx, st);
+        if (with_U)
+          launch_uniform(codes.as<uint16_t>(), h, w, runs[r].first, runs[r].second, 1, P.w_motion, P.w_grad,
+                         height ? 1 : 0, const_cast<double*>(R.U), st);
+      }
+      carve_run_all(S, st, [](int) {}, false);
+      for (auto& R : S.runs) dp += R.iters;
+      const int nH = height ? th : curH, nW = height ? curW : tw;
+      const bool last = ph + 1 == phases.size();
+      DBuf next;
+      uint8_t* dst = out;
+      if (!last) {
+        next = DBuf((size_t)T * nH * nW * C, st);
+        dst = next.as<uint8_t>();
+      }
+      const size_t obytes = (size_t)nH * nW * C;
+      for (size_t r = 0; r < runs.size(); ++r) {
+        const RunCarve& R = S.runs[r];
+        launch_replay(cur + fbytes * runs[r].first, dst + obytes * runs[r].first, runs[r].second, curH, curW, C,
+                      R.idx, R.stride, target, height ? 1 : 0, st);
+      }
+      // keep S alive until the replays are enqueued (stream-ordered frees)
+      cur = dst;
+      curH = nH;
+      curW = nW;
+      tmp = std::move(next);
+    }
+    result->dp_passes = dp;
+    SCPL_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int scpl_cumulative_energy(scpl_ctx* ctx, const double* energy, int h, int w, double* ce, int8_t* back,
+                           void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(h >= 1 && w >= 1, "expected a non-empty 2-d energy map");
+    launch_dp_tables(energy, h, w, ce, back, (cudaStream_t)stream);
+  });
+}
+
+int scpl_label_parents(scpl_ctx* ctx, const int8_t* back, int h, int w, int64_t* labels, void* stream) {
+  return guarded(ctx, [&] { launch_labels(back, h, w, (long*)labels, (cudaStream_t)stream); });
+}
+
+int scpl_trace_columns(scpl_ctx* ctx, const int8_t* back, int h, int w, const int64_t* cols, int b,
+                       int64_t* offsets, void* stream) {
+  return guarded(ctx, [&] { launch_trace(back, h, w, (const long*)cols, b, (long*)offsets, (cudaStream_t)stream); });
+}
+
+int scpl_select_batch(scpl_ctx* ctx, const double* last, const int64_t* labels, int w, int k, int64_t* cols,
+                      double* costs, int* nb, void* stream) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    DBuf d_nb(sizeof(int), st);
+    launch_select_tables(last, (const long*)labels, w, k, (long*)cols, costs, d_nb.as<int>(), st);
+    SCPL_CUDA(cudaMemcpyAsync(nb, d_nb.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int scpl_remove_columns(scpl_ctx* ctx, const uint8_t* in, int h, int w, int channels, const int64_t* offsets, int b,
+                        uint8_t* out, int* rowcount, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(b >= 0 && b <= w, "batch larger than the frame");
+    launch_remove_cols(in, h, w, channels, (const long*)offsets, b, out, rowcount, (cudaStream_t)stream);
+  });
+}
+
+int scpl_sums_start(scpl_ctx* ctx, const double* e, long n, double* S, double* Q, void* stream) {
+  return guarded(ctx, [&] { launch_sums(e, n, nullptr, nullptr, S, Q, (cudaStream_t)stream); });
+}
+
+int scpl_sums_push(scpl_ctx* ctx, const double* e, long n, const double* S_in, const double* Q_in, double* S,
+                   double* Q, void* stream) {
+  return guarded(ctx, [&] { launch_sums(e, n, S_in, Q_in, S, Q, (cudaStream_t)stream); });
+}
+
+int scpl_sums_map(scpl_ctx* ctx, const double* S, const double* Q, long N, int n, int what, double* out,
+                  void* stream) {
+  return guarded(ctx, [&] { launch_sums_map(S, Q, N, n, what, out, (cudaStream_t)stream); });
+}
+
+int scpl_asde_from_sums(scpl_ctx* ctx, const double* S, const double* Q, long N, int n, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    SCPL_ARG(N >= 1 && n >= 1, "empty buffer");
+    const PwPlan& plan = plan_for(ctx, N);
+    DBuf leafsum(sizeof(double) * plan.nleaves, st);
+    DBuf d(sizeof(double), st);
+    launch_asde_sums(S, Q, N, n, plan.leaves, plan.nleaves, plan.vnodes, leafsum.as<double>(), d.as<double>(), st);
+    SCPL_CUDA(cudaMemcpyAsync(out, d.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

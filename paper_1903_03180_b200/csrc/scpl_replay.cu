@@ -1,0 +1,110 @@
+// K8: replay a run's batches on every frame of the run.
+//
+// Replaces replay_batches (pipeline.py:140-154), which calls remove_batch once per frame
+// per batch (75% of the reference's buffered wall time).  Within a batch the removed
+// columns address the frame the batch was selected on, so replaying all batches equals
+// one gather through the composed original-column index map; one pass per frame reads
+// H*W*C bytes and writes H*W'*C bytes.
+//
+// Width phase: out[t][i][y] = in[t][i][idx[i][y]] -- a CTA stages input rows in shared
+// memory with 16-byte loads, gathers, and writes the output rows with 16-byte stores.
+// Height phase (carve on the transposed frame): out[t][y][j] = in[t][idx[j][y]][j] --
+// 32x32 tiles of the index map are transposed through shared memory so both the index
+// reads and the pixel writes are coalesced.
+#include "scpl_common.cuh"
+#include "scpl_kernels.h"
+
+namespace scpl {
+
+constexpr int kReplayRows = 4;
+
+template <int C>
+__global__ void __launch_bounds__(256) replay_rows_kernel(const uint8_t* __restrict__ in,
+                                                          uint8_t* __restrict__ out, int H, int W,
+                                                          const int16_t* __restrict__ idx, int stride, int tw,
+                                                          int vec) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* rin = smem;
+  uint8_t* rout = smem + (((size_t)W * C + 15) & ~(size_t)15);
+  const int t = blockIdx.y;
+  const size_t in_row = (size_t)W * C, out_row = (size_t)tw * C;
+  for (int rr = 0; rr < kReplayRows; ++rr) {
+    const int i = blockIdx.x * kReplayRows + rr;
+    if (i >= H) break;
+    const uint8_t* src = in + ((size_t)t * H + i) * in_row;
+    uint8_t* dst = out + ((size_t)t * H + i) * out_row;
+    if (vec) {
+      for (size_t q = threadIdx.x; q < in_row / 16; q += blockDim.x)
+        reinterpret_cast<uint4*>(rin)[q] = reinterpret_cast<const uint4*>(src)[q];
+    } else {
+      for (size_t q = threadIdx.x; q < in_row; q += blockDim.x) rin[q] = src[q];
+    }
+    __syncthreads();
+    const int16_t* ir = idx + (size_t)i * stride;
+    for (int y = threadIdx.x; y < tw; y += blockDim.x) {
+      int s = ir[y];
+#pragma unroll
+      for (int c = 0; c < C; ++c) rout[y * C + c] = rin[s * C + c];
+    }
+    __syncthreads();
+    if (vec) {
+      for (size_t q = threadIdx.x; q < out_row / 16; q += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[q] = reinterpret_cast<const uint4*>(rout)[q];
+    } else {
+      for (size_t q = threadIdx.x; q < out_row; q += blockDim.x) dst[q] = rout[q];
+    }
+    __syncthreads();
+  }
+}
+
+template <int C>
+__global__ void replay_cols_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int H, int W,
+                                   const int16_t* __restrict__ idx, int stride, int th) {
+  __shared__ int16_t tile[32][33];
+  const int t = blockIdx.z;
+  const int j0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  // idx is (W, stride): carve row j = original column j, entries = original rows
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int j = j0 + r, y = y0 + threadIdx.x;
+    tile[r][threadIdx.x] = (j < W && y < th) ? idx[(size_t)j * stride + y] : (int16_t)0;
+  }
+  __syncthreads();
+  const uint8_t* src = in + (size_t)t * H * W * C;
+  uint8_t* dst = out + (size_t)t * th * W * C;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int y = y0 + r, j = j0 + threadIdx.x;
+    if (y < th && j < W) {
+      int s = tile[threadIdx.x][r];
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[((size_t)y * W + j) * C + c] = src[((size_t)s * W + j) * C + c];
+    }
+  }
+}
+
+void launch_replay(const uint8_t* in, uint8_t* out, int T, int H, int W, int C, const int16_t* idx, int stride,
+                   int target, int transposed, cudaStream_t st) {
+  if (T <= 0) return;
+  if (!transposed) {
+    bool vec = ((size_t)W * C % 16 == 0) && ((size_t)target * C % 16 == 0) &&
+               ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    size_t smem = (((size_t)W * C + 15) & ~(size_t)15) + (size_t)target * C + 16;
+    SCPL_ARG(smem <= 227 * 1024, "frame too wide for the replay kernel");
+    dim3 grid(cdiv(H, kReplayRows), T);
+    if (C == 3) {
+      SCPL_CUDA(cudaFuncSetAttribute(replay_rows_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      replay_rows_kernel<3><<<grid, 256, smem, st>>>(in, out, H, W, idx, stride, target, vec ? 1 : 0);
+    } else {
+      SCPL_CUDA(cudaFuncSetAttribute(replay_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      replay_rows_kernel<1><<<grid, 256, smem, st>>>(in, out, H, W, idx, stride, target, vec ? 1 : 0);
+    }
+  } else {
+    dim3 grid(cdiv(W, 32), cdiv(target, 32), T);
+    if (C == 3)
+      replay_cols_kernel<3><<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, idx, stride, target);
+    else
+      replay_cols_kernel<1><<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, idx, stride, target);
+  }
+  SCPL_CHECK_LAUNCH();
+}
+
+}  // namespace scpl

@@ -1,0 +1,252 @@
+// K2: window statistics for the spatio-temporal buffer scan (ASDE), bit-exact.
+//
+// Replaces SpatioTemporalBuffer.push's candidate test (buffering.py:115-119) and
+// _asde_from_sums (buffering.py:174-176).  For a run start s with n_acc frames already
+// accepted, one launch evaluates L candidate lengths n = n_acc+1 .. n_acc+L:
+//   S += e_t, Q += fl(e_t*e_t)                      (per pixel, stream order; :116-117)
+//   var = fl(Q/n) - fl(fl(S/n)^2); std = sqrt(max(var, 0))
+//   ASDE(n) = pairwise_sum(std over the row-major map) / (H*W)   (numpy's tree)
+// numpy's pairwise tree splits [0, N) recursively (n2 = n/2 rounded down to a multiple of
+// 8) into leaves of <= 128 elements, each summed with 8 strided accumulators.  The host
+// enumerates the leaves once per shape; here a group of 8 lanes owns one leaf, lane j
+// holding accumulator r[j] and the S,Q of its pixels in registers across all L
+// candidates.  A second kernel folds the leaf sums with the same tree (one CTA per
+// candidate).  The per-pixel S,Q after the chunk are checkpointed so the next chunk of
+// the same run resumes without re-reading earlier frames.
+#include <vector>
+
+#include "scpl_common.cuh"
+#include "scpl_kernels.h"
+
+namespace scpl {
+
+// ------------------------------------------------------------ host: pairwise plan
+static void plan_rec(long off, long n, std::vector<int2>& leaves) {
+  if (n <= 128) {
+    leaves.push_back(make_int2((int)off, (int)n));
+    return;
+  }
+  long h = n / 2;
+  h -= h % 8;
+  plan_rec(off, h, leaves);
+  plan_rec(off + h, n - h, leaves);
+}
+
+static long count_leaves(long n) {
+  if (n <= 128) return 1;
+  long h = n / 2;
+  h -= h % 8;
+  return count_leaves(h) + count_leaves(n - h);
+}
+
+// virtual complete tree of depth D over the recursion: node v (D bits, MSB = first split)
+static void vnodes_rec(long n, int depth, int D, int v, long first_leaf, std::vector<PwVnode>& out) {
+  if (depth == D) {
+    out[v] = PwVnode{(int)first_leaf, n};
+    return;
+  }
+  if (n <= 128) {
+    // leaf above depth D: the leftmost descendant carries it, the rest add +0.0 (exact)
+    int shift = D - depth;
+    out[v << shift] = PwVnode{(int)first_leaf, n};
+    return;
+  }
+  long h = n / 2;
+  h -= h % 8;
+  vnodes_rec(h, depth + 1, D, 2 * v, first_leaf, out);
+  vnodes_rec(n - h, depth + 1, D, 2 * v + 1, first_leaf + count_leaves(h), out);
+}
+
+void build_pairwise_plan(long N, std::vector<int2>& leaves, std::vector<PwVnode>& vnodes) {
+  leaves.clear();
+  plan_rec(0, N, leaves);
+  vnodes.assign(1 << kPwDepth, PwVnode{0, 0});
+  vnodes_rec(N, 0, kPwDepth, 0, 0, vnodes);
+}
+
+// ------------------------------------------------------------ device: leaf sums
+constexpr int kMaxPerLane = 16;  // 128 / 8
+
+__global__ void __launch_bounds__(256) window_stats_kernel(const uint16_t* __restrict__ codes, long N,
+                                                           const int2* __restrict__ leaves, int nleaves,
+                                                           int s, int n_acc, int L, int first_pure, int init,
+                                                           double wm, double wg, double* __restrict__ ckS,
+                                                           double* __restrict__ ckQ,
+                                                           double* __restrict__ leafsum) {
+  __shared__ double A[256], B[256];
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+    A[k] = __dmul_rn(wm, (double)k);
+    B[k] = __dmul_rn(wg, (double)k);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & 7;
+  const int leaf = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const bool active = leaf < nleaves;
+  int2 lf = active ? leaves[leaf] : make_int2(0, 8);
+  const int len = lf.y;
+  const int nmain = len >> 3;    // elements per lane in the 8-accumulator region
+  const int ntail = len & 7;     // sequential tail, element i = 8*nmain + k held by lane k
+  const long base = lf.x;
+
+  double S[kMaxPerLane + 1], Q[kMaxPerLane + 1];
+#pragma unroll
+  for (int k = 0; k <= kMaxPerLane; ++k) {
+    long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
+    bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
+    if (valid) {
+      if (init) {
+        uint32_t c = codes[(size_t)s * N + p];
+        double e = energy_of(c, first_pure && s == 0, A, B);
+        S[k] = e;
+        Q[k] = __dmul_rn(e, e);
+      } else {
+        S[k] = ckS[p];
+        Q[k] = ckQ[p];
+      }
+    } else {
+      S[k] = 0.0;
+      Q[k] = 0.0;
+    }
+  }
+
+  for (int c = 0; c < L; ++c) {
+    const int t = s + n_acc + c;
+    const int n = n_acc + c + 1;
+    const double dn = (double)n;
+    const double rn = __ddiv_rn(1.0, dn);
+    const uint16_t* ct = codes + (size_t)t * N;
+    const bool pure = first_pure && t == 0;
+    double acc = 0.0, tail = 0.0;
+#pragma unroll
+    for (int k = 0; k <= kMaxPerLane; ++k) {
+      long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
+      bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
+      if (valid) {
+        double e = energy_of(ct[p], pure, A, B);
+        S[k] = __dadd_rn(S[k], e);
+        Q[k] = __dadd_rn(Q[k], __dmul_rn(e, e));
+        double m = div_small(S[k], dn, rn);
+        double var = __dsub_rn(div_small(Q[k], dn, rn), __dmul_rn(m, m));
+        double sd = __dsqrt_rn(var >= 0.0 ? var : 0.0);
+        if (k < kMaxPerLane)
+          acc = (k == 0) ? sd : __dadd_rn(acc, sd);
+        else
+          tail = sd;
+      }
+    }
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)): IEEE addition commutes, so xor-shuffles give
+    // exactly numpy's bracketing.
+    double x = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 2));
+    x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 4));
+    const int g0 = lane & ~7;
+    for (int k = 0; k < 7; ++k) {  // tail elements in order (uniform trip count for shuffles)
+      double tv = __shfl_sync(0xffffffffu, tail, g0 + k);
+      if (k < ntail) x = __dadd_rn(x, tv);
+    }
+    if (active && sub == 0) leafsum[(size_t)c * nleaves + leaf] = x;
+  }
+
+  // checkpoint S,Q after n_acc + L frames
+#pragma unroll
+  for (int k = 0; k <= kMaxPerLane; ++k) {
+    long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
+    bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
+    if (valid) {
+      ckS[p] = S[k];
+      ckQ[p] = Q[k];
+    }
+  }
+}
+
+// ------------------------------------------------------------ device: tree fold
+__device__ double pw_eval(long n, const double* __restrict__ ls, int& li) {
+  if (n <= 128) return ls[li++];
+  long h = n / 2;
+  h -= h % 8;
+  double a = pw_eval(h, ls, li);
+  double b = pw_eval(n - h, ls, li);
+  return __dadd_rn(a, b);
+}
+
+__global__ void __launch_bounds__(1024) pairwise_fold_kernel(const double* __restrict__ leafsum, int nleaves,
+                                                             const PwVnode* __restrict__ vnodes, long N,
+                                                             double* __restrict__ asde_out) {
+  __shared__ double v[1 << kPwDepth];
+  const int c = blockIdx.x;
+  const double* ls = leafsum + (size_t)c * nleaves;
+  for (int t = threadIdx.x; t < (1 << kPwDepth); t += blockDim.x) {
+    PwVnode vn = vnodes[t];
+    double x = 0.0;
+    if (vn.n > 0) {
+      int li = vn.first_leaf;
+      x = pw_eval(vn.n, ls, li);
+    }
+    v[t] = x;
+  }
+  __syncthreads();
+  for (int size = (1 << kPwDepth) >> 1; size >= 1; size >>= 1) {
+    for (int t = threadIdx.x; t < size; t += blockDim.x) v[t] = __dadd_rn(v[2 * t], v[2 * t + 1]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) asde_out[c] = __ddiv_rn(__dadd_rn(0.0, v[0]), (double)N);
+}
+
+void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int nleaves, int s, int n_acc,
+                         int L, int first_pure, int init, double wm, double wg, double* ckS, double* ckQ,
+                         double* leafsum, const PwVnode* vnodes, double* asde_out, cudaStream_t st) {
+  int threads = 256;
+  int blocks = cdiv((long)nleaves * 8, threads);
+  window_stats_kernel<<<blocks, threads, 0, st>>>(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init, wm,
+                                                  wg, ckS, ckQ, leafsum);
+  SCPL_CHECK_LAUNCH();
+  pairwise_fold_kernel<<<L, 1024, 0, st>>>(leafsum, nleaves, vnodes, N, asde_out);
+  SCPL_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------ K3: uniform map
+// FixedRun.uniform_energy (buffering.py:69-71): sequential per-pixel sum over the run's
+// frames, divided by T (equal to np.stack(maps).mean(axis=0) bit for bit).  Written in
+// the carve orientation (transposed for a height phase) with a 32x32 smem tile.
+__global__ void uniform_kernel(const uint16_t* __restrict__ codes, int H, int W, int s, int n, int first_pure,
+                               double wm, double wg, int transposed, double* __restrict__ out) {
+  __shared__ double A[256], B[256];
+  __shared__ double tile[32][33];
+  for (int k = threadIdx.y * 32 + threadIdx.x; k < 256; k += 256) {
+    A[k] = __dmul_rn(wm, (double)k);
+    B[k] = __dmul_rn(wg, (double)k);
+  }
+  __syncthreads();
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  const long N = (long)H * W;
+  const double dn = (double)n;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int i = i0 + r, j = j0 + threadIdx.x;
+    double acc = 0.0;
+    if (i < H && j < W) {
+      long p = (long)i * W + j;
+      acc = energy_of(codes[(size_t)s * N + p], first_pure && s == 0, A, B);
+      for (int t = s + 1; t < s + n; ++t) acc = __dadd_rn(acc, energy_of(codes[(size_t)t * N + p], false, A, B));
+      acc = __ddiv_rn(acc, dn);
+      if (!transposed) out[p] = acc;
+    }
+    tile[r][threadIdx.x] = acc;
+  }
+  if (!transposed) return;
+  __syncthreads();
+  // out is (W, H): out[j][i]
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int j = j0 + r, i = i0 + threadIdx.x;
+    if (i < H && j < W) out[(long)j * H + i] = tile[threadIdx.x][r];
+  }
+}
+
+void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
+                    int transposed, double* out, cudaStream_t st) {
+  dim3 grid(cdiv(W, 32), cdiv(H, 32));
+  uniform_kernel<<<grid, dim3(32, 8), 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, transposed, out);
+  SCPL_CHECK_LAUNCH();
+}
+
+}  // namespace scpl

@@ -1,0 +1,62 @@
+"""CPU-side checks of the C-ABI boundary: the library loads and exports every entry point
+declared in include/scpl.h (no compute calls: there is no GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "scpl.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(scpl_\w+)\s*\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1903_03180_b200 import build_ext
+    build_ext.build()
+    return ctypes.CDLL(build_ext.LIB)
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    assert "scpl_retarget_video" in names and "scpl_window_asde" in names and len(names) >= 20
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header():
+    from paper_1903_03180_b200 import _lib
+    assert sorted(_lib.exported_symbols()) == _declared()
+
+
+def test_version_and_error_without_gpu(lib):
+    lib.scpl_version.restype = ctypes.c_int
+    assert lib.scpl_version() == 1
+    lib.scpl_last_error.restype = ctypes.c_char_p
+    out = ctypes.c_void_p()
+    rc = lib.scpl_create(0, ctypes.byref(out))
+    assert rc != 0  # no CUDA device in the build container: fails loudly, no fallback
+    assert lib.scpl_last_error()
+
+
+def test_product_has_no_oracle_imports():
+    pkg = os.path.join(ROOT, "paper_1903_03180_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
+
+
+def test_compute_entry_points_fail_loudly_without_cuda():
+    import numpy as np
+    import paper_1903_03180_b200 as P
+    with pytest.raises(RuntimeError):
+        P.retarget_video([np.zeros((8, 8, 3), np.uint8)], P.RetargetConfig(target_width=4, mode="buffered"))

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden vectors
+and the CPU oracle. Bit-exact everywhere (integer/byte outputs and float64 maps alike).
+"""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+import cases
+from cases import fhex, sha
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def small():
+    with open(os.path.join(GOLD, "small.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1903_03180_b200 as P
+    return P
+
+
+def _batch_rec(b):
+    offs = np.stack([s.offsets for s in b.seams], axis=1).astype(np.int32) if len(b) else np.zeros((0, 0), np.int32)
+    return {"b": len(b), "cols": [int(s.offsets[-1]) for s in b.seams], "costs": [fhex(s.cost) for s in b.seams],
+            "offsets_sha": sha(offs), "source_width": b.source_width}
+
+
+# ------------------------------------------------------------------ energy
+def test_luma_all_2pow24_triples(P):
+    lt = cases.luma_table_frame()
+    want = open(os.path.join(GOLD, "luma_table.sha256")).read().strip()
+    assert sha(P.to_luma(lt)) == want
+
+
+def test_energy_golden(P, small):
+    for s in cases.ENERGY_SEEDS:
+        curr, prev = cases.energy_case(s)
+        g = small["energy"][str(s)]
+        assert sha(P.to_luma(curr)) == g["luma"], s
+        assert sha(P.gradient_energy(P.to_luma(curr))) == g["grad"], s
+        assert sha(P.motion_energy(curr, prev)) == g["motion"], s
+        assert sha(P.motion_energy(curr, None)) == g["motion_first"], s
+        assert sha(P.motion_energy(curr, prev, 0.3, 0.7)) == g["motion_w"], s
+
+
+def test_energy_known_answers(P):
+    assert (P.to_luma(np.full((4, 5, 3), 100, np.uint8)) == 100).all()
+    red = np.zeros((3, 3, 3), np.uint8)
+    red[..., 0] = 255
+    assert P.to_luma(red)[0, 0] == 76
+    assert (P.motion_energy(np.full((5, 5), 60, np.uint8), np.full((5, 5), 50, np.uint8)) == 6.0).all()
+    f = np.zeros((6, 6), np.uint8)
+    f[:, 3:] = 255
+    assert sorted(set(np.nonzero(P.gradient_energy(f))[1].tolist())) == [2, 3]
+
+
+def test_energy_codes_random_frames_vs_oracle(P):
+    from oracle import scpl_oracle as O
+    rng = np.random.default_rng(5)
+    for h, w in [(3, 3), (7, 13), (64, 80), (241, 333), (1080, 1920)]:
+        a = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+        b = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+        assert np.array_equal(P.motion_energy(a, b), O.motion_energy(a, b)), (h, w)
+        assert np.array_equal(P.motion_energy(a, None), O.motion_energy(a, None)), (h, w)
+
+
+# ------------------------------------------------------------------ DP / labels / batches
+def test_dp_labels_batches_golden(P, small):
+    for s in cases.MAP_SEEDS:
+        m = cases.map_case(s)
+        g = small["dp"][str(s)]
+        t = P.cumulative_energy(m)
+        assert sha(t.ce) == g["ce"] and sha(t.back) == g["back"], s
+        lab = P.label_parents(t)
+        assert lab.tolist() == g["labels"], s
+        assert _batch_rec(P.select_batch(t, lab)) == g["batch"], s
+        assert _batch_rec(P.select_batch(t, lab, k=g["k"])) == g["batch_k"], s
+
+
+def test_known_answer_tables(P):
+    t = P.cumulative_energy(np.array([[1, 2, 3], [4, 5, 6], [7, 8, 9]], dtype=np.float64))
+    assert t.ce.tolist() == [[1, 2, 3], [5, 6, 8], [12, 13, 15]]
+    assert P.min_seam(t).offsets.tolist() == [0, 0, 0]
+    t2 = P.cumulative_energy(np.full((2, 3), 5.0))
+    lab = P.label_parents(t2)
+    assert lab.tolist() == [0, 0, 1]
+    b = P.select_batch(t2, lab)
+    assert [s.offsets.tolist() for s in b] == [[0, 0], [1, 2]]
+    assert P.remove_batch(np.array([[1, 2, 3], [4, 5, 6]], np.uint8), b).tolist() == [[3], [5]]
+
+
+def test_batch_carve_golden(P, small):
+    for s in cases.CARVE_SEEDS:
+        frame, target, energy = cases.carve_case(s)
+        carved, batches = P.batch_carve(frame, target, energy=energy)
+        g = small["carve"][str(s)]
+        assert [_batch_rec(b) for b in batches] == g["batches"], s
+        assert sha(carved) == g["carved"], s
+
+
+def test_batch_carve_zero_band(P):
+    energy = np.full((2, 12), 100.0)
+    energy[:, 5:8] = 0.0
+    out, batches = P.batch_carve(np.zeros((2, 12), np.uint8), 10, energy=energy)
+    assert out.shape == (2, 10) and len(batches[0]) == 2
+    for seam in batches[0]:
+        assert seam.cost == 0.0 and all(5 <= int(c) <= 7 for c in seam.offsets)
+
+
+def test_batch_carve_random_vs_oracle(P):
+    from oracle import scpl_oracle as O
+    rng = np.random.default_rng(9)
+    for k in range(6):
+        h, w = int(rng.integers(16, 200)), int(rng.integers(16, 300))
+        frame = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+        energy = rng.uniform(0, 255, size=(h, w)) / 3 if k % 2 else None
+        tgt = int(rng.integers(max(1, w // 2), w))
+        c1, b1 = P.batch_carve(frame, tgt, energy=energy)
+        c2, b2 = O.batch_carve(frame, tgt, energy=energy)
+        assert np.array_equal(c1, c2)
+        assert [len(x) for x in b1] == [len(x) for x in b2]
+        for x, y in zip(b1, b2):
+            assert [int(s.offsets[-1]) for s in x] == [int(c) for c in y.cols]
+            assert [s.cost for s in x] == [float(c) for c in y.costs]
+            assert np.array_equal(np.stack([s.offsets for s in x], 1), y.offsets)
+
+
+# ------------------------------------------------------------------ buffer
+def test_buffer_stream_golden(P, small):
+    for s in cases.STREAM_SEEDS:
+        maps = cases.stream_case(s)
+        g = small["stream"][str(s)]
+        buf = P.SpatioTemporalBuffer(policy=P.BufferPolicy())
+        runs = []
+        for m in maps:
+            r = buf.push(np.zeros(m.shape, np.uint8), m)
+            if r is not None:
+                runs.append(len(r))
+        runs.append(len(buf.flush()))
+        assert runs == g["runs"], s
+
+
+def test_buffer_known_answers(P):
+    assert P.threshold(2, P.BufferPolicy()) == pytest.approx(25.5, abs=1e-12)
+    buf = P.SpatioTemporalBuffer(policy=P.BufferPolicy(alpha=1000.0))
+    for m in [np.zeros((3, 3)), np.full((3, 3), 255.0)]:
+        buf.push(np.zeros((3, 3), np.uint8), m)
+    assert buf.asde() == pytest.approx(127.5, abs=1e-12)
+    assert (buf.uniform_energy() == 127.5).all()
+    pol = P.BufferPolicy(max_len=4)
+    b2 = P.SpatioTemporalBuffer(policy=pol)
+    runs = [len(r) for r in (b2.push(np.zeros((3, 3), np.uint8), np.full((3, 3), 50.0)) for _ in range(10)) if r]
+    runs.append(len(b2.flush()))
+    assert runs == [4, 4, 2]
+
+
+# ------------------------------------------------------------------ pipeline
+def _cfg(P, cfg):
+    cfg = dict(cfg)
+    pol = P.BufferPolicy(**{k: cfg.pop(k) for k in ("alpha", "max_len") if k in cfg})
+    return P.RetargetConfig(policy=pol, **cfg)
+
+
+def test_pipeline_small_clips_golden(P, small):
+    for name, (ck, cfg) in cases.CLIP_CASES.items():
+        frames = cases.small_clip(**ck)
+        out, m = P.retarget_video(frames, _cfg(P, cfg))
+        g = small["clips"][name]
+        assert m.dp_passes == g["dp_passes"], name
+        assert [list(f.shape) for f in out] == g["shapes"], name
+        assert [sha(f) for f in out] == g["frames"], name
+
+
+def test_pipeline_errors(P):
+    with pytest.raises(ValueError, match="exceeds"):
+        P.retarget_image(np.zeros((8, 8), np.uint8), P.RetargetConfig(target_width=9))
+    with pytest.raises(ValueError, match="too small"):
+        P.retarget_image(np.zeros((2, 8), np.uint8), P.RetargetConfig(target_width=4))
+    with pytest.raises(ValueError, match="frame 1"):
+        P.retarget_video([np.zeros((8, 8), np.uint8), np.zeros((8, 9), np.uint8)], P.RetargetConfig(target_width=4))
+    out, m = P.retarget_video([], P.RetargetConfig(target_width=4, mode="buffered"))
+    assert out == [] and m.frames_out == 0 and m.dp_passes == 0
+
+
+def test_image_raw_pass_counts(P):
+    rng = np.random.default_rng(51)
+    frame = rng.integers(0, 256, size=(10, 15, 3), dtype=np.uint8)
+    out, m = P.retarget_image(frame, P.RetargetConfig(target_width=10, mode="raw"))
+    assert out.shape == (10, 10, 3) and m.dp_passes == 5
+
+
+def _config_golden(name):
+    return sorted(glob.glob(os.path.join(GOLD, f"{name}*.json")))
+
+
+@pytest.mark.parametrize("path", _config_golden("C1") + _config_golden("C2") + _config_golden("C3")
+                         + _config_golden("C4") + _config_golden("C5"))
+def test_config_clip_golden(P, path):
+    """Full BASELINE config clips vs the reference's own run (runs, dp_passes, every frame)."""
+    from paper_1903_03180_b200.synth import config_clip
+    import torch
+    g = json.load(open(path))
+    clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
+    dev = torch.from_numpy(clip).cuda()
+    out, m = P.retarget_video_tensor(dev, P.RetargetConfig(target_width=tw, target_height=th, mode="buffered"))
+    assert [list(r) for r in m.runs] == g["runs"]
+    assert m.dp_passes == g["dp_passes"]
+    host = out.cpu().numpy()
+    assert list(host.shape[1:]) == g["out_shape"]
+    bad = [t for t in range(host.shape[0]) if sha(host[t]) != g["frames_sha"][t]]
+    assert not bad, f"{len(bad)} frames differ, first {bad[:5]}"
