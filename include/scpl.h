@@ -34,6 +34,7 @@ extern "C" {
 typedef struct scpl_ctx scpl_ctx;
 
 int scpl_version(void);
+long scpl_kernel_launches(void); /* kernels this library has launched so far (process-wide) */
 const char* scpl_last_error(void);
 int scpl_create(int device, scpl_ctx** out);
 void scpl_destroy(scpl_ctx* ctx);
@@ -110,6 +111,7 @@ typedef struct {
   int n_runs;
   int* run_start;      /* host, capacity T (nullable) */
   int* run_len;        /* host, capacity T (nullable) */
+  float phase_ms[4];   /* device time of: energy codes, buffer scan, carve, replay */
 } scpl_video_result;
 
 /* vidcarve.pipeline.retarget_video (pipeline.py:92-137), buffered / scpl / raw modes,

@@ -380,7 +380,7 @@ def _transpose(a):
     return np.ascontiguousarray(np.swapaxes(np.asarray(a), 0, 1))
 
 
-def _carve_frames(frames, tw, th, first_energy, height_first, kmax):
+def _carve_frames(frames, tw, th, first_energy, height_first, kmax, literal_replay=False):
     """_process_run / _retarget_single (pipeline.py:196-226, 246-277): width then height,
     the first carved phase on `first_energy`, later phases on gradient energy; the carve
     runs on frames[0] and is replayed on every frame of the group."""
@@ -396,8 +396,11 @@ def _carve_frames(frames, tw, th, first_energy, height_first, kmax):
         work = [_transpose(f) for f in cur] if axis == "height" else cur
         pe = (_transpose(emap) if emap is not None else None) if axis == "height" else emap
         _, batches = batch_carve(work[0], target, energy=pe, kmax=kmax)
-        idx = compose_index(work[0].shape[0], work[0].shape[1], batches)
-        work = replay_gather(work, idx)
+        if literal_replay:   # the reference's batch-by-batch remove_batch loop (timing fidelity)
+            work = replay_batches(work, batches)
+        else:
+            idx = compose_index(work[0].shape[0], work[0].shape[1], batches)
+            work = replay_gather(work, idx)
         passes += len(batches)
         per_phase.append(batches)
         cur = [_transpose(f) for f in work] if axis == "height" else work
@@ -417,7 +420,7 @@ def _resolve(size, target, axis):
 
 def retarget_video(frames, target_width=None, target_height=None, mode="buffered",
                    policy: BufferPolicy = BufferPolicy(), w_motion=0.6, w_grad=0.4,
-                   height_first=False, keep_batches=False) -> Result:
+                   height_first=False, keep_batches=False, literal_replay=False) -> Result:
     """pipeline.py:92-137 (buffered, scpl, raw branches; reaverage_energy=False)."""
     t0 = time.perf_counter()
     frames = [np.asarray(f) for f in frames]
@@ -434,7 +437,7 @@ def retarget_video(frames, target_width=None, target_height=None, mode="buffered
     out, passes, all_batches = [], 0, []
     if mode == "raw":
         for f in frames:
-            c, n, b = _carve_frames([f], tw, th, None, height_first, kmax=1)
+            c, n, b = _carve_frames([f], tw, th, None, height_first, kmax=1, literal_replay=literal_replay)
             out += c
             passes += n
             all_batches.append(b if keep_batches else None)
@@ -450,7 +453,8 @@ def retarget_video(frames, target_width=None, target_height=None, mode="buffered
             u = emaps[s] if n == 1 else uniform_energy(emaps[s:s + n])
             if mode == "scpl":
                 u = emaps[s]
-            c, p, b = _carve_frames(frames[s:s + n], tw, th, u, height_first, kmax=None)
+            c, p, b = _carve_frames(frames[s:s + n], tw, th, u, height_first, kmax=None,
+                                    literal_replay=literal_replay)
             out += c
             passes += p
             all_batches.append(b if keep_batches else None)

@@ -32,13 +32,14 @@ class VideoParams(ctypes.Structure):
 class VideoResult(ctypes.Structure):
     _fields_ = [
         ("dp_passes", ctypes.c_long), ("n_runs", ctypes.c_int),
-        ("run_start", _c_int_p), ("run_len", _c_int_p),
+        ("run_start", _c_int_p), ("run_len", _c_int_p), ("phase_ms", ctypes.c_float * 4),
     ]
 
 
 # name -> argtypes (all return int unless listed in _RESTYPE)
 _SIGS = {
     "scpl_version": [],
+    "scpl_kernel_launches": [],
     "scpl_last_error": [],
     "scpl_create": [ctypes.c_int, ctypes.POINTER(_vp)],
     "scpl_destroy": [_vp],
@@ -67,7 +68,7 @@ _SIGS = {
     "scpl_sums_map": [_vp, _vp, _vp, ctypes.c_long, ctypes.c_int, ctypes.c_int, _vp, _vp],
     "scpl_asde_from_sums": [_vp, _vp, _vp, ctypes.c_long, ctypes.c_int, ctypes.POINTER(ctypes.c_double), _vp],
 }
-_RESTYPE = {"scpl_last_error": ctypes.c_char_p, "scpl_destroy": None}
+_RESTYPE = {"scpl_last_error": ctypes.c_char_p, "scpl_destroy": None, "scpl_kernel_launches": ctypes.c_long}
 
 _lib = None
 _lock = threading.Lock()

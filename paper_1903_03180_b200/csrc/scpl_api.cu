@@ -26,6 +26,7 @@ using namespace scpl;
 namespace scpl {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+std::atomic<long> g_launches{0};
 }  // namespace scpl
 
 struct PwPlan {
@@ -259,6 +260,7 @@ void carve_run_all(CarveSlab& S, cudaStream_t st, F&& on_iter, bool per_iter_syn
 extern "C" {
 
 int scpl_version(void) { return 1; }
+long scpl_kernel_launches(void) { return g_launches.load(); }
 const char* scpl_last_error(void) { return g_err.c_str(); }
 
 int scpl_create(int device, scpl_ctx** out) {
@@ -406,9 +408,21 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
     SCPL_ARG(P.mode != 2 || P.phi != nullptr, "phi table required for buffered mode");
     result->dp_passes = 0;
     result->n_runs = 0;
+    for (float& x : result->phase_ms) x = 0.f;
     if (T <= 0) return;
     const int C = channels;
     const int tw = P.target_width, th = P.target_height;
+    // device-side phase timing (codes, scan, carve, replay) for the bench
+    cudaEvent_t ev[5];
+    for (auto& e : ev) SCPL_CUDA(cudaEventCreate(&e));
+    struct EvGuard {
+      cudaEvent_t* e;
+      ~EvGuard() {
+        for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+      }
+    } evg{ev};
+    float carve_ms = 0.f, replay_ms = 0.f;
+    SCPL_CUDA(cudaEventRecord(ev[0], st));
 
     // 1. energy codes (not needed by raw mode: gradient only)
     DBuf codes;
@@ -416,6 +430,7 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
       codes = DBuf(sizeof(uint16_t) * (size_t)T * h * w, st);
       launch_codes(frames, nullptr, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, st);
     }
+    SCPL_CUDA(cudaEventRecord(ev[1], st));
     // 2. runs
     std::vector<std::pair<int, int>> runs;
     if (P.mode == 2) {
@@ -423,6 +438,10 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
     } else {
       for (int t = 0; t < T; ++t) runs.push_back({t, 1});
     }
+    SCPL_CUDA(cudaEventRecord(ev[2], st));
+    SCPL_CUDA(cudaEventSynchronize(ev[2]));
+    SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[0], ev[0], ev[1]));
+    SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[1], ev[1], ev[2]));
     result->n_runs = (int)runs.size();
     if (result->run_start && result->run_len)
       for (size_t r = 0; r < runs.size(); ++r) {
@@ -460,7 +479,9 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
           launch_uniform(codes.as<uint16_t>(), h, w, runs[r].first, runs[r].second, 1, P.w_motion, P.w_grad,
                          height ? 1 : 0, const_cast<double*>(R.U), st);
       }
+      SCPL_CUDA(cudaEventRecord(ev[3], st));
       carve_run_all(S, st, [](int) {}, false);
+      SCPL_CUDA(cudaEventRecord(ev[4], st));
       for (auto& R : S.runs) dp += R.iters;
       const int nH = height ? th : curH, nW = height ? curW : tw;
       const bool last = ph + 1 == phases.size();
@@ -476,6 +497,13 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
         launch_replay(cur + fbytes * runs[r].first, dst + obytes * runs[r].first, runs[r].second, curH, curW, C,
                       R.idx, R.stride, target, height ? 1 : 0, st);
       }
+      SCPL_CUDA(cudaEventRecord(ev[2], st));
+      SCPL_CUDA(cudaEventSynchronize(ev[2]));
+      float a = 0.f, b = 0.f;
+      SCPL_CUDA(cudaEventElapsedTime(&a, ev[3], ev[4]));
+      SCPL_CUDA(cudaEventElapsedTime(&b, ev[4], ev[2]));
+      carve_ms += a;
+      replay_ms += b;
       // keep S alive until the replays are enqueued (stream-ordered frees)
       cur = dst;
       curH = nH;
@@ -484,6 +512,8 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
     }
     result->dp_passes = dp;
     SCPL_CUDA(cudaStreamSynchronize(st));
+    result->phase_ms[2] = carve_ms;
+    result->phase_ms[3] = replay_ms;
   });
 }
 

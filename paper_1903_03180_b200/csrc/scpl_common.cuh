@@ -3,12 +3,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 namespace scpl {
 
 // ---------------------------------------------------------------- error plumbing
 void set_error(const std::string& msg);
+extern std::atomic<long> g_launches;  // kernels launched by this library (bench evidence)
 struct Error {
   int code;  // 1 = invalid argument (ValueError), 2 = CUDA/runtime (RuntimeError)
   std::string msg;
@@ -20,7 +22,11 @@ struct Error {
     if (_e != cudaSuccess)                                                                  \
       throw ::scpl::Error{2, std::string(#x) + ": " + cudaGetErrorString(_e)};              \
   } while (0)
-#define SCPL_CHECK_LAUNCH() SCPL_CUDA(cudaGetLastError())
+#define SCPL_CHECK_LAUNCH()                                  \
+  do {                                                       \
+    ::scpl::g_launches.fetch_add(1, std::memory_order_relaxed); \
+    SCPL_CUDA(cudaGetLastError());                           \
+  } while (0)
 #define SCPL_ARG(cond, msg)                                      \
   do {                                                           \
     if (!(cond)) throw ::scpl::Error{1, std::string(msg)};       \

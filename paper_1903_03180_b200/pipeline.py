@@ -112,7 +112,12 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int):
                                                ctypes.byref(params), out.data_ptr(), ctypes.byref(res),
                                                _lib.stream()))
     runs = [(starts[i], lens[i]) for i in range(res.n_runs)]
+    global last_phase_ms
+    last_phase_ms = dict(zip(("codes", "scan", "carve", "replay"), (float(x) for x in res.phase_ms)))
     return out, int(res.dp_passes), runs
+
+
+last_phase_ms: dict = {}   # device time per phase of the last clip (bench instrumentation)
 
 
 def retarget_video_tensor(clip, config: RetargetConfig):
@@ -134,6 +139,18 @@ def retarget_video_tensor(clip, config: RetargetConfig):
     return out, RunMetrics(dp_passes=dp, wall_time=time.perf_counter() - start, frames_out=T, runs=runs)
 
 
+def _retarget_host_tensor(clip, config: RetargetConfig):
+    """Host (ideally pinned) uint8 tensor (T,H,W[,C]) in, host tensor out: H2D, carve, D2H."""
+    torch = _lib.torch_cuda()
+    start = time.perf_counter()
+    dev = clip.cuda(non_blocking=clip.is_pinned())
+    out, m = retarget_video_tensor(dev, config)
+    host = torch.empty(out.shape, dtype=torch.uint8, pin_memory=True)
+    host.copy_(out)
+    m.wall_time = time.perf_counter() - start
+    return host, m
+
+
 def retarget_video(frames: Iterable[np.ndarray], config: RetargetConfig):
     """pipeline.py:92-137: carve a stream of frames; output count always equals input count."""
     torch = None
@@ -141,8 +158,10 @@ def retarget_video(frames: Iterable[np.ndarray], config: RetargetConfig):
         import torch  # noqa: F401
     except ImportError:  # pragma: no cover
         pass
-    if torch is not None and isinstance(frames, torch.Tensor) and frames.is_cuda:
-        return retarget_video_tensor(frames, config)
+    if torch is not None and isinstance(frames, torch.Tensor):
+        if frames.is_cuda:
+            return retarget_video_tensor(frames, config)
+        return _retarget_host_tensor(frames, config)
     start = time.perf_counter()
     arrs = []
     shape = None

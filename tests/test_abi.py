@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "scpl.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(scpl_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|long|void|const char\*)\s+(scpl_\w+)\s*\(", src, re.M)))
 
 
 @pytest.fixture(scope="module")
