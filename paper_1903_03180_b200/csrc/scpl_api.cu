@@ -273,6 +273,11 @@ int scpl_create(int device, scpl_ctx** out) {
     auto* c = new scpl_ctx();
     c->device = device;
     SCPL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    // keep freed workspace in the stream-ordered pool (no unmap/remap of GBs per clip)
+    cudaMemPool_t pool;
+    SCPL_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    SCPL_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     *out = c;
   });
 }

@@ -271,8 +271,10 @@ __global__ void __launch_bounds__(1024) fold_one_kernel(const double* __restrict
     v[t] = x;
   }
   __syncthreads();
-  for (int size = (1 << kPwDepth) >> 1; size >= 1; size >>= 1) {
-    for (int t = threadIdx.x; t < size; t += blockDim.x) v[t] = __dadd_rn(v[2 * t], v[2 * t + 1]);
+  // fold the complete tree in place at the left child's slot: v[2ts] = v[2ts] + v[2ts+s]
+  for (int s = 1; s < (1 << kPwDepth); s <<= 1) {
+    for (int t = threadIdx.x; t < ((1 << kPwDepth) >> 1) / s; t += blockDim.x)
+      v[2 * t * s] = __dadd_rn(v[2 * t * s], v[2 * t * s + s]);
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = __ddiv_rn(__dadd_rn(0.0, v[0]), (double)N);
