@@ -112,6 +112,8 @@ typedef struct {
   int* run_start;      /* host, capacity T (nullable) */
   int* run_len;        /* host, capacity T (nullable) */
   float phase_ms[4];   /* device time of: energy codes, buffer scan, carve, replay */
+  long long carve_cycles[4]; /* SM cycles of the slowest run's carve: dp, select, compact, gradient */
+  int carve_cluster;   /* CTAs per run cluster used by the carve */
 } scpl_video_result;
 
 /* vidcarve.pipeline.retarget_video (pipeline.py:92-137), buffered / scpl / raw modes,

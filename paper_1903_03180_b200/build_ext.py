@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libscpl.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["scpl_energy.cu", "scpl_stats.cu", "scpl_carve.cu", "scpl_replay.cu", "scpl_tables.cu", "scpl_api.cu"]
+SOURCES = ["scpl_energy.cu", "scpl_stats.cu", "scpl_carve2.cu", "scpl_replay.cu", "scpl_tables.cu", "scpl_api.cu"]
 HEADERS = ["scpl_common.cuh", "scpl_kernels.h", os.path.join("..", "..", "include", "scpl.h")]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -170,87 +170,91 @@ std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* code
 }
 
 // ------------------------------------------------------------------ carve driver
-struct CarveSlab {
-  DBuf mem;
-  std::vector<RunCarve> runs;
-  DBuf runs_d;
-  int rows = 0, stride = 0;
-};
-
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// allocate per-run planes for `nruns` carves of rows x cols; with_U adds an fp64 plane
-void carve_alloc(CarveSlab& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
-                 cudaStream_t st) {
+// Planes for `nruns` carves of rows x cols (carve orientation) in one stream-ordered slab.
+struct CarveSet {
+  DBuf mem, runs_d;
+  std::vector<CarveRun> runs;
+  int rows = 0, cols = 0, pitch = 0, target = 0, cl = 1;
+  long long prof[4] = {0, 0, 0, 0};
+};
+
+void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
+                 int cl, cudaStream_t st) {
+  const int pitch = (cols + 15) & ~15;
   const int nblk = std::max(1, (rows - 1 + kBlockRows - 1) / kBlockRows);
-  const size_t plane = (size_t)rows * cols;
-  size_t per = align256(plane) * 2 + align256(plane * 2) * 2 + align256((size_t)nblk * cols * 4) +
-               align256((size_t)nblk * cols) + align256((size_t)nblk * cols * 2) + align256((size_t)cols * 8) +
+  const int rem_cap = std::max(1, cols - target);
+  const int alive_pitch = ((cols + 31) / 32 + 3) & ~3;
+  const size_t plane = (size_t)rows * pitch;
+  size_t per = align256(plane) * 2 + align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
+               align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
+               align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(64) +
                (with_U ? align256(plane * 8) : 0) +
-               (dbg ? align256((size_t)cols * 8) + align256((size_t)cols * 2) + align256((size_t)cols * 4) : 0);
+               (dbg ? align256((size_t)cols * 4) + align256((size_t)cols * 2) + align256((size_t)cols * 8) : 0);
   S.mem = DBuf(per * nruns, st);
   S.rows = rows;
-  S.stride = cols;
-  S.runs.assign(nruns, RunCarve{});
+  S.cols = cols;
+  S.pitch = pitch;
+  S.target = target;
+  S.cl = cl;
+  S.runs.assign(nruns, CarveRun{});
   uint8_t* base = S.mem.as<uint8_t>();
+  const int stage = carve_stage_dtab(rows, pitch, carve_warps(cols, cl)) ? 1 : 0;
   for (int r = 0; r < nruns; ++r) {
     uint8_t* p = base + per * r;
-    RunCarve& R = S.runs[r];
     auto take = [&](size_t bytes) {
       uint8_t* q = p;
       p += align256(bytes);
       return q;
     };
+    CarveRun& R = S.runs[r];
     R.rows = rows;
-    R.stride = cols;
+    R.pitch = pitch;
+    R.width0 = cols;
     R.target = target;
     R.kmax = kmax;
+    R.stage_dtab = stage;
     R.luma = take(plane);
     R.grad = take(plane);
     R.idx = reinterpret_cast<int16_t*>(take(plane * 2));
-    R.rem = reinterpret_cast<int16_t*>(take(plane * 2));
-    R.pw = reinterpret_cast<uint32_t*>(take((size_t)nblk * cols * 4));
-    R.delta = reinterpret_cast<int8_t*>(take((size_t)nblk * cols));
-    R.col_end = reinterpret_cast<int16_t*>(take((size_t)nblk * cols * 2));
-    R.lastce = reinterpret_cast<double*>(take((size_t)cols * 8));
+    R.pw = reinterpret_cast<uint32_t*>(take((size_t)nblk * pitch * 4));
+    R.delta = reinterpret_cast<int8_t*>(take((size_t)nblk * pitch));
+    R.lastce = reinterpret_cast<double*>(take((size_t)pitch * 8));
+    R.rem = reinterpret_cast<int16_t*>(take((size_t)rows * rem_cap * 2));
+    R.rem_cap = rem_cap;
+    R.alive = reinterpret_cast<uint32_t*>(take((size_t)rows * alive_pitch * 4));
+    R.alive_pitch = alive_pitch;
+    R.cend = reinterpret_cast<int16_t*>(take((size_t)nblk * pitch * 2));
+    R.prof = reinterpret_cast<long long*>(take(64));
     R.U = with_U ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
     if (dbg) {
-      R.dbg_costs = reinterpret_cast<double*>(take((size_t)cols * 8));
-      R.dbg_cols = reinterpret_cast<int16_t*>(take((size_t)cols * 2));
-      R.dbg_sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
+      R.sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
+      R.cols = reinterpret_cast<int16_t*>(take((size_t)cols * 2));
+      R.costs = reinterpret_cast<double*>(take((size_t)cols * 8));
     }
-    R.width = cols;
-    R.done = cols <= target;
   }
 }
 
-// run every carve in S to completion; on_iter(iteration) is called after each pass's
-// host sync when given (forces one pass per sync)
-template <class F>
-void carve_run_all(CarveSlab& S, cudaStream_t st, F&& on_iter, bool per_iter_sync) {
+// carve every run to its target in one persistent cluster launch; reads back iters/removed
+void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
   const int nruns = (int)S.runs.size();
-  if (nruns == 0) return;
-  S.runs_d = DBuf(sizeof(RunCarve) * nruns, st);
-  SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, S.runs.data(), sizeof(RunCarve) * nruns, cudaMemcpyHostToDevice, st));
-  RunCarve* rd = S.runs_d.as<RunCarve>();
-  bool any_U = false;
-  for (auto& R : S.runs) any_U |= R.U != nullptr;
-  int it = 0;
-  const int burst = per_iter_sync ? 1 : 8;
-  while (true) {
-    for (int k = 0; k < burst; ++k, ++it) {
-      launch_carve_gradient(rd, nruns, S.rows, S.stride, it == 0 ? 1 : 0, st);
-      if (it == 0 && any_U) launch_carve_dp(rd, nruns, true, S.stride, st);
-      launch_carve_dp(rd, nruns, false, S.stride, st);
-      launch_carve_select(rd, nruns, S.stride, S.rows, st);
-      launch_carve_compact(rd, nruns, S.rows, st);
+  if (nruns == 0 || S.cols <= S.target) return;
+  S.runs_d = DBuf(sizeof(CarveRun) * nruns, st);
+  SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, S.runs.data(), sizeof(CarveRun) * nruns, cudaMemcpyHostToDevice, st));
+  launch_carve_cluster(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st);
+  SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
+  SCPL_CUDA(cudaStreamSynchronize(st));
+  // per-phase SM cycles of the slowest run (the carve's critical path)
+  long long best = -1;
+  for (auto& R : S.runs) {
+    long long c[4];
+    SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
+    long long tot = c[0] + c[1] + c[2] + c[3];
+    if (tot > best) {
+      best = tot;
+      for (int k = 0; k < 4; ++k) S.prof[k] = c[k];
     }
-    SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(RunCarve) * nruns, cudaMemcpyDeviceToHost, st));
-    SCPL_CUDA(cudaStreamSynchronize(st));
-    if (per_iter_sync) on_iter(it - 1);
-    bool all = true;
-    for (auto& R : S.runs) all &= R.done != 0;
-    if (all) break;
   }
 }
 
@@ -365,35 +369,31 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
     SCPL_ARG(target >= 1, "target width must be >= 1");
     SCPL_ARG(target <= w, "target width exceeds frame width");
     SCPL_ARG(h >= 1 && w >= 1, "empty frame");
-    CarveSlab S;
-    carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, st);
-    RunCarve& R = S.runs[0];
-    launch_carve_setup_luma(frame, h, w, channels, 0, R.luma, R.idx, st);
-    if (energy) SCPL_CUDA(cudaMemcpyAsync(const_cast<double*>(R.U), energy, sizeof(double) * h * w,
-                                          cudaMemcpyDeviceToDevice, st));
-    int removed = 0;
-    std::vector<int16_t> rem;
-    carve_run_all(
-        S, st,
-        [&](int) {
-          if (!offsets) return;
-          const RunCarve& Rh = S.runs[0];
-          int b = Rh.b;
-          rem.resize((size_t)h * b);
-          SCPL_CUDA(cudaMemcpy(rem.data(), Rh.rem, sizeof(int16_t) * h * b, cudaMemcpyDeviceToHost));
-          for (int s = 0; s < b; ++s)
-            for (int i = 0; i < h; ++i) offsets[(size_t)(removed + s) * h + i] = rem[(size_t)i * b + s];
-          removed += b;
-        },
-        true);
-    const RunCarve& Rh = S.runs[0];
-    *n_batches = Rh.iters;
-    SCPL_CUDA(cudaMemcpyAsync(batch_sizes, Rh.dbg_sizes, sizeof(int) * Rh.iters, cudaMemcpyDeviceToHost, st));
-    SCPL_CUDA(cudaMemcpyAsync(batch_cols, Rh.dbg_cols, sizeof(int16_t) * Rh.nremoved, cudaMemcpyDeviceToHost, st));
-    SCPL_CUDA(
-        cudaMemcpyAsync(batch_costs, Rh.dbg_costs, sizeof(double) * Rh.nremoved, cudaMemcpyDeviceToHost, st));
-    SCPL_CUDA(cudaMemcpy2DAsync(index_out, sizeof(int16_t) * target, Rh.idx, sizeof(int16_t) * w,
+    CarveSet S;
+    carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, carve_cluster_size(1, w, ctx->num_sms), st);
+    CarveRun& R = S.runs[0];
+    launch_run_setup(frame, h, w, channels, 0, nullptr, R, st);
+    if (energy)
+      SCPL_CUDA(cudaMemcpy2DAsync(const_cast<double*>(R.U), sizeof(double) * R.pitch, energy, sizeof(double) * w,
+                                  sizeof(double) * w, h, cudaMemcpyDeviceToDevice, st));
+    carve_run_all(ctx, S, st);
+    const CarveRun& Rh = S.runs[0];
+    const int iters = w > target ? Rh.iters : 0, removed = w > target ? Rh.removed : 0;
+    *n_batches = iters;
+    if (iters) {
+      SCPL_CUDA(cudaMemcpyAsync(batch_sizes, Rh.sizes, sizeof(int) * iters, cudaMemcpyDeviceToHost, st));
+      SCPL_CUDA(cudaMemcpyAsync(batch_cols, Rh.cols, sizeof(int16_t) * removed, cudaMemcpyDeviceToHost, st));
+      SCPL_CUDA(cudaMemcpyAsync(batch_costs, Rh.costs, sizeof(double) * removed, cudaMemcpyDeviceToHost, st));
+    }
+    SCPL_CUDA(cudaMemcpy2DAsync(index_out, sizeof(int16_t) * target, Rh.idx, sizeof(int16_t) * Rh.pitch,
                                 sizeof(int16_t) * target, h, cudaMemcpyDeviceToDevice, st));
+    if (offsets && removed) {
+      std::vector<int16_t> log((size_t)h * Rh.rem_cap);
+      SCPL_CUDA(cudaMemcpyAsync(log.data(), Rh.rem, sizeof(int16_t) * log.size(), cudaMemcpyDeviceToHost, st));
+      SCPL_CUDA(cudaStreamSynchronize(st));
+      for (int s = 0; s < removed; ++s)
+        for (int i = 0; i < h; ++i) offsets[(size_t)s * h + i] = log[(size_t)i * Rh.rem_cap + s];
+    }
     SCPL_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -414,6 +414,8 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
     result->dp_passes = 0;
     result->n_runs = 0;
     for (float& x : result->phase_ms) x = 0.f;
+    for (long long& x : result->carve_cycles) x = 0;
+    result->carve_cluster = 0;
     if (T <= 0) return;
     const int C = channels;
     const int tw = P.target_width, th = P.target_height;
@@ -474,20 +476,27 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
       const int rows = height ? curW : curH, cols = height ? curH : curW;
       const int target = height ? th : tw;
       const bool with_U = (ph == 0) && P.mode != 0;
-      CarveSlab S;
-      carve_alloc(S, (int)runs.size(), rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false, st);
+      CarveSet S;
+      carve_alloc(S, (int)runs.size(), rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
+                  carve_cluster_size((int)runs.size(), cols, ctx->num_sms), st);
       const size_t fbytes = (size_t)curH * curW * C;
       for (size_t r = 0; r < runs.size(); ++r) {
-        RunCarve& R = S.runs[r];
-        launch_carve_setup_luma(cur + fbytes * runs[r].first, curH, curW, C, height ? 1 : 0, R.luma, R.idx, st);
+        CarveRun& R = S.runs[r];
+        // the first carved axis works on the original frames, whose energy codes carry the
+        // Sobel gradient of every frame (so the carve's gradient plane needs no recompute)
+        const uint16_t* fcodes = (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)runs[r].first * h * w
+                                                           : nullptr;
+        launch_run_setup(cur + fbytes * runs[r].first, curH, curW, C, height ? 1 : 0, fcodes, R, st);
         if (with_U)
           launch_uniform(codes.as<uint16_t>(), h, w, runs[r].first, runs[r].second, 1, P.w_motion, P.w_grad,
-                         height ? 1 : 0, const_cast<double*>(R.U), st);
+                         height ? 1 : 0, const_cast<double*>(R.U), st, R.pitch);
       }
       SCPL_CUDA(cudaEventRecord(ev[3], st));
-      carve_run_all(S, st, [](int) {}, false);
+      carve_run_all(ctx, S, st);
       SCPL_CUDA(cudaEventRecord(ev[4], st));
       for (auto& R : S.runs) dp += R.iters;
+      for (int k = 0; k < 4; ++k) result->carve_cycles[k] += S.prof[k];
+      result->carve_cluster = S.cl;
       const int nH = height ? th : curH, nW = height ? curW : tw;
       const bool last = ph + 1 == phases.size();
       DBuf next;
@@ -498,9 +507,9 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
       }
       const size_t obytes = (size_t)nH * nW * C;
       for (size_t r = 0; r < runs.size(); ++r) {
-        const RunCarve& R = S.runs[r];
+        const CarveRun& R = S.runs[r];
         launch_replay(cur + fbytes * runs[r].first, dst + obytes * runs[r].first, runs[r].second, curH, curW, C,
-                      R.idx, R.stride, target, height ? 1 : 0, st);
+                      R.idx, R.pitch, target, height ? 1 : 0, st);
       }
       SCPL_CUDA(cudaEventRecord(ev[2], st));
       SCPL_CUDA(cudaEventSynchronize(ev[2]));

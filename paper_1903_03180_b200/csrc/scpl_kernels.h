@@ -28,43 +28,39 @@ void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int 
                          int L, int first_pure, int init, double wm, double wg, double* ckS, double* ckQ,
                          double* leafsum, const PwVnode* vnodes, double* asde_out, cudaStream_t st);
 void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
-                    int transposed, double* out, cudaStream_t st);
+                    int transposed, double* out, cudaStream_t st, int pitch = 0);
 
-// ------------------------------------------------------------------ carve state (one per run)
-// Carve orientation: `rows` x `cols` where a vertical seam removes one column per row
-// (for a height phase the planes are the transposed frame).  Planes have row stride
-// `stride` (= the initial cols).
-struct RunCarve {
-  // static
-  int rows, stride, target;
+// ------------------------------------------------------------------ carve v2 (scpl_carve2.cu)
+// One run's carve state; planes are rows x pitch (pitch >= width0, multiple of 16).
+struct CarveRun {
+  int rows, pitch, width0, target;
   int kmax;             // 0 = SCPL batch (k = remaining), 1 = raw (one min seam per pass)
-  const double* U;      // fp64 energy for the first pass, or nullptr (gradient from the start)
-  uint8_t* luma;        // rows x stride, compacted in place
-  uint8_t* grad;        // rows x stride, gradient of the compacted luma
-  int16_t* idx;         // rows x stride, original column of each current column
-  uint32_t* pw;         // nblk x stride path words at block-end rows
-  int8_t* delta;        // nblk x stride landing delta of each block-end column
-  int16_t* col_end;     // nblk x stride block-end column of each last-row column's path
-  int16_t* rem;         // rows x stride removed columns of the current batch (row-major, b per row)
-  double* lastce;       // stride
-  double* dbg_costs;    // optional: per batch costs (sum over batches <= stride) or nullptr
-  int16_t* dbg_cols;    // optional: per batch last-row columns
-  int* dbg_sizes;       // optional: per batch size
-  // dynamic
-  int width;            // current width
-  int iters;            // DP passes done
-  int b;                // size of the current batch
-  int done;
-  int nremoved;         // total removed so far (offset into dbg arrays)
+  int stage_dtab;       // stage the landing-delta table in shared memory (set by the launcher)
+  const double* U;      // fp64 energy of the first pass, or nullptr (gradient from the start)
+  uint8_t* luma;        // compacted in place
+  uint8_t* grad;        // gradient of the compacted luma (incrementally maintained)
+  int16_t* idx;         // output: original column of each kept column (rows x pitch)
+  uint32_t* alive;      // rows x alive_pitch bitmask of surviving original columns
+  int alive_pitch;
+  int16_t* cend;        // nblk x pitch scratch: block-end columns of the selected seams
+  long long* prof;      // optional: SM cycles in dp / select / compact / gradient
+  uint32_t* pw;         // nblk x pitch path words at block-end rows
+  int8_t* delta;        // nblk x pitch landing deltas
+  double* lastce;       // pitch
+  int16_t* rem;         // rows x rem_cap: removed columns of every batch, in that batch's coordinates
+  int rem_cap;          // >= width0 - target
+  int* sizes;           // optional per-batch sizes (capacity width0)
+  int16_t* cols;        // optional per-seam last-row column (capacity width0)
+  double* costs;        // optional per-seam cost
+  // results
+  int iters, removed;
 };
-
-void launch_carve_gradient(RunCarve* runs, int nruns, int max_rows, int max_stride, int first_iter,
-                           cudaStream_t st);
-void launch_carve_dp(RunCarve* runs, int nruns, bool fp64, int max_stride, cudaStream_t st);
-void launch_carve_select(RunCarve* runs, int nruns, int max_stride, int max_rows, cudaStream_t st);
-void launch_carve_compact(RunCarve* runs, int nruns, int max_rows, cudaStream_t st);
-void launch_carve_setup_luma(const uint8_t* frame, int H, int W, int C, int transposed, uint8_t* luma,
-                             int16_t* idx, cudaStream_t st);
+void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes,
+                      const CarveRun& R, cudaStream_t st);
+int carve_cluster_size(int nruns, int width, int num_sms);
+void launch_carve_cluster(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st);
+bool carve_stage_dtab(int rows, int pitch, int warps);
+int carve_warps(int width, int cl);
 
 void launch_replay(const uint8_t* in, uint8_t* out, int T, int H, int W, int C, const int16_t* idx, int stride,
                    int tw, int transposed, cudaStream_t st);

@@ -212,7 +212,7 @@ void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int 
 // frames, divided by T (equal to np.stack(maps).mean(axis=0) bit for bit).  Written in
 // the carve orientation (transposed for a height phase) with a 32x32 smem tile.
 __global__ void uniform_kernel(const uint16_t* __restrict__ codes, int H, int W, int s, int n, int first_pure,
-                               double wm, double wg, int transposed, double* __restrict__ out) {
+                               double wm, double wg, int transposed, double* __restrict__ out, int pitch) {
   __shared__ double A[256], B[256];
   __shared__ double tile[32][33];
   for (int k = threadIdx.y * 32 + threadIdx.x; k < 256; k += 256) {
@@ -231,7 +231,7 @@ __global__ void uniform_kernel(const uint16_t* __restrict__ codes, int H, int W,
       acc = energy_of(codes[(size_t)s * N + p], first_pure && s == 0, A, B);
       for (int t = s + 1; t < s + n; ++t) acc = __dadd_rn(acc, energy_of(codes[(size_t)t * N + p], false, A, B));
       acc = __ddiv_rn(acc, dn);
-      if (!transposed) out[p] = acc;
+      if (!transposed) out[(long)i * pitch + j] = acc;
     }
     tile[r][threadIdx.x] = acc;
   }
@@ -240,14 +240,15 @@ __global__ void uniform_kernel(const uint16_t* __restrict__ codes, int H, int W,
   // out is (W, H): out[j][i]
   for (int r = threadIdx.y; r < 32; r += 8) {
     int j = j0 + r, i = i0 + threadIdx.x;
-    if (i < H && j < W) out[(long)j * H + i] = tile[threadIdx.x][r];
+    if (i < H && j < W) out[(long)j * pitch + i] = tile[threadIdx.x][r];
   }
 }
 
 void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
-                    int transposed, double* out, cudaStream_t st) {
+                    int transposed, double* out, cudaStream_t st, int pitch) {
+  if (pitch <= 0) pitch = transposed ? H : W;
   dim3 grid(cdiv(W, 32), cdiv(H, 32));
-  uniform_kernel<<<grid, dim3(32, 8), 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, transposed, out);
+  uniform_kernel<<<grid, dim3(32, 8), 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, transposed, out, pitch);
   SCPL_CHECK_LAUNCH();
 }
 

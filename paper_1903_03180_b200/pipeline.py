@@ -114,6 +114,9 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int):
     runs = [(starts[i], lens[i]) for i in range(res.n_runs)]
     global last_phase_ms
     last_phase_ms = dict(zip(("codes", "scan", "carve", "replay"), (float(x) for x in res.phase_ms)))
+    last_phase_ms.update({f"carve_{k}_Mcyc": c / 1e6 for k, c in zip(("dp", "select", "compact", "grad"),
+                                                                      res.carve_cycles)})
+    last_phase_ms["carve_cluster"] = res.carve_cluster
     return out, int(res.dp_passes), runs
 
 
