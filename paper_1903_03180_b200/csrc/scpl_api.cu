@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -189,7 +191,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   const size_t plane = (size_t)rows * pitch;
   size_t per = align256(plane) * 2 + align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
                align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
-               align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(64) +
+               align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(128) +
                (with_U ? align256(plane * 8) : 0) +
                (dbg ? align256((size_t)cols * 4) + align256((size_t)cols * 2) + align256((size_t)cols * 8) : 0);
   S.mem = DBuf(per * nruns, st);
@@ -200,7 +202,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   S.cl = cl;
   S.runs.assign(nruns, CarveRun{});
   uint8_t* base = S.mem.as<uint8_t>();
-  const int stage = carve_stage_dtab(rows, pitch, carve_warps(cols, cl)) ? 1 : 0;
+  const int stage = carve_stage_dtab(rows, pitch, cl) ? 1 : 0;
   for (int r = 0; r < nruns; ++r) {
     uint8_t* p = base + per * r;
     auto take = [&](size_t bytes) {
@@ -226,7 +228,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.alive = reinterpret_cast<uint32_t*>(take((size_t)rows * alive_pitch * 4));
     R.alive_pitch = alive_pitch;
     R.cend = reinterpret_cast<int16_t*>(take((size_t)nblk * pitch * 2));
-    R.prof = reinterpret_cast<long long*>(take(64));
+    R.prof = reinterpret_cast<long long*>(take(128));
     R.U = with_U ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
     if (dbg) {
       R.sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
@@ -248,8 +250,9 @@ void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
   // per-phase SM cycles of the slowest run (the carve's critical path)
   long long best = -1;
   for (auto& R : S.runs) {
-    long long c[4];
+    long long c[12];
     SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
+    if (getenv("SCPL_PROF")) fprintf(stderr, "carve prof: iters %d rows %d | dp %lld sel %lld comp %lld grad %lld | xwait %lld ringwait %lld xblock-total %lld | warp1 %lld %lld %lld\n", R.iters, R.rows, c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[8], c[9], c[10]);
     long long tot = c[0] + c[1] + c[2] + c[3];
     if (tot > best) {
       best = tot;

@@ -37,10 +37,11 @@
 
 namespace scpl {
 
-constexpr int kLanesCols = 4;                     // columns per lane in a warp window
-constexpr int kWin = 32 * kLanesCols;             // 128-column window
-constexpr int kHalo = kBlockRows;                 // 16 = rows per exchange
-constexpr int kOwn = kWin - 2 * kHalo;            // 96 owned columns per warp
+constexpr int kC = 6;                             // columns per lane in a DP warp window
+constexpr int kWin = 32 * kC;                     // 192-column window
+constexpr int kXRows = 32;                        // rows between boundary exchanges (= halo)
+constexpr int kOwn = kWin - 2 * kXRows;           // 128 owned columns per DP warp
+constexpr int kDpWarps = 4;                       // DP warps per CTA: one per SM sub-partition
 constexpr int kIntInf = 0x3fffffff;
 constexpr int kMaxWarps = 16;                    // 512 threads: <= 128 registers per thread
 
@@ -62,6 +63,28 @@ __device__ __forceinline__ void st_cluster(uint32_t addr, int v) {
 }
 __device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+// neighbour exchange barriers: release/acquire at cluster scope, local or remote arrive
+__device__ __forceinline__ void mbar_arrive_cluster_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(map_rank(bar, rank))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITX_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITX_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ DP value traits
@@ -89,62 +112,88 @@ struct Geo {  // per-pass column ownership
   int win_lo;          // first window column of this warp (own_lo - 16)
 };
 
-// raw energy of one lane's 4 window columns in row i: int path = one 32-bit word of the
-// u8 gradient plane, fp64 path = 4 doubles of the uniform map.  Columns outside [0, w) are
-// masked by the caller; only in-row addresses are touched.
-__device__ __forceinline__ uint32_t load_e_int(const CarveRun& R, int i, int j0, int w) {
-  if (j0 < 0 || j0 >= w) return 0u;
-  return __ldg(reinterpret_cast<const uint32_t*>(R.grad + (long)i * R.pitch + j0));
-}
-__device__ __forceinline__ void load_e_f64(const CarveRun& R, int i, int j0, int w, double (&e)[kLanesCols]) {
-  const double* row = R.U + (long)i * R.pitch;
-  if (j0 >= 0 && j0 + 3 < w) {
-    double2 a = __ldg(reinterpret_cast<const double2*>(row + j0));
-    double2 b = __ldg(reinterpret_cast<const double2*>(row + j0 + 2));
-    e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
-  } else {
-#pragma unroll
-    for (int k = 0; k < kLanesCols; ++k) e[k] = (j0 + k >= 0 && j0 + k < w) ? row[j0 + k] : 0.0;
-  }
-}
-
+// ------------------------------------------------------------------ DP (v3)
+// Window layout: a DP warp owns kOwn = 128 columns and computes a 192-column window
+// (owned +- 32), 6 contiguous columns per lane, for kXRows = 32 rows between exchanges.
+// Energy rows reach shared memory through TMA bulk copies (one 1-D copy per window row,
+// issued by lane 0 a stage ahead); async-proxy copies do not hold back the release of the
+// block-boundary exchange, and the lanes read them with plain LDS.
 template <bool F64>
-struct ERow;
+struct DpCfg;
 template <>
-struct ERow<false> {
-  uint32_t v;
-  __device__ __forceinline__ void load(const CarveRun& R, int i, int j0, int w) { v = load_e_int(R, i, j0, w); }
-  __device__ __forceinline__ int get(int k) const { return (int)((v >> (8 * k)) & 255u); }
+struct DpCfg<false> {
+  static constexpr int kStageRows = 32, kStages = 2;  // a whole exchange block in flight
 };
 template <>
-struct ERow<true> {
-  double v[kLanesCols];
-  __device__ __forceinline__ void load(const CarveRun& R, int i, int j0, int w) { load_e_f64(R, i, j0, w, v); }
-  __device__ __forceinline__ double get(int k) const { return v[k]; }
+struct DpCfg<true> {
+  static constexpr int kStageRows = 4, kStages = 6;   // fp64 rows are 8x larger: finer ring
 };
-
-// one DP row for a lane's 4 columns (seams.py:54-64): strict '<' in the order -1, 0, +1
 template <bool F64>
-__device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kLanesCols], uint32_t (&pw)[kLanesCols],
-                                       const ERow<F64>& e, const bool (&in)[kLanesCols], int lane) {
+__host__ __device__ constexpr size_t dp_ring_bytes() {
+  return (size_t)DpCfg<F64>::kStages * DpCfg<F64>::kStageRows * kWin * (F64 ? 8 : 1);
+}
+
+// issue stage `st` (rows 1 + st*RS ...) of this warp's energy window into ring slot st % S
+template <bool F64>
+__device__ __forceinline__ void dp_issue_stage(const CarveRun& R, int st, int win_lo, uint8_t* ring,
+                                               uint64_t* bars) {
+  constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
+  constexpr int sz = F64 ? 8 : 1;
+  const int slot = st % S;
+  const int i0 = 1 + st * RS;
+  const int nrow = min(RS, R.rows - i0);
+  if (nrow <= 0) return;
+  const int c0 = max(win_lo, 0);
+  const int c1 = min(win_lo + kWin, R.pitch);
+  const uint32_t bytes = (uint32_t)((c1 - c0) * sz);
+  const uint8_t* base = F64 ? reinterpret_cast<const uint8_t*>(R.U) : R.grad;
+  uint8_t* dst0 = ring + (size_t)slot * RS * kWin * sz + (size_t)(c0 - win_lo) * sz;
+  fence_proxy_async_global();
+  mbar_arrive_tx(&bars[slot], bytes * nrow);
+  for (int r = 0; r < nrow; ++r)
+    bulk_g2s(dst0 + (size_t)r * kWin * sz, base + ((size_t)(i0 + r) * R.pitch + c0) * sz, bytes, &bars[slot]);
+}
+
+// one DP row for a lane's kC columns (seams.py:54-64): strict '<' in the order -1, 0, +1
+template <bool F64, bool EDGE>
+__device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t (&pw)[kC],
+                                       const uint8_t* erow, const bool (&in)[kC], int lane) {
   using V = Val<F64>;
   using T = typename V::T;
-  T left = __shfl_up_sync(0xffffffffu, ce[kLanesCols - 1], 1);
+  T e[kC];
+  if constexpr (F64) {
+    const double2* p = reinterpret_cast<const double2*>(erow) + lane * (kC / 2);
+#pragma unroll
+    for (int q = 0; q < kC / 2; ++q) {
+      double2 v = p[q];
+      e[2 * q] = v.x;
+      e[2 * q + 1] = v.y;
+    }
+  } else {
+    const uint16_t* p = reinterpret_cast<const uint16_t*>(erow) + lane * (kC / 2);
+#pragma unroll
+    for (int q = 0; q < kC / 2; ++q) {
+      uint32_t v = p[q];
+      e[2 * q] = (int)(v & 255u);
+      e[2 * q + 1] = (int)(v >> 8);
+    }
+  }
+  T left = __shfl_up_sync(0xffffffffu, ce[kC - 1], 1);
   T right = __shfl_down_sync(0xffffffffu, ce[0], 1);
-  uint32_t pleft = __shfl_up_sync(0xffffffffu, pw[kLanesCols - 1], 1);
+  uint32_t pleft = __shfl_up_sync(0xffffffffu, pw[kC - 1], 1);
   uint32_t pright = __shfl_down_sync(0xffffffffu, pw[0], 1);
   if (lane == 0) left = V::inf();
   if (lane == 31) right = V::inf();
-  T nce[kLanesCols];
-  uint32_t npw[kLanesCols];
+  T nce[kC];
+  uint32_t npw[kC];
 #pragma unroll
-  for (int k = 0; k < kLanesCols; ++k) {
+  for (int k = 0; k < kC; ++k) {
     T l = k > 0 ? ce[k - 1] : left;
     T c = ce[k];
-    T r = k + 1 < kLanesCols ? ce[k + 1] : right;
+    T r = k + 1 < kC ? ce[k + 1] : right;
     uint32_t pl = k > 0 ? pw[k - 1] : pleft;
     uint32_t pc = pw[k];
-    uint32_t pr = k + 1 < kLanesCols ? pw[k + 1] : pright;
+    uint32_t pr = k + 1 < kC ? pw[k + 1] : pright;
     bool p1 = c < l;
     T m = p1 ? c : l;
     uint32_t ps = p1 ? pc : pl;
@@ -153,104 +202,185 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kLanesCols], u
     m = p2 ? r : m;
     ps = p2 ? pr : ps;
     code = p2 ? 2u : code;
-    nce[k] = in[k] ? V::add((T)e.get(k), m) : V::inf();
+    T v = V::add(e[k], m);
+    nce[k] = (!EDGE || in[k]) ? v : V::inf();
     npw[k] = (ps << 2) | code;
   }
 #pragma unroll
-  for (int k = 0; k < kLanesCols; ++k) {
+  for (int k = 0; k < kC; ++k) {
     ce[k] = nce[k];
     pw[k] = npw[k];
   }
 }
 
-// One DP pass over all rows for this warp's window. ceX: smem exchange rows [2][pitch].
-template <bool F64>
-__device__ void dp_pass(const CarveRun& R, const Geo& g, typename Val<F64>::T* ceX, int CL, uint32_t rank,
-                        int per_cta) {
+// One DP pass for this warp's window.  ceX: smem exchange rows [2][pitch]; ring: this
+// warp's energy ring; bars: its S ring mbarriers (phase bits in rph); xbar/xc: the
+// neighbour-exchange barriers and exchange counter (buffer = xc & 1, parity = (xc>>1) & 1).
+// Exchange blocks of 32 rows: when every CTA owns >= 32 columns only adjacent CTAs supply
+// halo and each CTA waits on its own mbarrier for its warps plus the adjacent CTAs' warps
+// (release/acquire at cluster scope).  Tiny widths fall back to a cluster barrier.
+template <bool F64, bool EDGE>
+__device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* ceX, int CL, uint32_t rank,
+                        int per_cta, uint64_t* xbar, uint32_t& xc, uint8_t* ring, uint64_t* bars, uint32_t& rph,
+                        bool dp_warp, long long* dprof) {
   using V = Val<F64>;
   using T = typename V::T;
-  constexpr int PF = F64 ? 4 : kBlockRows;  // rows of energy in flight
+  constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
+  constexpr int sz = F64 ? 8 : 1;
+  static_assert(kXRows % RS == 0 && kBlockRows % RS == 0 || RS == kXRows, "stage layout");
   const int lane = threadIdx.x & 31;
   const int rows = R.rows, w = g.w;
-  const bool active = g.own_lo < g.own_hi;
-  const int j0 = g.win_lo + lane * kLanesCols;
-  T ce[kLanesCols];
-  uint32_t pw[kLanesCols];
-  bool in[kLanesCols];
+  const bool active = dp_warp && g.own_lo < g.own_hi;
+  const int j0 = g.win_lo + lane * kC;
+  const bool nb_mode = per_cta >= kXRows;
+  T ce[kC];
+  uint32_t pw[kC];
+  bool in[kC];
 #pragma unroll
-  for (int k = 0; k < kLanesCols; ++k) in[k] = (j0 + k >= 0) && (j0 + k < w);
-  ERow<F64> ring[PF];
+  for (int k = 0; k < kC; ++k) in[k] = (j0 + k >= 0) && (j0 + k < w);
+  const int nstage = (rows - 1 + RS - 1) / RS;
+  int issued = 0;  // stages issued so far (lane 0's view; uniform enough for the loop below)
   if (active) {
-    ERow<F64> e0;
-    e0.load(R, 0, j0, w);
 #pragma unroll
-    for (int k = 0; k < kLanesCols; ++k) ce[k] = in[k] ? (T)e0.get(k) : V::inf();
-#pragma unroll
-    for (int q = 0; q < PF; ++q)
-      if (1 + q < rows) ring[q].load(R, 1 + q, j0, w);
+    for (int k = 0; k < kC; ++k) {
+      T v;
+      if constexpr (F64)
+        v = in[k] ? R.U[j0 + k] : 0.0;
+      else
+        v = in[k] ? (int)R.grad[j0 + k] : 0;
+      ce[k] = in[k] ? v : V::inf();
+    }
+    issued = min(S - 1, nstage);
+    if (lane == 0)
+      for (int st = 0; st < issued; ++st) dp_issue_stage<F64>(R, st, g.win_lo, ring, bars);
   }
-  const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
-  for (int blk = 0; blk < nblk; ++blk) {
-    const int i0 = 1 + blk * kBlockRows;
-    const int nr = min(kBlockRows, rows - i0);
+  // wait for stage st (issuing the one S-1 ahead first) and return its ring rows
+  auto stage_rows = [&](int st) -> const uint8_t* {
+    __syncwarp();
+    if (lane == 0 && st + S - 1 < nstage) dp_issue_stage<F64>(R, st + S - 1, g.win_lo, ring, bars);
+    const int slot = st % S;
+    long long tq = clock64();
+    mbar_wait(&bars[slot], (rph >> slot) & 1u);
+    __syncwarp();  // reconverge after the per-lane wait loop: the row shuffles need a converged warp
+    dprof[1] += clock64() - tq;
+    rph ^= 1u << slot;
+    return ring + (size_t)slot * RS * kWin * sz;
+  };
+  const int nx = (rows - 1 + kXRows - 1) / kXRows;
+  for (int xb = 0; xb < nx; ++xb) {
+    long long tx = clock64();
+    if (xb > 0 && nb_mode) {
+      const uint32_t e = xc - 1;
+      mbar_wait_cluster(&xbar[e & 1], (e >> 1) & 1);
+    }
+    __syncwarp();
+    dprof[0] += clock64() - tx;
     if (active) {
-      if (blk > 0) {
-        const T* src = ceX + (size_t)((blk - 1) & 1) * R.pitch;
+      if (xb > 0) {
+        const T* src = ceX + (size_t)((xc - 1) & 1) * R.pitch;
 #pragma unroll
-        for (int k = 0; k < kLanesCols; ++k) ce[k] = in[k] ? src[j0 + k] : V::inf();
+        for (int k = 0; k < kC; ++k) ce[k] = in[k] ? src[j0 + k] : V::inf();
       }
+      const uint8_t* stage = nullptr;
+      if constexpr (RS == kXRows) stage = stage_rows(xb);
+#pragma unroll 1
+      for (int pb = 0; pb < kXRows / kBlockRows; ++pb) {
+        const int i0 = 1 + xb * kXRows + pb * kBlockRows;
+        const int nr = min(kBlockRows, rows - i0);
+        if (nr <= 0) break;
 #pragma unroll
-      for (int k = 0; k < kLanesCols; ++k) pw[k] = 0u;
-      if constexpr (F64) {
+        for (int k = 0; k < kC; ++k) pw[k] = 0u;  // path words restart every 16 rows
+        if (nr == kBlockRows) {
 #pragma unroll
-        for (int r = 0; r < kBlockRows; ++r) {
-          if (r < nr) {
-            ERow<true> e = ring[r % PF];
-            if (i0 + r + PF < rows) ring[r % PF].load(R, i0 + r + PF, j0, w);
-            dp_row<true>(ce, pw, e, in, lane);
+          for (int r = 0; r < kBlockRows; ++r) {
+            const uint8_t* erow;
+            if constexpr (RS == kXRows) {
+              erow = stage + (size_t)(pb * kBlockRows + r) * kWin * sz;
+            } else {
+              if (r % RS == 0) stage = stage_rows((i0 - 1) / RS + r / RS);
+              erow = stage + (size_t)(r % RS) * kWin * sz;
+            }
+            dp_row<F64, EDGE>(ce, pw, erow, in, lane);
+          }
+        } else {
+#pragma unroll 1
+          for (int r = 0; r < nr; ++r) {
+            const int i = i0 + r;
+            const uint8_t* erow;
+            if constexpr (RS == kXRows) {
+              erow = stage + (size_t)(pb * kBlockRows + r) * kWin * sz;
+            } else {
+              if ((i - 1) % RS == 0) stage = stage_rows((i - 1) / RS);
+              erow = stage + (size_t)((i - 1) % RS) * kWin * sz;
+            }
+            dp_row<F64, EDGE>(ce, pw, erow, in, lane);
           }
         }
-      } else {
-        ERow<false> cur[kBlockRows];
+        // path-word block end: owned words and landing deltas (read after the pass)
+        const int pbi = (i0 - 1) / kBlockRows;
 #pragma unroll
-        for (int r = 0; r < kBlockRows; ++r) cur[r] = ring[r];
-        // next block's energy rows in flight while this block computes
-#pragma unroll
-        for (int r = 0; r < kBlockRows; ++r)
-          if (i0 + kBlockRows + r < rows) ring[r].load(R, i0 + kBlockRows + r, j0, w);
-#pragma unroll
-        for (int r = 0; r < kBlockRows; ++r)
-          if (r < nr) dp_row<false>(ce, pw, cur[r], in, lane);
+        for (int k = 0; k < kC; ++k) {
+          int j = j0 + k;
+          if (j >= g.own_lo && j < g.own_hi) {
+            int sum = __popc(pw[k] & 0x55555555u) + 2 * __popc(pw[k] & 0xAAAAAAAAu);
+            R.pw[(long)pbi * R.pitch + j] = pw[k];
+            R.delta[(long)pbi * R.pitch + j] = (int8_t)(sum - nr);
+          }
+        }
       }
-      // block end: owned columns publish path words, landing deltas and ce
-      T* dst = ceX + (size_t)(blk & 1) * R.pitch;
+      dprof[2] += clock64() - tx;  // waits + rows of this exchange block
+      // exchange-block end: owned ce to this CTA's buffer, halo to the adjacent CTAs
+      T* dst = ceX + (size_t)(xc & 1) * R.pitch;
 #pragma unroll
-      for (int k = 0; k < kLanesCols; ++k) {
+      for (int k = 0; k < kC; ++k) {
         int j = j0 + k;
         if (j >= g.own_lo && j < g.own_hi) {
-          int sum = __popc(pw[k] & 0x55555555u) + 2 * __popc(pw[k] & 0xAAAAAAAAu);
-          R.pw[(long)blk * R.pitch + j] = pw[k];
-          R.delta[(long)blk * R.pitch + j] = (int8_t)(sum - nr);
           dst[j] = ce[k];
-          // halo for every other CTA whose warps' windows reach column j
-          for (int q = 0; q < CL; ++q) {
-            if (q == (int)rank) continue;
-            int lo = min(w, q * per_cta), hi = min(w, lo + per_cta);
-            if (lo < hi && j >= lo - kHalo && j < hi + kHalo) st_cluster(map_rank(&dst[j], q), ce[k]);
+          if (nb_mode) {
+            if (rank > 0 && j < g.cta_lo + kXRows) st_cluster(map_rank(&dst[j], rank - 1), ce[k]);
+            if ((int)rank + 1 < CL && j >= g.cta_hi - kXRows) st_cluster(map_rank(&dst[j], rank + 1), ce[k]);
+          } else {
+            for (int q = 0; q < CL; ++q) {
+              if (q == (int)rank) continue;
+              int lo = min(w, q * per_cta), hi = min(w, lo + per_cta);
+              if (lo < hi && j >= lo - kXRows && j < hi + kXRows) st_cluster(map_rank(&dst[j], q), ce[k]);
+            }
           }
         }
       }
     }
-    cluster_sync();
+    if (nb_mode) {
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cluster_local(&xbar[xc & 1]);
+        if (rank > 0) mbar_arrive_cluster_remote(&xbar[xc & 1], rank - 1);
+        if ((int)rank + 1 < CL) mbar_arrive_cluster_remote(&xbar[xc & 1], rank + 1);
+      }
+    } else {
+      cluster_sync();
+    }
+    ++xc;
   }
-  // last row
   if (active) {
 #pragma unroll
-    for (int k = 0; k < kLanesCols; ++k) {
+    for (int k = 0; k < kC; ++k) {
       int j = j0 + k;
       if (j >= g.own_lo && j < g.own_hi) R.lastce[j] = V::to_d(ce[k]);
     }
   }
+  (void)issued;
+}
+
+template <bool F64>
+__device__ void dp_pass(const CarveRun& R, const Geo& g, typename Val<F64>::T* ceX, int CL, uint32_t rank,
+                        int per_cta, uint64_t* xbar, uint32_t& xc, uint8_t* ring, uint64_t* bars, uint32_t& rph,
+                        bool dp_warp, long long* dprof) {
+  // interior windows skip the per-column range masks
+  const bool edge = g.win_lo < 0 || g.win_lo + kWin > g.w;
+  if (__any_sync(0xffffffffu, edge))
+    dp_rows<F64, true>(R, g, ceX, CL, rank, per_cta, xbar, xc, ring, bars, rph, dp_warp, dprof);
+  else
+    dp_rows<F64, false>(R, g, ceX, CL, rank, per_cta, xbar, xc, ring, bars, rph, dp_warp, dprof);
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -291,10 +421,6 @@ struct SelSmem {
   int8_t* dtab;    // staged delta table [nblk][pitch] (or nullptr: chain in global)
 };
 
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
 // warp-inclusive scan of v over lanes
 __device__ __forceinline__ int warp_incl_scan(int v) {
   const int lane = threadIdx.x & 31;
@@ -309,6 +435,8 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 // Alive-column bitmask of one row (nw32 words, <= 32*kMaxAliveWordsPerLane): the lanes hold
 // words m = lane + 32u; wv/pre (per-warp smem) receive the words and exclusive popcounts.
 constexpr int kMaxAliveWordsPerLane = 4;  // widths up to 4096
+constexpr int kListCap = 192;             // per-warp staged removal-list entries per row
+constexpr int kWarpScratch = 1024 + 3 * kListCap * 2;  // wv + pre + three row lists
 __device__ __forceinline__ void alive_row_prefix(const uint32_t* row, int nw32, uint32_t* wv, int* pre) {
   const int lane = threadIdx.x & 31;
   int running = 0;
@@ -337,10 +465,12 @@ __device__ __forceinline__ int alive_select(const uint32_t* wv, const int* pre, 
   return lo * 32 + (int)__fns(wv[lo], 0, c - pre[lo] + 1);
 }
 
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveRun* __restrict__ runs, int CL) {
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveRun* __restrict__ runs, int CL, int ncw) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int ws[32];
   __shared__ __align__(8) uint64_t s_bar[kMaxWarps * 2];
+  __shared__ __align__(8) uint64_t s_xbar[2];
+  __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
   const uint32_t rank = cluster_rank();
   CarveRun& Rg = runs[blockIdx.x / CL];
   const CarveRun R = Rg;  // static fields in registers
@@ -354,6 +484,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
   int w = R.width0;
   int iters = 0, removed = 0;
   long long prof[4] = {0, 0, 0, 0};
+  long long dprof[3] = {0, 0, 0};
+
   long long tp = clock64();
 
   // all columns alive; per-warp mbarriers for the staged compaction
@@ -365,8 +497,18 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
   if (lane == 0) {
     mbar_init(&s_bar[2 * wid], 1);
     mbar_init(&s_bar[2 * wid + 1], 1);
-    fence_mbar_init();
   }
+  // DP warps own 128 columns each; the ring buffers exist for the first ndp warps
+  const int ndp = min(kMaxWarps, (((R.width0 + CL - 1) / CL + 15) / 16 * 16 + kOwn - 1) / kOwn);
+  if (tid == 0) {  // every DP warp of this CTA and of the adjacent CTAs arrives per exchange
+    const int nadj = (rank > 0 ? 1 : 0) + ((int)rank + 1 < CL ? 1 : 0);
+    mbar_init(&s_xbar[0], (uint32_t)(ndp * (1 + nadj)));
+    mbar_init(&s_xbar[1], (uint32_t)(ndp * (1 + nadj)));
+  }
+  if (lane == 0)
+    for (int k = 0; k < 6; ++k) mbar_init(&s_rbar[wid * 6 + k], 1);
+  if (lane == 0) fence_mbar_init();
+  uint32_t xc = 0, rph = 0;
   uint32_t phase[2] = {0u, 0u};
   cluster_sync();
 
@@ -374,16 +516,30 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
     // ---------------- 1. DP
     Geo g;
     g.w = w;
-    const int per = ((w + CL - 1) / CL + 3) & ~3;
+    const int per = ((w + CL - 1) / CL + 15) & ~15;
     g.cta_lo = min(w, (int)rank * per);
     g.cta_hi = min(w, g.cta_lo + per);
     g.own_lo = g.cta_lo + wid * kOwn;
     g.own_hi = min(g.cta_hi, g.own_lo + kOwn);
-    g.win_lo = g.own_lo - kHalo;
-    if (iters == 0 && R.U != nullptr)
-      dp_pass<true>(R, g, reinterpret_cast<double*>(smem), CL, rank, per);
+    g.win_lo = g.own_lo - kXRows;
+    // warps outside the DP go straight to the cluster barrier -- unless the pass falls back
+    // to cluster barriers per exchange (tiny widths), which every thread must join
+    const bool in_dp = wid < ndp || per < kXRows;
+    if (in_dp) {
+      uint8_t* ring = smem + 2 * sizeof(double) * (size_t)pitch;
+      if (iters == 0 && R.U != nullptr)
+        dp_pass<true>(R, g, reinterpret_cast<double*>(smem), CL, rank, per, s_xbar, xc,
+                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, wid < ndp, dprof);
+      else
+        dp_pass<false>(R, g, reinterpret_cast<int*>(smem), CL, rank, per, s_xbar, xc,
+                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, wid < ndp, dprof);
+    }
+    // warps outside the DP park on a named barrier (descheduled, no issue slots taken)
+    // until the DP warps are done; then everyone joins the cluster barrier
+    if (in_dp)
+      asm volatile("bar.arrive 1, %0;" ::"r"(blockDim.x) : "memory");
     else
-      dp_pass<false>(R, g, reinterpret_cast<int*>(smem), CL, rank, per);
+      asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
     cluster_sync();  // lastce / pw / delta of all CTAs visible
     if (tid == 0) { long long t = clock64(); prof[0] += t - tp; tp = t; }
 
@@ -540,7 +696,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
     const int w0 = w;
     const int wn = w - b;
     {
-      uint8_t* wbuf = smem + (size_t)wid * (4 * RB + 1024);
+      uint8_t* wbuf = smem + (size_t)wid * (4 * RB + kWarpScratch);
       uint32_t* wv = reinterpret_cast<uint32_t*>(wbuf + 4 * RB);
       int* pre = reinterpret_cast<int*>(wbuf + 4 * RB + 512);
       const uint32_t nbytes = (uint32_t)((w0 + 15) & ~15);
@@ -553,17 +709,24 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
         }
       };
       int kk = 0;
-      if (rlo + wid < rhi) issue(rlo + wid, 0);
-      for (int i = rlo + wid; i < rhi; i += nw, ++kk) {
+      if (wid < ncw && rlo + wid < rhi) issue(rlo + wid, 0);
+      for (int i = rlo + wid; wid < ncw && i < rhi; i += ncw, ++kk) {
         const int slot = kk & 1;
-        if (i + nw < rhi) issue(i + nw, slot ^ 1);
+        if (i + ncw < rhi) issue(i + ncw, slot ^ 1);
         mbar_wait(&s_bar[2 * wid + slot], phase[slot]);
         phase[slot] ^= 1u;
         const uint8_t* Ls = wbuf + (size_t)slot * 2 * RB;
         const uint8_t* Gs = Ls + RB;
         uint32_t* Lg = reinterpret_cast<uint32_t*>(R.luma + (long)i * pitch);
         uint32_t* Gg = reinterpret_cast<uint32_t*>(R.grad + (long)i * pitch);
-        const int16_t* rr = log + (long)i * R.rem_cap + removed;  // sorted, old coordinates
+        const int16_t* rg = log + (long)i * R.rem_cap + removed;  // sorted, old coordinates
+        int16_t* lst = reinterpret_cast<int16_t*>(wbuf + 4 * RB + 1024);
+        const int16_t* rr = rg;
+        if (b <= kListCap) {  // stage the list: the walk below is a dependent chain
+          for (int t = lane; t < b; t += 32) lst[t] = rg[t];
+          __syncwarp();
+          rr = lst;
+        }
         // output byte y reads input byte y + #{t : rr[t] - t <= y}
         int tptr = 0;  // warp-uniform: entries with rr[t]-t < chunk start
         const int nwo = (wn + 3) >> 2;
@@ -625,14 +788,28 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
     // ---------------- 4. incremental gradient (batching.py:110-115 on the carved frame)
     if (wn > R.target) {
       const bool zero = rows < 3 || wn < 3;
-      for (int i = rlo + wid; i < rhi; i += nw) {
+      for (int i = rlo + wid; wid < ncw && i < rhi; i += ncw) {
         uint8_t* gr = R.grad + (long)i * pitch;
         if (zero) {
           for (int y = lane; y < wn; y += 32) gr[y] = 0;
           continue;
         }
-        const int16_t* ri = log + (long)i * R.rem_cap + removed;  // row i's removed (sorted)
         const int ia = max(i - 1, 0), ib = min(i + 1, rows - 1);
+        // rows {i-1, i, i+1}'s removed columns (sorted), staged per warp when they fit
+        const int16_t* l3[3] = {log + (long)ia * R.rem_cap + removed, log + (long)i * R.rem_cap + removed,
+                                log + (long)ib * R.rem_cap + removed};
+        if (b <= kListCap) {
+          int16_t* lst = reinterpret_cast<int16_t*>(smem + (size_t)wid * (4 * RB + kWarpScratch) + 4 * RB + 1024);
+          for (int t = lane; t < 3 * b; t += 32) {
+            int rs = t / b;
+            lst[rs * kListCap + (t - rs * b)] = l3[rs][t - rs * b];
+          }
+          __syncwarp();
+          l3[0] = lst;
+          l3[1] = lst + kListCap;
+          l3[2] = lst + 2 * kListCap;
+        }
+        const int16_t* ri = l3[1];
         const uint8_t* la = R.luma + (long)ia * pitch;
         const uint8_t* lb = R.luma + (long)i * pitch;
         const uint8_t* lc = R.luma + (long)ib * pitch;
@@ -641,8 +818,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
         for (int q = lane; q < ncand; q += 32) {
           int rsel = q / (3 * b), rem = q - rsel * 3 * b;
           int s = rem / 3, off = rem - s * 3 - 1;
-          int r = rsel == 0 ? ia : (rsel == 1 ? i : ib);
-          int x = log[(long)r * R.rem_cap + removed + s] + off;
+          int x = l3[rsel][s] + off;
           if (x < 0 || x >= w0) continue;
           int lo = 0, hi = b;  // number of row-i removed columns < x
           while (lo < hi) {
@@ -657,6 +833,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
           int gv = abs(gx) + abs(gy);
           gr[y] = (uint8_t)(gv > 255 ? 255 : gv);
         }
+        __syncwarp();  // the staged lists are reused by the next row
       }
     }
     removed += b;
@@ -668,10 +845,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
 
   // final index map (original column of every kept column) from the alive bitmask
   {
-    uint8_t* wbuf = smem + (size_t)wid * (4 * RB + 1024);
+    uint8_t* wbuf = smem + (size_t)wid * (4 * RB + kWarpScratch);
     uint32_t* wv = reinterpret_cast<uint32_t*>(wbuf + 4 * RB);
     int* pre = reinterpret_cast<int*>(wbuf + 4 * RB + 512);
-    for (int i = rlo + wid; i < rhi; i += nw) {
+    for (int i = rlo + wid; wid < ncw && i < rhi; i += ncw) {
       alive_row_prefix(R.alive + (long)i * R.alive_pitch, nw32, wv, pre);
       int16_t* ir = R.idx + (long)i * pitch;
       for (int m = lane; m < nw32; m += 32) {
@@ -686,11 +863,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
       __syncwarp();
     }
   }
+  if (rank == 0 && tid == 32 && R.prof)
+    for (int k = 0; k < 3; ++k) R.prof[8 + k] = dprof[k];
   if (rank == 0 && tid == 0) {
     Rg.iters = iters;
     Rg.removed = removed;
-    if (R.prof)
+    if (R.prof) {
       for (int k = 0; k < 4; ++k) R.prof[k] = prof[k];
+      for (int k = 0; k < 3; ++k) R.prof[4 + k] = dprof[k];
+
+    }
   }
 }
 
@@ -766,39 +948,53 @@ void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed,
 }
 
 int carve_cluster_size(int nruns, int width, int num_sms) {
-  int cl = 1;
-  while (cl < 8 && (long)nruns * cl * 2 <= num_sms) cl <<= 1;  // one cluster per run, all resident
-  while ((long)kOwn * kMaxWarps * cl < width && cl < 8) cl <<= 1;  // <= kMaxWarps warps per CTA
-  return cl;
+  // one DP warp per SM sub-partition: kDpWarps x 128 columns per CTA, at most 8 CTAs
+  int cl = (width + kOwn * kDpWarps - 1) / (kOwn * kDpWarps);
+  return cl < 1 ? 1 : (cl > 8 ? 8 : cl);
 }
 
-size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps) {
+int carve_dp_warps(int width, int cl) {
+  const int per = ((width + cl - 1) / cl + 15) & ~15;
+  return (per + kOwn - 1) / kOwn;
+}
+
+constexpr size_t kSmemBudget = 220 * 1024;
+
+// warps that stage rows for the compaction / gradient phases (4 staged rows each)
+int carve_comp_warps(int pitch) {
+  const size_t RB = (((size_t)pitch + 15) & ~(size_t)15) + 16;
+  size_t n = kSmemBudget / (4 * RB + kWarpScratch);
+  return (int)(n > (size_t)kMaxWarps ? kMaxWarps : n);
+}
+
+size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps) {
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
-  size_t dp = 2 * sizeof(double) * (size_t)pitch;
+  size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * dp_ring_bytes<true>();
   size_t sel = (size_t)pitch * (8 + 8 + 4 * 4) + 16;
   if (stage) sel += (size_t)nblk * pitch;
   const size_t RB = (((size_t)pitch + 15) & ~(size_t)15) + 16;
-  size_t comp = (size_t)warps * (4 * RB + 1024);
+  size_t comp = (size_t)warps * (4 * RB + kWarpScratch);
   size_t m = dp > sel ? dp : sel;
   return m > comp ? m : comp;
 }
 
-int carve_warps(int width, int cl) {
-  const int per_cta = (((width + cl - 1) / cl) + 3) & ~3;
-  int warps = (per_cta + kOwn - 1) / kOwn;
-  return warps < 4 ? 4 : warps;
-}
+int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
 
-bool carve_stage_dtab(int rows, int pitch, int warps) {
-  return carve_smem_bytes(rows, pitch, true, warps) <= 220 * 1024;
+bool carve_stage_dtab(int rows, int pitch, int cl) {
+  return carve_smem_bytes(rows, pitch, true, carve_comp_warps(pitch), carve_dp_warps(pitch, cl)) <= kSmemBudget;
 }
 
 void launch_carve_cluster(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st) {
   if (nruns == 0) return;
-  const int warps = carve_warps(width, cl);
-  SCPL_ARG(warps <= kMaxWarps, "carve width too large for the cluster size");
-  const bool stage = carve_stage_dtab(rows, pitch, warps);
-  size_t smem = carve_smem_bytes(rows, pitch, stage, warps);
+  // the DP needs carve_dp_warps() warps (128 owned columns each); the row-parallel phases
+  // use every warp, so the CTA always runs kMaxWarps (DP-idle warps skip the DP)
+  const int dpw = carve_dp_warps(width, cl);
+  SCPL_ARG(dpw <= kMaxWarps, "carve width too large for the cluster size");
+  const int warps = kMaxWarps;
+  const int ncw = carve_comp_warps(pitch);
+  SCPL_ARG(ncw >= 1, "carve plane too wide for the compaction stage");
+  const bool stage = carve_stage_dtab(rows, pitch, cl);
+  size_t smem = carve_smem_bytes(rows, pitch, stage, ncw, dpw);
   SCPL_ARG(smem <= 227 * 1024, "carve plane too large for shared memory");
   SCPL_CUDA(cudaFuncSetAttribute(carve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
@@ -813,7 +1009,7 @@ void launch_carve_cluster(CarveRun* runs_d, int nruns, int rows, int pitch, int 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_cluster_kernel, runs_d, cl));
+  SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_cluster_kernel, runs_d, cl, ncw));
   SCPL_CHECK_LAUNCH();
 }
 

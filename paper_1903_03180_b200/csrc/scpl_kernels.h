@@ -59,7 +59,7 @@ void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed,
                       const CarveRun& R, cudaStream_t st);
 int carve_cluster_size(int nruns, int width, int num_sms);
 void launch_carve_cluster(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st);
-bool carve_stage_dtab(int rows, int pitch, int warps);
+bool carve_stage_dtab(int rows, int pitch, int cl);
 int carve_warps(int width, int cl);
 
 void launch_replay(const uint8_t* in, uint8_t* out, int T, int H, int W, int C, const int16_t* idx, int stride,
