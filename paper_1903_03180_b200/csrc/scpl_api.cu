@@ -189,11 +189,11 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   const int rem_cap = std::max(1, cols - target);
   const int alive_pitch = ((cols + 31) / 32 + 3) & ~3;
   const size_t plane = (size_t)rows * pitch;
-  size_t per = align256(plane) * 2 + align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
+  size_t per = align256(plane) * 4 + align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
                align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
-               align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(128) +
-               (with_U ? align256(plane * 8) : 0) +
-               (dbg ? align256((size_t)cols * 4) + align256((size_t)cols * 2) + align256((size_t)cols * 8) : 0);
+               align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(256) +
+               (with_U ? align256(plane * 8) : 0) + align256((size_t)cols * 4) +
+               (dbg ? align256((size_t)cols * 2) + align256((size_t)cols * 8) : 0);
   S.mem = DBuf(per * nruns, st);
   S.rows = rows;
   S.cols = cols;
@@ -217,8 +217,11 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.target = target;
     R.kmax = kmax;
     R.stage_dtab = stage;
-    R.luma = take(plane);
-    R.grad = take(plane);
+    R.luma[0] = take(plane);
+    R.luma[1] = take(plane);
+    R.grad[0] = take(plane);
+    R.grad[1] = take(plane);
+    R.width = cols;
     R.idx = reinterpret_cast<int16_t*>(take(plane * 2));
     R.pw = reinterpret_cast<uint32_t*>(take((size_t)nblk * pitch * 4));
     R.delta = reinterpret_cast<int8_t*>(take((size_t)nblk * pitch));
@@ -228,32 +231,48 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.alive = reinterpret_cast<uint32_t*>(take((size_t)rows * alive_pitch * 4));
     R.alive_pitch = alive_pitch;
     R.cend = reinterpret_cast<int16_t*>(take((size_t)nblk * pitch * 2));
-    R.prof = reinterpret_cast<long long*>(take(128));
+    R.prof = reinterpret_cast<long long*>(take(256));
     R.U = with_U ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
+    R.sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
     if (dbg) {
-      R.sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
       R.cols = reinterpret_cast<int16_t*>(take((size_t)cols * 2));
       R.costs = reinterpret_cast<double*>(take((size_t)cols * 8));
     }
+    encode_carve_tensor_maps(R);
   }
 }
 
-// carve every run to its target in one persistent cluster launch; reads back iters/removed
+// carve every run to its target: per iteration one cluster pass (DP + select + trace) and
+// the row kernels (compaction, gradient update); the host checks completion every 8 passes
 void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
+  (void)ctx;
   const int nruns = (int)S.runs.size();
-  if (nruns == 0 || S.cols <= S.target) return;
+  if (nruns == 0) return;
+  for (auto& R : S.runs) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, 256, st));
   S.runs_d = DBuf(sizeof(CarveRun) * nruns, st);
   SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, S.runs.data(), sizeof(CarveRun) * nruns, cudaMemcpyHostToDevice, st));
-  launch_carve_cluster(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st);
+  if (S.cols > S.target) {
+    while (true) {
+      for (int k = 0; k < 8; ++k)
+        launch_carve_iteration(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st);
+      SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
+      SCPL_CUDA(cudaStreamSynchronize(st));
+      bool all = true;
+      for (auto& R : S.runs) all &= R.width <= R.target;
+      if (all) break;
+    }
+  }
+  launch_carve_index(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
   SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
   SCPL_CUDA(cudaStreamSynchronize(st));
-  // per-phase SM cycles of the slowest run (the carve's critical path)
   long long best = -1;
   for (auto& R : S.runs) {
     long long c[12];
     SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
-    if (getenv("SCPL_PROF")) fprintf(stderr, "carve prof: iters %d rows %d | dp %lld sel %lld comp %lld grad %lld | xwait %lld ringwait %lld xblock-total %lld | warp1 %lld %lld %lld\n", R.iters, R.rows, c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[8], c[9], c[10]);
-    long long tot = c[0] + c[1] + c[2] + c[3];
+    if (getenv("SCPL_PROF"))
+      fprintf(stderr, "carve prof: iters %d rows %d | dp %lld sel %lld | xwait %lld ringwait %lld rows %lld publish %lld\n",
+              R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7]);
+    long long tot = c[0] + c[1];
     if (tot > best) {
       best = tot;
       for (int k = 0; k < 4; ++k) S.prof[k] = c[k];

@@ -29,6 +29,8 @@
 //     batch's columns in place (warp per row, 32-column chunks left to right).
 //  4. Gradient, row-split and incremental: a pixel's Sobel value changes only if a removed
 //     pixel of rows i-1..i+1 lay within one column of it; only those are recomputed.
+#include <cudaTypedefs.h>
+
 #include <cfloat>
 #include <climits>
 
@@ -42,8 +44,9 @@ constexpr int kWin = 32 * kC;                     // 192-column window
 constexpr int kXRows = 32;                        // rows between boundary exchanges (= halo)
 constexpr int kOwn = kWin - 2 * kXRows;           // 128 owned columns per DP warp
 constexpr int kDpWarps = 4;                       // DP warps per CTA: one per SM sub-partition
+constexpr int kRingW = kWin + 16;                 // ring row: a 16-aligned superset of the window
 constexpr int kIntInf = 0x3fffffff;
-constexpr int kMaxWarps = 16;                    // 512 threads: <= 128 registers per thread
+constexpr int kMaxWarps = 12;                    // 384 threads: up to 168 registers per thread
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -58,11 +61,33 @@ __device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
   return out;
 }
+// remote store that completes 4/8 bytes on the target CTA's mbarrier (no fence needed)
+__device__ __forceinline__ void st_async_remote(const int* local_dst, int v, uint64_t* local_bar, uint32_t rank) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   map_rank(local_dst, rank)),
+               "r"(v), "r"(map_rank(local_bar, rank))
+               : "memory");
+}
+__device__ __forceinline__ void st_async_remote(const double* local_dst, double v, uint64_t* local_bar,
+                                                uint32_t rank) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                   map_rank(local_dst, rank)),
+               "l"(__double_as_longlong(v)), "r"(map_rank(local_bar, rank))
+               : "memory");
+}
 __device__ __forceinline__ void st_cluster(uint32_t addr, int v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // neighbour exchange barriers: release/acquire at cluster scope, local or remote arrive
@@ -130,28 +155,24 @@ struct DpCfg<true> {
 };
 template <bool F64>
 __host__ __device__ constexpr size_t dp_ring_bytes() {
-  return (size_t)DpCfg<F64>::kStages * DpCfg<F64>::kStageRows * kWin * (F64 ? 8 : 1);
+  return (size_t)DpCfg<F64>::kStages * DpCfg<F64>::kStageRows * kRingW * (F64 ? 8 : 1);
 }
 
-// issue stage `st` (rows 1 + st*RS ...) of this warp's energy window into ring slot st % S
+// issue stage `st` (rows 1 + st*RS ...) of this warp's energy window into ring slot st % S:
+// one 2-D TMA box (kRingW columns from the 16-aligned column at or below the window start,
+// RS rows); out-of-range columns and rows land as 0
 template <bool F64>
-__device__ __forceinline__ void dp_issue_stage(const CarveRun& R, int st, int win_lo, uint8_t* ring,
-                                               uint64_t* bars) {
+__device__ __forceinline__ void dp_issue_stage(const CarveRun& Rg, int plane, int rows, int st, int win_lo,
+                                               uint8_t* ring, uint64_t* bars) {
   constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
   constexpr int sz = F64 ? 8 : 1;
   const int slot = st % S;
   const int i0 = 1 + st * RS;
-  const int nrow = min(RS, R.rows - i0);
-  if (nrow <= 0) return;
-  const int c0 = max(win_lo, 0);
-  const int c1 = min(win_lo + kWin, R.pitch);
-  const uint32_t bytes = (uint32_t)((c1 - c0) * sz);
-  const uint8_t* base = F64 ? reinterpret_cast<const uint8_t*>(R.U) : R.grad;
-  uint8_t* dst0 = ring + (size_t)slot * RS * kWin * sz + (size_t)(c0 - win_lo) * sz;
+  if (i0 >= rows) return;
   fence_proxy_async_global();
-  mbar_arrive_tx(&bars[slot], bytes * nrow);
-  for (int r = 0; r < nrow; ++r)
-    bulk_g2s(dst0 + (size_t)r * kWin * sz, base + ((size_t)(i0 + r) * R.pitch + c0) * sz, bytes, &bars[slot]);
+  mbar_arrive_tx(&bars[slot], (uint32_t)(RS * kRingW * sz));
+  tma_load_2d(ring + (size_t)slot * RS * kRingW * sz, F64 ? &Rg.tm_U : &Rg.tm_grad[plane], win_lo & ~15, i0,
+              &bars[slot]);
 }
 
 // one DP row for a lane's kC columns (seams.py:54-64): strict '<' in the order -1, 0, +1
@@ -162,21 +183,13 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t 
   using T = typename V::T;
   T e[kC];
   if constexpr (F64) {
-    const double2* p = reinterpret_cast<const double2*>(erow) + lane * (kC / 2);
+    const double* p = reinterpret_cast<const double*>(erow) + lane * kC;
 #pragma unroll
-    for (int q = 0; q < kC / 2; ++q) {
-      double2 v = p[q];
-      e[2 * q] = v.x;
-      e[2 * q + 1] = v.y;
-    }
+    for (int k = 0; k < kC; ++k) e[k] = p[k];
   } else {
-    const uint16_t* p = reinterpret_cast<const uint16_t*>(erow) + lane * (kC / 2);
+    const uint8_t* p = erow + lane * kC;
 #pragma unroll
-    for (int q = 0; q < kC / 2; ++q) {
-      uint32_t v = p[q];
-      e[2 * q] = (int)(v & 255u);
-      e[2 * q + 1] = (int)(v >> 8);
-    }
+    for (int k = 0; k < kC; ++k) e[k] = (int)p[k];
   }
   T left = __shfl_up_sync(0xffffffffu, ce[kC - 1], 1);
   T right = __shfl_down_sync(0xffffffffu, ce[0], 1);
@@ -219,10 +232,25 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t 
 // Exchange blocks of 32 rows: when every CTA owns >= 32 columns only adjacent CTAs supply
 // halo and each CTA waits on its own mbarrier for its warps plus the adjacent CTAs' warps
 // (release/acquire at cluster scope).  Tiny widths fall back to a cluster barrier.
+// halo bytes a CTA receives per exchange at width w: the adjacent CTAs' owned columns
+// within 32 of its own range (only adjacent CTAs reach when every CTA owns >= 32 columns)
+__device__ __forceinline__ uint32_t halo_bytes_for(int w, int CL, uint32_t rank, int sz) {
+  const int per = ((w + CL - 1) / CL + 15) & ~15;
+  const int lo_me = min(w, (int)rank * per), hi_me = min(w, lo_me + per);
+  uint32_t bytes = 0;
+  for (int q = (int)rank - 1; q <= (int)rank + 1; q += 2) {
+    if (q < 0 || q >= CL) continue;
+    int lo = min(w, q * per), hi = min(w, lo + per);
+    int a = max(lo, lo_me - kXRows), b = min(hi, hi_me + kXRows);
+    if (b > a) bytes += (uint32_t)((b - a) * sz);
+  }
+  return bytes;
+}
+
 template <bool F64, bool EDGE>
-__device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* ceX, int CL, uint32_t rank,
-                        int per_cta, uint64_t* xbar, uint32_t& xc, uint8_t* ring, uint64_t* bars, uint32_t& rph,
-                        bool dp_warp, long long* dprof) {
+__device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
+                        uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
+                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof) {
   using V = Val<F64>;
   using T = typename V::T;
   constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
@@ -230,7 +258,7 @@ __device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* c
   static_assert(kXRows % RS == 0 && kBlockRows % RS == 0 || RS == kXRows, "stage layout");
   const int lane = threadIdx.x & 31;
   const int rows = R.rows, w = g.w;
-  const bool active = dp_warp && g.own_lo < g.own_hi;
+  const bool active = g.own_lo < g.own_hi;
   const int j0 = g.win_lo + lane * kC;
   const bool nb_mode = per_cta >= kXRows;
   T ce[kC];
@@ -239,7 +267,6 @@ __device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* c
 #pragma unroll
   for (int k = 0; k < kC; ++k) in[k] = (j0 + k >= 0) && (j0 + k < w);
   const int nstage = (rows - 1 + RS - 1) / RS;
-  int issued = 0;  // stages issued so far (lane 0's view; uniform enough for the loop below)
   if (active) {
 #pragma unroll
     for (int k = 0; k < kC; ++k) {
@@ -247,33 +274,51 @@ __device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* c
       if constexpr (F64)
         v = in[k] ? R.U[j0 + k] : 0.0;
       else
-        v = in[k] ? (int)R.grad[j0 + k] : 0;
+        v = in[k] ? (int)R.grad[plane][j0 + k] : 0;
       ce[k] = in[k] ? v : V::inf();
     }
-    issued = min(S - 1, nstage);
     if (lane == 0)
-      for (int st = 0; st < issued; ++st) dp_issue_stage<F64>(R, st, g.win_lo, ring, bars);
+      for (int st = 0; st < S - 1 && st < nstage; ++st) dp_issue_stage<F64>(Rg, plane, rows, st, g.win_lo, ring, bars);
   }
+  // Exchange protocol (nb_mode): a CTA announces the bytes of exchange e on its barrier
+  // before it sends its own data of exchange e-1 (end of block e-1) -- or, for a pass's
+  // first exchange, before the cluster barrier that precedes the pass -- so complete_tx
+  // from a neighbour can never precede the matching expect_tx.
+  const uint32_t halo_bytes = nb_mode ? halo_bytes_for(w, CL, rank, (int)sizeof(T)) : 0u;
   // wait for stage st (issuing the one S-1 ahead first) and return its ring rows
   auto stage_rows = [&](int st) -> const uint8_t* {
     __syncwarp();
-    if (lane == 0 && st + S - 1 < nstage) dp_issue_stage<F64>(R, st + S - 1, g.win_lo, ring, bars);
+    if (lane == 0 && st + S - 1 < nstage) dp_issue_stage<F64>(Rg, plane, rows, st + S - 1, g.win_lo, ring, bars);
     const int slot = st % S;
     long long tq = clock64();
     mbar_wait(&bars[slot], (rph >> slot) & 1u);
-    __syncwarp();  // reconverge after the per-lane wait loop: the row shuffles need a converged warp
+    __syncwarp();
     dprof[1] += clock64() - tq;
     rph ^= 1u << slot;
-    return ring + (size_t)slot * RS * kWin * sz;
+    return ring + ((size_t)slot * RS * kRingW + (g.win_lo & 15)) * sz;
   };
+  auto store_pw = [&](int pbi, int nrb) {
+#pragma unroll
+    for (int k = 0; k < kC; ++k) {
+      int j = j0 + k;
+      if (j >= g.own_lo && j < g.own_hi) {
+        int sum = __popc(pw[k] & 0x55555555u) + 2 * __popc(pw[k] & 0xAAAAAAAAu);
+        R.pw[(long)pbi * R.pitch + j] = pw[k];
+        R.delta[(long)pbi * R.pitch + j] = (int8_t)(sum - nrb);
+      }
+    }
+  };
+  int last_pbi = -1, last_nr = 0;
   const int nx = (rows - 1 + kXRows - 1) / kXRows;
   for (int xb = 0; xb < nx; ++xb) {
     long long tx = clock64();
-    if (xb > 0 && nb_mode) {
-      const uint32_t e = xc - 1;
-      mbar_wait_cluster(&xbar[e & 1], (e >> 1) & 1);
+    if (nb_mode) {
+      if (xb > 0) {  // halo of the previous exchange landed (st.async completion)
+        const uint32_t e = xm - 1;
+        mbar_wait(&xbar[e & 1], (e >> 1) & 1);
+        __syncwarp();
+      }
     }
-    __syncwarp();
     dprof[0] += clock64() - tx;
     if (active) {
       if (xb > 0) {
@@ -291,16 +336,18 @@ __device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* c
 #pragma unroll
         for (int k = 0; k < kC; ++k) pw[k] = 0u;  // path words restart every 16 rows
         if (nr == kBlockRows) {
-#pragma unroll
-          for (int r = 0; r < kBlockRows; ++r) {
-            const uint8_t* erow;
+          // 4 rows unrolled per step: short enough for the instruction cache
+#pragma unroll 1
+          for (int r4 = 0; r4 < kBlockRows; r4 += 4) {
+            const uint8_t* ebase;
             if constexpr (RS == kXRows) {
-              erow = stage + (size_t)(pb * kBlockRows + r) * kWin * sz;
+              ebase = stage + (size_t)(pb * kBlockRows + r4) * kRingW * sz;
             } else {
-              if (r % RS == 0) stage = stage_rows((i0 - 1) / RS + r / RS);
-              erow = stage + (size_t)(r % RS) * kWin * sz;
+              static_assert(RS == 4, "fp64 stages hold 4 rows");
+              ebase = stage_rows((i0 - 1 + r4) / RS);
             }
-            dp_row<F64, EDGE>(ce, pw, erow, in, lane);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) dp_row<F64, EDGE>(ce, pw, ebase + (size_t)r * kRingW * sz, in, lane);
           }
         } else {
 #pragma unroll 1
@@ -308,37 +355,44 @@ __device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* c
             const int i = i0 + r;
             const uint8_t* erow;
             if constexpr (RS == kXRows) {
-              erow = stage + (size_t)(pb * kBlockRows + r) * kWin * sz;
+              erow = stage + (size_t)(pb * kBlockRows + r) * kRingW * sz;
             } else {
               if ((i - 1) % RS == 0) stage = stage_rows((i - 1) / RS);
-              erow = stage + (size_t)((i - 1) % RS) * kWin * sz;
+              erow = stage + (size_t)((i - 1) % RS) * kRingW * sz;
             }
             dp_row<F64, EDGE>(ce, pw, erow, in, lane);
           }
         }
-        // path-word block end: owned words and landing deltas (read after the pass)
-        const int pbi = (i0 - 1) / kBlockRows;
-#pragma unroll
-        for (int k = 0; k < kC; ++k) {
-          int j = j0 + k;
-          if (j >= g.own_lo && j < g.own_hi) {
-            int sum = __popc(pw[k] & 0x55555555u) + 2 * __popc(pw[k] & 0xAAAAAAAAu);
-            R.pw[(long)pbi * R.pitch + j] = pw[k];
-            R.delta[(long)pbi * R.pitch + j] = (int8_t)(sum - nr);
-          }
-        }
+        // path-word block end: owned words and landing deltas (read after the pass); the
+        // exchange block's last one is stored after the exchange below
+        last_pbi = (i0 - 1) / kBlockRows;
+        last_nr = nr;
+        if (pb + 1 < kXRows / kBlockRows && i0 + nr < rows) store_pw(last_pbi, last_nr);
       }
-      dprof[2] += clock64() - tx;  // waits + rows of this exchange block
-      // exchange-block end: owned ce to this CTA's buffer, halo to the adjacent CTAs
+      dprof[2] += clock64() - tx;
+      tx = clock64();
+    }
+    // announce the next exchange's bytes, then let the block's data go out (the named
+    // barrier orders the announcement before every local warp's sends)
+    if (nb_mode) {
+      if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
+      asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");
+    }
+    if (active) {
+      // exchange-block end: owned ce into this CTA's buffer; halo columns straight into the
+      // adjacent CTAs' buffers with st.async, completing bytes on their exchange barrier
       T* dst = ceX + (size_t)(xc & 1) * R.pitch;
+
 #pragma unroll
       for (int k = 0; k < kC; ++k) {
         int j = j0 + k;
         if (j >= g.own_lo && j < g.own_hi) {
           dst[j] = ce[k];
           if (nb_mode) {
-            if (rank > 0 && j < g.cta_lo + kXRows) st_cluster(map_rank(&dst[j], rank - 1), ce[k]);
-            if ((int)rank + 1 < CL && j >= g.cta_hi - kXRows) st_cluster(map_rank(&dst[j], rank + 1), ce[k]);
+            if (rank > 0 && j < g.cta_lo + kXRows)
+              st_async_remote(&dst[j], ce[k], &xbar[xm & 1], rank - 1);
+            if ((int)rank + 1 < CL && j >= g.cta_hi - kXRows)
+              st_async_remote(&dst[j], ce[k], &xbar[xm & 1], rank + 1);
           } else {
             for (int q = 0; q < CL; ++q) {
               if (q == (int)rank) continue;
@@ -349,17 +403,22 @@ __device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* c
         }
       }
     }
-    if (nb_mode) {
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster_local(&xbar[xc & 1]);
-        if (rank > 0) mbar_arrive_cluster_remote(&xbar[xc & 1], rank - 1);
-        if ((int)rank + 1 < CL) mbar_arrive_cluster_remote(&xbar[xc & 1], rank + 1);
-      }
-    } else {
+    if (nb_mode)
+      asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");  // this CTA's DP warps' values
+    else
       cluster_sync();
+    if (active && last_pbi >= 0) {
+      store_pw(last_pbi, last_nr);
+      last_pbi = -1;
     }
+    if (active) dprof[3] += clock64() - tx;
     ++xc;
+    if (nb_mode) ++xm;
+  }
+  if (nb_mode && nx > 0) {  // the last exchange must be complete before the smem is reused
+    const uint32_t e = xm - 1;
+    mbar_wait(&xbar[e & 1], (e >> 1) & 1);
+    __syncwarp();
   }
   if (active) {
 #pragma unroll
@@ -368,19 +427,17 @@ __device__ void dp_rows(const CarveRun& R, const Geo& g, typename Val<F64>::T* c
       if (j >= g.own_lo && j < g.own_hi) R.lastce[j] = V::to_d(ce[k]);
     }
   }
-  (void)issued;
 }
 
 template <bool F64>
-__device__ void dp_pass(const CarveRun& R, const Geo& g, typename Val<F64>::T* ceX, int CL, uint32_t rank,
-                        int per_cta, uint64_t* xbar, uint32_t& xc, uint8_t* ring, uint64_t* bars, uint32_t& rph,
-                        bool dp_warp, long long* dprof) {
-  // interior windows skip the per-column range masks
-  const bool edge = g.win_lo < 0 || g.win_lo + kWin > g.w;
-  if (__any_sync(0xffffffffu, edge))
-    dp_rows<F64, true>(R, g, ceX, CL, rank, per_cta, xbar, xc, ring, bars, rph, dp_warp, dprof);
+__device__ void dp_pass(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
+                        uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
+                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof) {
+  // windows lie inside [0, w) unless the plane is narrower than one window
+  if (g.w < kWin)
+    dp_rows<F64, true>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof);
   else
-    dp_rows<F64, false>(R, g, ceX, CL, rank, per_cta, xbar, xc, ring, bars, rph, dp_warp, dprof);
+    dp_rows<F64, false>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof);
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -436,7 +493,7 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 // words m = lane + 32u; wv/pre (per-warp smem) receive the words and exclusive popcounts.
 constexpr int kMaxAliveWordsPerLane = 4;  // widths up to 4096
 constexpr int kListCap = 192;             // per-warp staged removal-list entries per row
-constexpr int kWarpScratch = 1024 + 3 * kListCap * 2;  // wv + pre + three row lists
+constexpr int kWarpScratch = 1024 + 4096;  // wv + pre + (shift table | three staged row lists)
 __device__ __forceinline__ void alive_row_prefix(const uint32_t* row, int nw32, uint32_t* wv, int* pre) {
   const int lane = threadIdx.x & 31;
   int running = 0;
@@ -465,83 +522,70 @@ __device__ __forceinline__ int alive_select(const uint32_t* wv, const int* pre, 
   return lo * 32 + (int)__fns(wv[lo], 0, c - pre[lo] + 1);
 }
 
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveRun* __restrict__ runs, int CL, int ncw) {
+// One DP pass + select + trace for every active run (one cluster per run).  Per-run state
+// (width, iters, removed) is read at entry and written back at exit; the gradient plane of
+// this pass is the ping-pong plane `iters & 1`.
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun* __restrict__ runs, int CL) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int ws[32];
-  __shared__ __align__(8) uint64_t s_bar[kMaxWarps * 2];
   __shared__ __align__(8) uint64_t s_xbar[2];
   __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
   const uint32_t rank = cluster_rank();
   CarveRun& Rg = runs[blockIdx.x / CL];
-  const CarveRun R = Rg;  // static fields in registers
+  const CarveRun R = Rg;  // state at entry (written back only after the final cluster barrier)
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int w = R.width, iters = R.iters, removed = R.removed;
+  if (w <= R.target) {  // done: nothing this iteration
+    if (rank == 0 && tid == 0) Rg.b = 0;
+    return;
+  }
   const int rows = R.rows, pitch = R.pitch;
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  const int nw32 = (R.width0 + 31) >> 5;
-  const int rlo = (int)((long)rows * rank / CL), rhi = (int)((long)rows * (rank + 1) / CL);
   const bool stage_dtab = R.stage_dtab != 0;
-  const int RB = ((pitch + 15) & ~15) + 16;  // staged row bytes (compaction)
-  int w = R.width0;
-  int iters = 0, removed = 0;
-  long long prof[4] = {0, 0, 0, 0};
-  long long dprof[3] = {0, 0, 0};
-
+  const int plane = iters & 1;
+  long long dprof[4] = {0, 0, 0, 0};
   long long tp = clock64();
 
-  // all columns alive; per-warp mbarriers for the staged compaction
-  for (int i = rlo + wid; i < rhi; i += nw)
-    for (int m = lane; m < nw32; m += 32) {
-      int hi = R.width0 - 32 * m;
-      R.alive[(long)i * R.alive_pitch + m] = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
-    }
-  if (lane == 0) {
-    mbar_init(&s_bar[2 * wid], 1);
-    mbar_init(&s_bar[2 * wid + 1], 1);
-  }
-  // DP warps own 128 columns each; the ring buffers exist for the first ndp warps
-  const int ndp = min(kMaxWarps, (((R.width0 + CL - 1) / CL + 15) / 16 * 16 + kOwn - 1) / kOwn);
-  if (tid == 0) {  // every DP warp of this CTA and of the adjacent CTAs arrives per exchange
-    const int nadj = (rank > 0 ? 1 : 0) + ((int)rank + 1 < CL ? 1 : 0);
-    mbar_init(&s_xbar[0], (uint32_t)(ndp * (1 + nadj)));
-    mbar_init(&s_xbar[1], (uint32_t)(ndp * (1 + nadj)));
+  const int per = ((w + CL - 1) / CL + 15) & ~15;
+  const int ndp = min(kMaxWarps, (per + kOwn - 1) / kOwn);
+  const bool fp64 = iters == 0 && R.U != nullptr;
+  if (tid == 0) {
+    mbar_init(&s_xbar[0], 1);
+    mbar_init(&s_xbar[1], 1);
+    if (rows > 1 && per >= kXRows)  // the pass's first exchange, announced before it can start
+      mbar_arrive_tx(&s_xbar[0], halo_bytes_for(w, CL, rank, fp64 ? 8 : 4));
   }
   if (lane == 0)
     for (int k = 0; k < 6; ++k) mbar_init(&s_rbar[wid * 6 + k], 1);
   if (lane == 0) fence_mbar_init();
-  uint32_t xc = 0, rph = 0;
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t xc = 0, xm = 0, rph = 0;
   cluster_sync();
 
-  while (w > R.target) {
-    // ---------------- 1. DP
+  // ---------------- 1. DP
+  {
     Geo g;
     g.w = w;
-    const int per = ((w + CL - 1) / CL + 15) & ~15;
     g.cta_lo = min(w, (int)rank * per);
     g.cta_hi = min(w, g.cta_lo + per);
     g.own_lo = g.cta_lo + wid * kOwn;
     g.own_hi = min(g.cta_hi, g.own_lo + kOwn);
-    g.win_lo = g.own_lo - kXRows;
-    // warps outside the DP go straight to the cluster barrier -- unless the pass falls back
-    // to cluster barriers per exchange (tiny widths), which every thread must join
+    // window: owned +- 32, shifted inside [0, w) when the plane is wide enough, so that a
+    // window edge is either an image border (exact +inf) or a decaying halo -- no masks
+    g.win_lo = w >= kWin ? min(max(g.own_lo - kXRows, 0), w - kWin) : g.own_lo - kXRows;
     const bool in_dp = wid < ndp || per < kXRows;
     if (in_dp) {
       uint8_t* ring = smem + 2 * sizeof(double) * (size_t)pitch;
-      if (iters == 0 && R.U != nullptr)
-        dp_pass<true>(R, g, reinterpret_cast<double*>(smem), CL, rank, per, s_xbar, xc,
-                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, wid < ndp, dprof);
+      if (fp64)
+        dp_pass<true>(R, Rg, g, plane, reinterpret_cast<double*>(smem), CL, rank, per, s_xbar, xc, xm,
+                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, ndp, dprof);
       else
-        dp_pass<false>(R, g, reinterpret_cast<int*>(smem), CL, rank, per, s_xbar, xc,
-                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, wid < ndp, dprof);
+        dp_pass<false>(R, Rg, g, plane, reinterpret_cast<int*>(smem), CL, rank, per, s_xbar, xc, xm,
+                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, ndp, dprof);
     }
-    // warps outside the DP park on a named barrier (descheduled, no issue slots taken)
-    // until the DP warps are done; then everyone joins the cluster barrier
-    if (in_dp)
-      asm volatile("bar.arrive 1, %0;" ::"r"(blockDim.x) : "memory");
-    else
-      asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
-    cluster_sync();  // lastce / pw / delta of all CTAs visible
-    if (tid == 0) { long long t = clock64(); prof[0] += t - tp; tp = t; }
+  }
+  cluster_sync();  // lastce / pw / delta of all CTAs visible
+  long long t_dp = clock64() - tp;
+  tp = clock64();
 
     // ---------------- 2. select (redundant per CTA)
     SelSmem S;
@@ -678,200 +722,199 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_cluster_kernel(CarveR
         word >>= 2;
       }
     }
-    if (rank == 0 && R.sizes != nullptr) {
+    if (rank == 0 && R.cols != nullptr)
       for (int s = tid; s < b; s += blockDim.x) {
         R.cols[removed + s] = (int16_t)S.sel[s];
         R.costs[removed + s] = S.lce[S.sel[s]];
       }
-      if (tid == 0) R.sizes[iters] = b;
+    if (rank == 0 && tid == 0) R.sizes[iters] = b;  // every CTA reads them in the final phase
+  cluster_sync();  // the batch's log is complete before the row kernels read it
+  if (rank == 0 && tid == 0) {
+    Rg.b = b;
+    Rg.width = w - b;
+    Rg.iters = iters + 1;
+    Rg.removed = removed + b;
+    if (R.prof) {
+      R.prof[0] += t_dp;
+      R.prof[1] += clock64() - tp;
+      for (int k = 0; k < 4; ++k) R.prof[4 + k] += dprof[k];
     }
-    cluster_sync();  // the whole batch's log is visible
-    if (tid == 0) { long long t = clock64(); prof[1] += t - tp; tp = t; }
-
-    // ---------------- 3. compact luma + grad in place, update the alive bitmask
-    // (remove_batch, batching.py:76-107).  Warp per row; the row pair is staged in shared
-    // memory by a TMA bulk copy (next row prefetched while this one is written back), and
-    // every output word is one funnel shift of two staged words unless a removed column
-    // falls inside it.
-    const int w0 = w;
-    const int wn = w - b;
-    {
-      uint8_t* wbuf = smem + (size_t)wid * (4 * RB + kWarpScratch);
-      uint32_t* wv = reinterpret_cast<uint32_t*>(wbuf + 4 * RB);
-      int* pre = reinterpret_cast<int*>(wbuf + 4 * RB + 512);
-      const uint32_t nbytes = (uint32_t)((w0 + 15) & ~15);
-      auto issue = [&](int row, int slot) {
-        if (lane == 0) {
-          fence_proxy_async_global();
-          mbar_arrive_tx(&s_bar[2 * wid + slot], 2 * nbytes);
-          bulk_g2s(wbuf + (size_t)slot * 2 * RB, R.luma + (long)row * pitch, nbytes, &s_bar[2 * wid + slot]);
-          bulk_g2s(wbuf + (size_t)slot * 2 * RB + RB, R.grad + (long)row * pitch, nbytes, &s_bar[2 * wid + slot]);
-        }
-      };
-      int kk = 0;
-      if (wid < ncw && rlo + wid < rhi) issue(rlo + wid, 0);
-      for (int i = rlo + wid; wid < ncw && i < rhi; i += ncw, ++kk) {
-        const int slot = kk & 1;
-        if (i + ncw < rhi) issue(i + ncw, slot ^ 1);
-        mbar_wait(&s_bar[2 * wid + slot], phase[slot]);
-        phase[slot] ^= 1u;
-        const uint8_t* Ls = wbuf + (size_t)slot * 2 * RB;
-        const uint8_t* Gs = Ls + RB;
-        uint32_t* Lg = reinterpret_cast<uint32_t*>(R.luma + (long)i * pitch);
-        uint32_t* Gg = reinterpret_cast<uint32_t*>(R.grad + (long)i * pitch);
-        const int16_t* rg = log + (long)i * R.rem_cap + removed;  // sorted, old coordinates
-        int16_t* lst = reinterpret_cast<int16_t*>(wbuf + 4 * RB + 1024);
-        const int16_t* rr = rg;
-        if (b <= kListCap) {  // stage the list: the walk below is a dependent chain
-          for (int t = lane; t < b; t += 32) lst[t] = rg[t];
-          __syncwarp();
-          rr = lst;
-        }
-        // output byte y reads input byte y + #{t : rr[t] - t <= y}
-        int tptr = 0;  // warp-uniform: entries with rr[t]-t < chunk start
-        const int nwo = (wn + 3) >> 2;
-        for (int q0 = 0; q0 < nwo; q0 += 32) {
-          const int y0 = 4 * (q0 + lane);
-          const int cend = 4 * (q0 + 32);
-          int s4[4] = {tptr, tptr, tptr, tptr};
-          int t = tptr;
-          while (t < b) {
-            int a = rr[t] - t;
-            if (a >= cend) break;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) s4[u] += (a <= y0 + u);
-            ++t;
-          }
-          tptr = t;  // warp-uniform: all lanes walked the same entries
-          // entries with a < chunk start are counted in the base; recount the in-chunk ones
-          if (q0 + lane < nwo) {
-            uint32_t lo, go;
-            if (s4[0] == s4[3]) {
-              const int x0 = y0 + s4[0];
-              const uint32_t* L32 = reinterpret_cast<const uint32_t*>(Ls) + (x0 >> 2);
-              const uint32_t* G32 = reinterpret_cast<const uint32_t*>(Gs) + (x0 >> 2);
-              const uint32_t sh = (uint32_t)(x0 & 3) * 8u;
-              lo = __funnelshift_r(L32[0], L32[1], sh);
-              go = __funnelshift_r(G32[0], G32[1], sh);
-            } else {
-              lo = go = 0u;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                lo |= (uint32_t)Ls[y0 + u + s4[u]] << (8 * u);
-                go |= (uint32_t)Gs[y0 + u + s4[u]] << (8 * u);
-              }
-            }
-            Lg[q0 + lane] = lo;
-            Gg[q0 + lane] = go;
-          }
-        }
-        // alive bitmask: clear the original columns of this batch's removed pixels
-        uint32_t* arow = R.alive + (long)i * R.alive_pitch;
-        alive_row_prefix(arow, nw32, wv, pre);
-        // highest seams first: clearing bits above a target never moves the target's
-        // select, so the prefix counts taken before the batch stay valid
-        for (int base = b - 1; base >= 0; base -= 32) {
-          const int s = base - lane;
-          int o = 0;
-          if (s >= 0) o = alive_select(wv, pre, nw32, rr[s]);
-          __syncwarp();
-          if (s >= 0) atomicAnd(&wv[o >> 5], ~(1u << (o & 31)));
-          __syncwarp();
-        }
-        for (int m = lane; m < nw32; m += 32) arow[m] = wv[m];
-        __syncwarp();
-      }
-    }
-    cluster_sync();  // compacted luma of every row visible
-    if (tid == 0) { long long t = clock64(); prof[2] += t - tp; tp = t; }
-
-    // ---------------- 4. incremental gradient (batching.py:110-115 on the carved frame)
-    if (wn > R.target) {
-      const bool zero = rows < 3 || wn < 3;
-      for (int i = rlo + wid; wid < ncw && i < rhi; i += ncw) {
-        uint8_t* gr = R.grad + (long)i * pitch;
-        if (zero) {
-          for (int y = lane; y < wn; y += 32) gr[y] = 0;
-          continue;
-        }
-        const int ia = max(i - 1, 0), ib = min(i + 1, rows - 1);
-        // rows {i-1, i, i+1}'s removed columns (sorted), staged per warp when they fit
-        const int16_t* l3[3] = {log + (long)ia * R.rem_cap + removed, log + (long)i * R.rem_cap + removed,
-                                log + (long)ib * R.rem_cap + removed};
-        if (b <= kListCap) {
-          int16_t* lst = reinterpret_cast<int16_t*>(smem + (size_t)wid * (4 * RB + kWarpScratch) + 4 * RB + 1024);
-          for (int t = lane; t < 3 * b; t += 32) {
-            int rs = t / b;
-            lst[rs * kListCap + (t - rs * b)] = l3[rs][t - rs * b];
-          }
-          __syncwarp();
-          l3[0] = lst;
-          l3[1] = lst + kListCap;
-          l3[2] = lst + 2 * kListCap;
-        }
-        const int16_t* ri = l3[1];
-        const uint8_t* la = R.luma + (long)ia * pitch;
-        const uint8_t* lb = R.luma + (long)i * pitch;
-        const uint8_t* lc = R.luma + (long)ib * pitch;
-        // candidates: rows {i-1, i, i+1} x seams x offsets {-1, 0, +1}, in old columns
-        const int ncand = 9 * b;
-        for (int q = lane; q < ncand; q += 32) {
-          int rsel = q / (3 * b), rem = q - rsel * 3 * b;
-          int s = rem / 3, off = rem - s * 3 - 1;
-          int x = l3[rsel][s] + off;
-          if (x < 0 || x >= w0) continue;
-          int lo = 0, hi = b;  // number of row-i removed columns < x
-          while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (ri[mid] < x) lo = mid + 1; else hi = mid;
-          }
-          if (lo < b && ri[lo] == x) continue;  // removed itself
-          int y = x - lo;
-          int ym = max(y - 1, 0), yp = min(y + 1, wn - 1);
-          int gx = (la[yp] + 2 * lb[yp] + lc[yp]) - (la[ym] + 2 * lb[ym] + lc[ym]);
-          int gy = (lc[ym] + 2 * lc[y] + lc[yp]) - (la[ym] + 2 * la[y] + la[yp]);
-          int gv = abs(gx) + abs(gy);
-          gr[y] = (uint8_t)(gv > 255 ? 255 : gv);
-        }
-        __syncwarp();  // the staged lists are reused by the next row
-      }
-    }
-    removed += b;
-    ++iters;
-    w = wn;
-    cluster_sync();
-    if (tid == 0) { long long t = clock64(); prof[3] += t - tp; tp = t; }
   }
+}
 
-  // final index map (original column of every kept column) from the alive bitmask
-  {
-    uint8_t* wbuf = smem + (size_t)wid * (4 * RB + kWarpScratch);
-    uint32_t* wv = reinterpret_cast<uint32_t*>(wbuf + 4 * RB);
-    int* pre = reinterpret_cast<int*>(wbuf + 4 * RB + 512);
-    for (int i = rlo + wid; wid < ncw && i < rhi; i += ncw) {
-      alive_row_prefix(R.alive + (long)i * R.alive_pitch, nw32, wv, pre);
-      int16_t* ir = R.idx + (long)i * pitch;
-      for (int m = lane; m < nw32; m += 32) {
-        uint32_t wd = wv[m];
-        int o = pre[m];
-        while (wd) {
-          int bit = __ffs(wd) - 1;
-          ir[o++] = (int16_t)(m * 32 + bit);
-          wd &= wd - 1;
-        }
+// ------------------------------------------------------------------ row kernels
+// Compact one row of luma and gradient (remove_batch, batching.py:76-107) from the ping-pong
+// plane `iters_before & 1` into the other one.  Output byte y reads input byte y + s(y),
+// s(y) = #{t : a_t <= y} with a_t = rem[t] - t (non-decreasing).  Lanes hold the a_t and
+// every lane counts, for its output words q = lane + 32k, the a_t <= 4q through shuffles;
+// a word with one shift is a funnel shift of two input words, the few words with a shift
+// change inside (a_t % 4 != 0) are then rewritten byte by byte.
+constexpr int kRowWarps = 8;
+
+__global__ void __launch_bounds__(kRowWarps * 32) carve_compact_kernel(CarveRun* __restrict__ runs) {
+  const CarveRun& R = runs[blockIdx.y];
+  const int b = R.b;
+  if (b == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (i >= R.rows) return;
+  const int wn = R.width, w0 = wn + b;
+  const int src = (R.iters - 1) & 1, dst = src ^ 1;  // iters already counts this batch
+  const int16_t* rg = R.rem + (long)i * R.rem_cap + (R.removed - b);
+  const uint32_t* Li = reinterpret_cast<const uint32_t*>(R.luma[src] + (long)i * R.pitch);
+  const uint32_t* Gi = reinterpret_cast<const uint32_t*>(R.grad[src] + (long)i * R.pitch);
+  uint32_t* Lo = reinterpret_cast<uint32_t*>(R.luma[dst] + (long)i * R.pitch);
+  uint32_t* Go = reinterpret_cast<uint32_t*>(R.grad[dst] + (long)i * R.pitch);
+  const int nwo = (wn + 3) >> 2;
+  const int nwi = (w0 + 3) >> 2;
+  constexpr int KG = 8;
+  for (int g0 = 0; g0 * 32 < nwo; g0 += KG) {
+    int sk[KG];
+#pragma unroll
+    for (int k = 0; k < KG; ++k) sk[k] = 0;
+    for (int c = 0; c < b; c += 32) {
+      const int av = (c + lane < b) ? rg[c + lane] - (c + lane) : 0x7fffffff;
+      const int nt = min(32, b - c);
+      for (int tt = 0; tt < nt; ++tt) {
+        const int a = __shfl_sync(0xffffffffu, av, tt);
+#pragma unroll
+        for (int k = 0; k < KG; ++k) sk[k] += (a <= 4 * ((g0 + k) * 32 + lane)) ? 1 : 0;
       }
+    }
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      const int q = (g0 + k) * 32 + lane;
+      if (q < nwo) {
+        const int x0 = 4 * q + sk[k];
+        const int wq = x0 >> 2;
+        const uint32_t sh = (uint32_t)(x0 & 3) * 8u;
+        const uint32_t l0 = Li[wq], g0v = Gi[wq];
+        const uint32_t l1 = wq + 1 < nwi ? Li[wq + 1] : 0u, g1v = wq + 1 < nwi ? Gi[wq + 1] : 0u;
+        Lo[q] = __funnelshift_r(l0, l1, sh);
+        Go[q] = __funnelshift_r(g0v, g1v, sh);
+      }
+    }
+  }
+  __syncwarp();
+  const uint8_t* Lb = R.luma[src] + (long)i * R.pitch;
+  const uint8_t* Gb = R.grad[src] + (long)i * R.pitch;
+  for (int t = lane; t < b; t += 32) {
+    const int at = rg[t] - t;
+    if ((at & 3) == 0 || (at >> 2) >= nwo) continue;
+    const int q = at >> 2, y0 = 4 * q;
+    uint32_t lv = 0u, gv = 0u;
+    for (int u = 0; u < 4; ++u) {
+      int su = 0;
+      for (int t2 = 0; t2 < b; ++t2) su += (rg[t2] - t2 <= y0 + u) ? 1 : 0;
+      const int x = y0 + u + su;
+      lv |= (uint32_t)(x < w0 ? Lb[x] : 0) << (8 * u);
+      gv |= (uint32_t)(x < w0 ? Gb[x] : 0) << (8 * u);
+    }
+    Lo[q] = lv;
+    Go[q] = gv;
+  }
+}
+
+// default_energy (batching.py:110-115) of the carved frame, incrementally: a pixel's Sobel
+// value changes only if a removed pixel of rows i-1..i+1 lay within one column of it.
+__global__ void __launch_bounds__(kRowWarps * 32) carve_dirty_kernel(CarveRun* __restrict__ runs) {
+  const CarveRun& R = runs[blockIdx.y];
+  const int b = R.b;
+  if (b == 0 || R.width <= R.target) return;  // no further pass reads this gradient
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  const int rows = R.rows;
+  if (i >= rows) return;
+  const int wn = R.width, w0 = wn + b;
+  const int dst = R.iters & 1;
+  uint8_t* gr = R.grad[dst] + (long)i * R.pitch;
+  if (rows < 3 || wn < 3) {
+    for (int y = lane; y < wn; y += 32) gr[y] = 0;
+    return;
+  }
+  const int off = R.removed - b;
+  const int ia = max(i - 1, 0), ib = min(i + 1, rows - 1);
+  const int16_t* l3[3] = {R.rem + (long)ia * R.rem_cap + off, R.rem + (long)i * R.rem_cap + off,
+                          R.rem + (long)ib * R.rem_cap + off};
+  const int16_t* ri = l3[1];
+  const uint8_t* la = R.luma[dst] + (long)ia * R.pitch;
+  const uint8_t* lb = R.luma[dst] + (long)i * R.pitch;
+  const uint8_t* lc = R.luma[dst] + (long)ib * R.pitch;
+  for (int q = lane; q < 9 * b; q += 32) {
+    const int rsel = q / (3 * b), rem = q - rsel * 3 * b;
+    const int s = rem / 3, offc = rem - s * 3 - 1;
+    const int x = l3[rsel][s] + offc;
+    if (x < 0 || x >= w0) continue;
+    int lo = 0, hi = b;  // row-i removed columns < x
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (ri[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    if (lo < b && ri[lo] == x) continue;  // removed itself
+    const int y = x - lo;
+    const int ym = max(y - 1, 0), yp = min(y + 1, wn - 1);
+    const int gx = (la[yp] + 2 * lb[yp] + lc[yp]) - (la[ym] + 2 * lb[ym] + lc[ym]);
+    const int gy = (lc[ym] + 2 * lc[y] + lc[yp]) - (la[ym] + 2 * la[y] + la[yp]);
+    const int gv = abs(gx) + abs(gy);
+    gr[y] = (uint8_t)(gv > 255 ? 255 : gv);
+  }
+}
+
+// Final index map (original column of every kept column): replay each row's batches on an
+// alive-column bitmask in shared memory.  A batch's columns are "the c-th alive column" of
+// the frame it was selected on; clearing the highest first keeps the prefix counts taken
+// before the batch valid for the lower ones.
+__global__ void __launch_bounds__(kRowWarps * 32) carve_index_kernel(CarveRun* __restrict__ runs) {
+  __shared__ uint32_t s_wv[kRowWarps][32 * kMaxAliveWordsPerLane];
+  __shared__ int s_pre[kRowWarps][32 * kMaxAliveWordsPerLane];
+  const CarveRun& R = runs[blockIdx.y];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int i = blockIdx.x * kRowWarps + wl;
+  if (i >= R.rows) return;
+  uint32_t* wv = s_wv[wl];
+  int* pre = s_pre[wl];
+  const int nw32 = (R.width0 + 31) >> 5;
+  for (int m = lane; m < nw32; m += 32) {
+    int hi = R.width0 - 32 * m;
+    wv[m] = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+  }
+  __syncwarp();
+  const int16_t* lg = R.rem + (long)i * R.rem_cap;
+  auto prefix = [&]() {
+    int running = 0;
+#pragma unroll
+    for (int u = 0; u < kMaxAliveWordsPerLane; ++u) {
+      int m = lane + 32 * u;
+      int p = m < nw32 ? __popc(wv[m]) : 0;
+      int incl = warp_incl_scan(p);
+      if (m < nw32) pre[m] = running + incl - p;
+      running += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+  };
+  int off = 0;
+  for (int k = 0; k < R.iters; ++k) {
+    const int bk = R.sizes[k];
+    prefix();
+    for (int base = bk - 1; base >= 0; base -= 32) {
+      const int sidx = base - lane;
+      int o = 0;
+      if (sidx >= 0) o = alive_select(wv, pre, nw32, lg[off + sidx]);
+      __syncwarp();
+      if (sidx >= 0) atomicAnd(&wv[o >> 5], ~(1u << (o & 31)));
       __syncwarp();
     }
+    off += bk;
   }
-  if (rank == 0 && tid == 32 && R.prof)
-    for (int k = 0; k < 3; ++k) R.prof[8 + k] = dprof[k];
-  if (rank == 0 && tid == 0) {
-    Rg.iters = iters;
-    Rg.removed = removed;
-    if (R.prof) {
-      for (int k = 0; k < 4; ++k) R.prof[k] = prof[k];
-      for (int k = 0; k < 3; ++k) R.prof[4 + k] = dprof[k];
-
+  prefix();
+  int16_t* ir = R.idx + (long)i * R.pitch;
+  for (int m = lane; m < nw32; m += 32) {
+    uint32_t wd = wv[m];
+    int o = pre[m];
+    while (wd) {
+      int bit = __ffs(wd) - 1;
+      ir[o++] = (int16_t)(m * 32 + bit);
+      wd &= wd - 1;
     }
   }
 }
@@ -937,14 +980,48 @@ __global__ void plane_sobel_kernel(const uint8_t* __restrict__ luma, int rows, i
 void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes,
                       const CarveRun& R, cudaStream_t st) {
   dim3 grid(cdiv(W, 32), cdiv(H, 32));
-  run_setup_kernel<<<grid, dim3(32, 8), 0, st>>>(frame, H, W, C, transposed, codes, R.pitch, R.luma, R.grad,
-                                                 R.idx);
+  run_setup_kernel<<<grid, dim3(32, 8), 0, st>>>(frame, H, W, C, transposed, codes, R.pitch, R.luma[0],
+                                                 R.grad[0], R.idx);
   SCPL_CHECK_LAUNCH();
   if (!codes) {
-    plane_sobel_kernel<<<dim3(cdiv(R.width0, 256), R.rows), 256, 0, st>>>(R.luma, R.rows, R.width0, R.pitch,
-                                                                         R.grad);
+    plane_sobel_kernel<<<dim3(cdiv(R.width0, 256), R.rows), 256, 0, st>>>(R.luma[0], R.rows, R.width0,
+                                                                         R.pitch, R.grad[0]);
     SCPL_CHECK_LAUNCH();
   }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    SCPL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    SCPL_ARG(q == cudaDriverEntryPointSuccess && p != nullptr, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static void encode_plane(CUtensorMap* tm, const void* base, CUtensorMapDataType dt, int esz, int cols, int rows,
+                         int pitch, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch * esz};
+  cuuint32_t box[2] = {(cuuint32_t)kRingW, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = tmap_encode()(tm, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SCPL_ARG(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed for a carve plane");
+}
+
+void encode_carve_tensor_maps(CarveRun& R) {
+  for (int p = 0; p < 2; ++p)
+    encode_plane(&R.tm_grad[p], R.grad[p], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, R.width0, R.rows, R.pitch,
+                 DpCfg<false>::kStageRows);
+  if (R.U)
+    encode_plane(&R.tm_U, R.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, R.width0, R.rows, R.pitch,
+                 DpCfg<true>::kStageRows);
 }
 
 int carve_cluster_size(int nruns, int width, int num_sms) {
@@ -981,25 +1058,20 @@ size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps
 int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
 
 bool carve_stage_dtab(int rows, int pitch, int cl) {
-  return carve_smem_bytes(rows, pitch, true, carve_comp_warps(pitch), carve_dp_warps(pitch, cl)) <= kSmemBudget;
+  return carve_smem_bytes(rows, pitch, true, 0, carve_dp_warps(pitch, cl)) <= kSmemBudget;
 }
 
-void launch_carve_cluster(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st) {
+void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st) {
   if (nruns == 0) return;
-  // the DP needs carve_dp_warps() warps (128 owned columns each); the row-parallel phases
-  // use every warp, so the CTA always runs kMaxWarps (DP-idle warps skip the DP)
   const int dpw = carve_dp_warps(width, cl);
   SCPL_ARG(dpw <= kMaxWarps, "carve width too large for the cluster size");
-  const int warps = kMaxWarps;
-  const int ncw = carve_comp_warps(pitch);
-  SCPL_ARG(ncw >= 1, "carve plane too wide for the compaction stage");
   const bool stage = carve_stage_dtab(rows, pitch, cl);
-  size_t smem = carve_smem_bytes(rows, pitch, stage, ncw, dpw);
+  size_t smem = carve_smem_bytes(rows, pitch, stage, 0, dpw);
   SCPL_ARG(smem <= 227 * 1024, "carve plane too large for shared memory");
-  SCPL_CUDA(cudaFuncSetAttribute(carve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SCPL_CUDA(cudaFuncSetAttribute(carve_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nruns * cl);
-  cfg.blockDim = dim3(warps * 32);
+  cfg.blockDim = dim3(kMaxWarps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1009,7 +1081,18 @@ void launch_carve_cluster(CarveRun* runs_d, int nruns, int rows, int pitch, int 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_cluster_kernel, runs_d, cl, ncw));
+  SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl));
+  SCPL_CHECK_LAUNCH();
+  dim3 rgrid(cdiv(rows, kRowWarps), nruns);
+  carve_compact_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
+  SCPL_CHECK_LAUNCH();
+  carve_dirty_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
+  SCPL_CHECK_LAUNCH();
+}
+
+void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st) {
+  if (nruns == 0) return;
+  carve_index_kernel<<<dim3(cdiv(rows, kRowWarps), nruns), kRowWarps * 32, 0, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();
 }
 

@@ -1,5 +1,6 @@
 // Internal kernel launchers (not part of the C-ABI; see include/scpl.h).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,13 +33,15 @@ void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first
 
 // ------------------------------------------------------------------ carve v2 (scpl_carve2.cu)
 // One run's carve state; planes are rows x pitch (pitch >= width0, multiple of 16).
-struct CarveRun {
+struct alignas(64) CarveRun {
+  CUtensorMap tm_grad[2];  // 2-D TMA descriptors of the energy planes (DP windows, OOB -> 0)
+  CUtensorMap tm_U;
   int rows, pitch, width0, target;
   int kmax;             // 0 = SCPL batch (k = remaining), 1 = raw (one min seam per pass)
   int stage_dtab;       // stage the landing-delta table in shared memory (set by the launcher)
   const double* U;      // fp64 energy of the first pass, or nullptr (gradient from the start)
-  uint8_t* luma;        // compacted in place
-  uint8_t* grad;        // gradient of the compacted luma (incrementally maintained)
+  uint8_t* luma[2];     // ping-pong: pass k reads plane k & 1, the row kernels write the other
+  uint8_t* grad[2];     // gradient of the compacted luma (incrementally maintained)
   int16_t* idx;         // output: original column of each kept column (rows x pitch)
   uint32_t* alive;      // rows x alive_pitch bitmask of surviving original columns
   int alive_pitch;
@@ -52,13 +55,18 @@ struct CarveRun {
   int* sizes;           // optional per-batch sizes (capacity width0)
   int16_t* cols;        // optional per-seam last-row column (capacity width0)
   double* costs;        // optional per-seam cost
-  // results
-  int iters, removed;
+  // state (read at every kernel entry, advanced by the pass kernel)
+  int width;            // current width
+  int iters;            // DP passes done
+  int removed;          // seams removed so far (offset of the next batch in the log)
+  int b;                // size of the batch selected by the latest pass (0: none)
 };
 void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes,
                       const CarveRun& R, cudaStream_t st);
 int carve_cluster_size(int nruns, int width, int num_sms);
-void launch_carve_cluster(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st);
+void encode_carve_tensor_maps(CarveRun& R);
+void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st);
+void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st);
 bool carve_stage_dtab(int rows, int pitch, int cl);
 int carve_warps(int width, int cl);
 
