@@ -122,6 +122,14 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames /*dev*/, int T, int
                         const scpl_video_params* params, uint8_t* out /*dev*/, scpl_video_result* result,
                         void* stream);
 
+/* Same call with HOST buffers (pinned for asynchronous copies): frames are copied in
+ * 16-frame chunks on a copy stream while the energy codes and the buffer scan run on the
+ * chunks already resident; each run's output frames are copied back on a second copy stream
+ * as soon as the run is replayed.  Returns once out is complete. */
+int scpl_retarget_video_host(scpl_ctx* ctx, const uint8_t* frames /*host*/, int T, int h, int w, int channels,
+                             const scpl_video_params* params, uint8_t* out /*host*/, scpl_video_result* result,
+                             void* stream);
+
 /* ---- lower-level reference functions (API completeness; not on the hot path) ---- */
 
 /* seams.cumulative_energy (seams.py:39-65): full float64 ce and int8 back tables. */

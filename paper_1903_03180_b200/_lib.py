@@ -59,6 +59,8 @@ _SIGS = {
                     ctypes.c_int, ctypes.c_int, _vp, _vp],
     "scpl_retarget_video": [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                             ctypes.POINTER(VideoParams), _vp, ctypes.POINTER(VideoResult), _vp],
+    "scpl_retarget_video_host": [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                            ctypes.POINTER(VideoParams), _vp, ctypes.POINTER(VideoResult), _vp],
     "scpl_cumulative_energy": [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp],
     "scpl_label_parents": [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp],
     "scpl_trace_columns": [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp, _vp],

@@ -40,6 +40,7 @@ struct PwPlan {
 struct scpl_ctx {
   int device = 0;
   int num_sms = 148;
+  cudaStream_t s_h2d = nullptr, s_codes = nullptr, s_d2h = nullptr;  // host-buffer pipeline
   double* h_asde = nullptr;  // pinned
   int h_asde_cap = 0;
   std::map<long, PwPlan> plans;
@@ -118,8 +119,9 @@ double* pinned_asde(scpl_ctx* ctx, int n) {
 
 // ------------------------------------------------------------------ buffer scan
 // SpatioTemporalBuffer.push/flush over the whole clip (buffering.py:93-138).
+template <class Ready>
 std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* codes, int T, int H, int W,
-                                             const scpl_video_params& P, cudaStream_t st) {
+                                             const scpl_video_params& P, cudaStream_t st, Ready&& ensure_codes) {
   std::vector<std::pair<int, int>> runs;
   if (T == 0) return runs;
   const long N = (long)H * W;
@@ -145,6 +147,7 @@ std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* code
       continue;
     }
     int L = std::min(spec, std::min(remaining, P.max_len - n_acc));
+    ensure_codes(s + n_acc + L - 1);  // codes of every frame this launch reads are on the stream
     launch_window_stats(codes, N, plan.leaves, plan.nleaves, s, n_acc, L, 1, init ? 1 : 0, P.w_motion,
                         P.w_grad, ck.as<double>(), ck.as<double>() + N, leafsum.as<double>(), plan.vnodes,
                         asde_d.as<double>(), st);
@@ -316,6 +319,8 @@ void scpl_destroy(scpl_ctx* ctx) {
     cudaFree(kv.second.vnodes);
   }
   if (ctx->h_asde) cudaFreeHost(ctx->h_asde);
+  for (cudaStream_t x : {ctx->s_h2d, ctx->s_codes, ctx->s_d2h})
+    if (x) cudaStreamDestroy(x);
   delete ctx;
 }
 
@@ -420,136 +425,224 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
   });
 }
 
-int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int w, int channels,
-                        const scpl_video_params* params, uint8_t* out, scpl_video_result* result, void* stream) {
-  return guarded(ctx, [&] {
-    cudaStream_t st = (cudaStream_t)stream;
-    SCPL_ARG(params != nullptr && result != nullptr, "params/result is NULL");
-    const scpl_video_params P = *params;
-    SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
-    SCPL_ARG(h >= 3 && w >= 3, "frame too small to carve");
-    SCPL_ARG(P.target_width >= 1 && P.target_width <= w, "target width out of range");
-    SCPL_ARG(P.target_height >= 1 && P.target_height <= h, "target height out of range");
-    SCPL_ARG(P.mode >= 0 && P.mode <= 2, "unknown mode");
-    SCPL_ARG(P.max_len >= 1, "max_len must be >= 1");
-    SCPL_ARG(P.mode != 2 || P.phi != nullptr, "phi table required for buffered mode");
-    result->dp_passes = 0;
-    result->n_runs = 0;
-    for (float& x : result->phase_ms) x = 0.f;
-    for (long long& x : result->carve_cycles) x = 0;
-    result->carve_cluster = 0;
-    if (T <= 0) return;
-    const int C = channels;
-    const int tw = P.target_width, th = P.target_height;
-    // device-side phase timing (codes, scan, carve, replay) for the bench
-    cudaEvent_t ev[5];
-    for (auto& e : ev) SCPL_CUDA(cudaEventCreate(&e));
-    struct EvGuard {
-      cudaEvent_t* e;
-      ~EvGuard() {
-        for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
-      }
-    } evg{ev};
-    float carve_ms = 0.f, replay_ms = 0.f;
-    SCPL_CUDA(cudaEventRecord(ev[0], st));
+}  // extern "C"
 
-    // 1. energy codes (not needed by raw mode: gradient only)
-    DBuf codes;
-    if (P.mode != 0) {
-      codes = DBuf(sizeof(uint16_t) * (size_t)T * h * w, st);
-      launch_codes(frames, nullptr, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, st);
+namespace {
+
+// retarget_video (pipeline.py:92-137).  Device buffers (frames, out) or, when frames_host /
+// out_host are given, pinned host buffers: the clip then arrives in chunks on a copy stream
+// while the energy codes and the buffer scan start on the first chunks, and every run's
+// output frames leave on a second copy stream as soon as that run is replayed.
+void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* frames_host, int T, int h, int w,
+                   int channels, const scpl_video_params& P, uint8_t* out_dev, uint8_t* out_host,
+                   scpl_video_result* result, cudaStream_t st) {
+  SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
+  SCPL_ARG(h >= 3 && w >= 3, "frame too small to carve");
+  SCPL_ARG(P.target_width >= 1 && P.target_width <= w, "target width out of range");
+  SCPL_ARG(P.target_height >= 1 && P.target_height <= h, "target height out of range");
+  SCPL_ARG(P.mode >= 0 && P.mode <= 2, "unknown mode");
+  SCPL_ARG(P.max_len >= 1, "max_len must be >= 1");
+  SCPL_ARG(P.mode != 2 || P.phi != nullptr, "phi table required for buffered mode");
+  result->dp_passes = 0;
+  result->n_runs = 0;
+  for (float& x : result->phase_ms) x = 0.f;
+  for (long long& x : result->carve_cycles) x = 0;
+  result->carve_cluster = 0;
+  if (T <= 0) return;
+  const int C = channels;
+  const int tw = P.target_width, th = P.target_height;
+  const size_t fbytes0 = (size_t)h * w * C;
+  const bool host_in = frames_host != nullptr, host_out = out_host != nullptr;
+  if (host_in || host_out) {
+    for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_codes, &ctx->s_d2h})
+      if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
+  }
+  std::vector<cudaEvent_t> events;
+  struct EvGuard {
+    std::vector<cudaEvent_t>& e;
+    ~EvGuard() {
+      for (auto x : e) cudaEventDestroy(x);
     }
+  } evg{events};
+  auto new_event = [&](bool timing) {
+    cudaEvent_t e;
+    SCPL_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    events.push_back(e);
+    return e;
+  };
+  cudaEvent_t ev[5];
+  for (auto& e : ev) e = new_event(true);
+  float carve_ms = 0.f, replay_ms = 0.f;
+  SCPL_CUDA(cudaEventRecord(ev[0], st));
+
+  // 0. frames (host: chunked H2D on the copy stream)
+  DBuf frames_buf;
+  const uint8_t* frames = frames_dev;
+  const int chunk = 16;
+  const int nchunk = (T + chunk - 1) / chunk;
+  std::vector<cudaEvent_t> ev_codes;
+  if (host_in) {
+    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev[0], 0));  // after earlier work on st
+    frames_buf = DBuf(fbytes0 * T, st);
     SCPL_CUDA(cudaEventRecord(ev[1], st));
-    // 2. runs
-    std::vector<std::pair<int, int>> runs;
-    if (P.mode == 2) {
-      runs = buffer_scan(ctx, codes.as<uint16_t>(), T, h, w, P, st);
-    } else {
-      for (int t = 0; t < T; ++t) runs.push_back({t, 1});
+    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev[1], 0));  // the allocation is ordered on st
+    frames = frames_buf.as<uint8_t>();
+  }
+  // 1. energy codes (not needed by raw mode: gradient only)
+  DBuf codes;
+  if (P.mode != 0) codes = DBuf(sizeof(uint16_t) * (size_t)T * h * w, st);
+  if (host_in) {
+    cudaEvent_t ready_codes = new_event(false);
+    SCPL_CUDA(cudaEventRecord(ready_codes, st));
+    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ready_codes, 0));
+    for (int c = 0; c < nchunk; ++c) {
+      const int t0 = c * chunk, n = std::min(chunk, T - t0);
+      SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
+                                fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
+      cudaEvent_t e = new_event(false);
+      SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
+      SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, e, 0));
+      if (P.mode != 0)
+        launch_codes(frames + fbytes0 * t0, t0 > 0 ? frames + fbytes0 * (t0 - 1) : nullptr, n, h, w, C,
+                     codes.as<uint16_t>() + (size_t)t0 * h * w, ctx->num_sms, ctx->s_codes);
+      cudaEvent_t ec = new_event(false);
+      SCPL_CUDA(cudaEventRecord(ec, ctx->s_codes));
+      ev_codes.push_back(ec);
+    }
+  } else if (P.mode != 0) {
+    launch_codes(frames, nullptr, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, st);
+  }
+  int codes_ready = host_in ? -1 : nchunk - 1;  // chunks st already waits for
+  auto ensure_codes = [&](int t_max) {
+    const int c = std::min(nchunk - 1, t_max / chunk);
+    while (codes_ready < c) SCPL_CUDA(cudaStreamWaitEvent(st, ev_codes[++codes_ready], 0));
+  };
+  SCPL_CUDA(cudaEventRecord(ev[1], st));
+  // 2. runs
+  std::vector<std::pair<int, int>> runs;
+  if (P.mode == 2) {
+    runs = buffer_scan(ctx, codes.as<uint16_t>(), T, h, w, P, st, ensure_codes);
+  } else {
+    for (int t = 0; t < T; ++t) runs.push_back({t, 1});
+  }
+  ensure_codes(T - 1);  // every frame and code is on the device from here on
+  SCPL_CUDA(cudaEventRecord(ev[2], st));
+  SCPL_CUDA(cudaEventSynchronize(ev[2]));
+  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[0], ev[0], ev[1]));
+  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[1], ev[1], ev[2]));
+  result->n_runs = (int)runs.size();
+  if (result->run_start && result->run_len)
+    for (size_t r = 0; r < runs.size(); ++r) {
+      result->run_start[r] = runs[r].first;
+      result->run_len[r] = runs[r].second;
+    }
+
+  // 3. phases (pipeline.py:192-193, 246-277)
+  std::vector<int> phases;  // 0 width, 1 height
+  for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
+    if (ax == 0 && tw < w) phases.push_back(0);
+    if (ax == 1 && th < h) phases.push_back(1);
+  }
+  DBuf out_buf;
+  uint8_t* out = out_dev;
+  if (host_out) {
+    out_buf = DBuf((size_t)T * th * tw * C, st);
+    out = out_buf.as<uint8_t>();
+  }
+  auto ship = [&](size_t off, size_t bytes) {  // D2H of finished output frames
+    if (!host_out) return;
+    cudaEvent_t e = new_event(false);
+    SCPL_CUDA(cudaEventRecord(e, st));
+    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
+    SCPL_CUDA(cudaMemcpyAsync(out_host + off, out + off, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
+  };
+  if (phases.empty()) {
+    SCPL_CUDA(cudaMemcpyAsync(out, frames, (size_t)T * h * w * C, cudaMemcpyDeviceToDevice, st));
+    ship(0, (size_t)T * h * w * C);
+  }
+  const uint8_t* cur = frames;
+  int curH = h, curW = w;
+  DBuf tmp;
+  long dp = 0;
+  for (size_t ph = 0; ph < phases.size(); ++ph) {
+    const bool height = phases[ph] == 1;
+    const int rows = height ? curW : curH, cols = height ? curH : curW;
+    const int target = height ? th : tw;
+    const bool with_U = (ph == 0) && P.mode != 0;
+    CarveSet S;
+    carve_alloc(S, (int)runs.size(), rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
+                carve_cluster_size((int)runs.size(), cols, ctx->num_sms), st);
+    const size_t fbytes = (size_t)curH * curW * C;
+    for (size_t r = 0; r < runs.size(); ++r) {
+      CarveRun& R = S.runs[r];
+      // the first carved axis works on the original frames, whose energy codes carry the
+      // Sobel gradient of every frame (so the carve's gradient plane needs no recompute)
+      const uint16_t* fcodes = (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)runs[r].first * h * w
+                                                         : nullptr;
+      launch_run_setup(cur + fbytes * runs[r].first, curH, curW, C, height ? 1 : 0, fcodes, R, st);
+      if (with_U)
+        launch_uniform(codes.as<uint16_t>(), h, w, runs[r].first, runs[r].second, 1, P.w_motion, P.w_grad,
+                       height ? 1 : 0, const_cast<double*>(R.U), st, R.pitch);
+    }
+    SCPL_CUDA(cudaEventRecord(ev[3], st));
+    carve_run_all(ctx, S, st);
+    SCPL_CUDA(cudaEventRecord(ev[4], st));
+    for (auto& R : S.runs) dp += R.iters;
+    for (int k = 0; k < 4; ++k) result->carve_cycles[k] += S.prof[k];
+    result->carve_cluster = S.cl;
+    const int nH = height ? th : curH, nW = height ? curW : tw;
+    const bool last = ph + 1 == phases.size();
+    DBuf next;
+    uint8_t* dst = out;
+    if (!last) {
+      next = DBuf((size_t)T * nH * nW * C, st);
+      dst = next.as<uint8_t>();
+    }
+    const size_t obytes = (size_t)nH * nW * C;
+    for (size_t r = 0; r < runs.size(); ++r) {
+      const CarveRun& R = S.runs[r];
+      launch_replay(cur + fbytes * runs[r].first, dst + obytes * runs[r].first, runs[r].second, curH, curW, C,
+                    R.idx, R.pitch, target, height ? 1 : 0, st);
+      if (last) ship(obytes * runs[r].first, obytes * runs[r].second);
     }
     SCPL_CUDA(cudaEventRecord(ev[2], st));
     SCPL_CUDA(cudaEventSynchronize(ev[2]));
-    SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[0], ev[0], ev[1]));
-    SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[1], ev[1], ev[2]));
-    result->n_runs = (int)runs.size();
-    if (result->run_start && result->run_len)
-      for (size_t r = 0; r < runs.size(); ++r) {
-        result->run_start[r] = runs[r].first;
-        result->run_len[r] = runs[r].second;
-      }
+    float a = 0.f, b = 0.f;
+    SCPL_CUDA(cudaEventElapsedTime(&a, ev[3], ev[4]));
+    SCPL_CUDA(cudaEventElapsedTime(&b, ev[4], ev[2]));
+    carve_ms += a;
+    replay_ms += b;
+    cur = dst;
+    curH = nH;
+    curW = nW;
+    tmp = std::move(next);
+  }
+  result->dp_passes = dp;
+  if (host_out) SCPL_CUDA(cudaStreamSynchronize(ctx->s_d2h));
+  SCPL_CUDA(cudaStreamSynchronize(st));
+  result->phase_ms[2] = carve_ms;
+  result->phase_ms[3] = replay_ms;
+}
 
-    // 3. phases (pipeline.py:192-193, 246-277)
-    std::vector<int> phases;  // 0 width, 1 height
-    for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
-      if (ax == 0 && tw < w) phases.push_back(0);
-      if (ax == 1 && th < h) phases.push_back(1);
-    }
-    if (phases.empty()) {
-      SCPL_CUDA(cudaMemcpyAsync(out, frames, (size_t)T * h * w * C, cudaMemcpyDeviceToDevice, st));
-      SCPL_CUDA(cudaStreamSynchronize(st));
-      return;
-    }
-    const uint8_t* cur = frames;
-    int curH = h, curW = w;
-    DBuf tmp;
-    long dp = 0;
-    for (size_t ph = 0; ph < phases.size(); ++ph) {
-      const bool height = phases[ph] == 1;
-      const int rows = height ? curW : curH, cols = height ? curH : curW;
-      const int target = height ? th : tw;
-      const bool with_U = (ph == 0) && P.mode != 0;
-      CarveSet S;
-      carve_alloc(S, (int)runs.size(), rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
-                  carve_cluster_size((int)runs.size(), cols, ctx->num_sms), st);
-      const size_t fbytes = (size_t)curH * curW * C;
-      for (size_t r = 0; r < runs.size(); ++r) {
-        CarveRun& R = S.runs[r];
-        // the first carved axis works on the original frames, whose energy codes carry the
-        // Sobel gradient of every frame (so the carve's gradient plane needs no recompute)
-        const uint16_t* fcodes = (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)runs[r].first * h * w
-                                                           : nullptr;
-        launch_run_setup(cur + fbytes * runs[r].first, curH, curW, C, height ? 1 : 0, fcodes, R, st);
-        if (with_U)
-          launch_uniform(codes.as<uint16_t>(), h, w, runs[r].first, runs[r].second, 1, P.w_motion, P.w_grad,
-                         height ? 1 : 0, const_cast<double*>(R.U), st, R.pitch);
-      }
-      SCPL_CUDA(cudaEventRecord(ev[3], st));
-      carve_run_all(ctx, S, st);
-      SCPL_CUDA(cudaEventRecord(ev[4], st));
-      for (auto& R : S.runs) dp += R.iters;
-      for (int k = 0; k < 4; ++k) result->carve_cycles[k] += S.prof[k];
-      result->carve_cluster = S.cl;
-      const int nH = height ? th : curH, nW = height ? curW : tw;
-      const bool last = ph + 1 == phases.size();
-      DBuf next;
-      uint8_t* dst = out;
-      if (!last) {
-        next = DBuf((size_t)T * nH * nW * C, st);
-        dst = next.as<uint8_t>();
-      }
-      const size_t obytes = (size_t)nH * nW * C;
-      for (size_t r = 0; r < runs.size(); ++r) {
-        const CarveRun& R = S.runs[r];
-        launch_replay(cur + fbytes * runs[r].first, dst + obytes * runs[r].first, runs[r].second, curH, curW, C,
-                      R.idx, R.pitch, target, height ? 1 : 0, st);
-      }
-      SCPL_CUDA(cudaEventRecord(ev[2], st));
-      SCPL_CUDA(cudaEventSynchronize(ev[2]));
-      float a = 0.f, b = 0.f;
-      SCPL_CUDA(cudaEventElapsedTime(&a, ev[3], ev[4]));
-      SCPL_CUDA(cudaEventElapsedTime(&b, ev[4], ev[2]));
-      carve_ms += a;
-      replay_ms += b;
-      // keep S alive until the replays are enqueued (stream-ordered frees)
-      cur = dst;
-      curH = nH;
-      curW = nW;
-      tmp = std::move(next);
-    }
-    result->dp_passes = dp;
-    SCPL_CUDA(cudaStreamSynchronize(st));
-    result->phase_ms[2] = carve_ms;
-    result->phase_ms[3] = replay_ms;
+}  // namespace
+
+extern "C" {
+
+int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int w, int channels,
+                        const scpl_video_params* params, uint8_t* out, scpl_video_result* result, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(params != nullptr && result != nullptr, "params/result is NULL");
+    retarget_core(ctx, frames, nullptr, T, h, w, channels, *params, out, nullptr, result, (cudaStream_t)stream);
+  });
+}
+
+int scpl_retarget_video_host(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int w, int channels,
+                             const scpl_video_params* params, uint8_t* out, scpl_video_result* result,
+                             void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(params != nullptr && result != nullptr, "params/result is NULL");
+    SCPL_ARG(frames != nullptr && out != nullptr, "frames/out is NULL");
+    retarget_core(ctx, nullptr, frames, T, h, w, channels, *params, nullptr, out, result, (cudaStream_t)stream);
   });
 }
 

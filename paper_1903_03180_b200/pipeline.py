@@ -92,14 +92,27 @@ def _phi_table(policy: BufferPolicy):
     return (ctypes.c_double * len(vals))(*vals)
 
 
-def _run_device(clip, config: RetargetConfig, tw: int, th: int):
-    """Call scpl_retarget_video on a CUDA uint8 clip (T, H, W, C); returns (out, dp, runs)."""
+def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
+    """Call libscpl on a uint8 clip (T, H, W, C); returns (out, dp, runs).
+
+    A CUDA clip goes through scpl_retarget_video (device in, device out).  A host clip goes
+    through scpl_retarget_video_host, which streams it in chunks, overlaps the copies with the
+    energy/scan kernels and ships every run's output frames back as soon as they are carved;
+    clip and out should be pinned for the copies to run asynchronously.
+    """
     torch = _lib.torch_cuda()
     if config.reaverage_energy:
         raise NotImplementedError("reaverage_energy=True is not implemented on the GPU path yet")
     T, H, W = clip.shape[:3]
     C = clip.shape[3] if clip.dim() == 4 else 1
-    out = torch.empty((T, th, tw, C), dtype=torch.uint8, device=clip.device)
+    host = not clip.is_cuda
+    if out is None:
+        out = (torch.empty((T, th, tw, C), dtype=torch.uint8, pin_memory=True) if host
+               else torch.empty((T, th, tw, C), dtype=torch.uint8, device=clip.device))
+    elif (tuple(out.shape) not in ((T, th, tw, C), (T, th, tw) if C == 1 else ()) or out.dtype != torch.uint8
+          or out.is_cuda == host or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous uint8 {'host' if host else 'CUDA'} tensor of shape "
+                         f"{(T, th, tw, C)}")
     phi = _phi_table(config.policy)
     params = _lib.VideoParams(tw, th, _MODE_ID[config.mode], int(config.height_first), config.policy.max_len,
                               float(config.w_motion), float(config.w_grad),
@@ -108,9 +121,10 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int):
     lens = (ctypes.c_int * max(T, 1))()
     res = _lib.VideoResult(0, 0, ctypes.cast(starts, ctypes.POINTER(ctypes.c_int)),
                            ctypes.cast(lens, ctypes.POINTER(ctypes.c_int)))
-    _lib.check(_lib.load().scpl_retarget_video(_lib.ctx(clip.device.index), clip.data_ptr(), T, H, W, C,
-                                               ctypes.byref(params), out.data_ptr(), ctypes.byref(res),
-                                               _lib.stream()))
+    fn = _lib.load().scpl_retarget_video_host if host else _lib.load().scpl_retarget_video
+    dev = torch.cuda.current_device() if host else clip.device.index
+    _lib.check(fn(_lib.ctx(dev), clip.data_ptr(), T, H, W, C, ctypes.byref(params), out.data_ptr(),
+                  ctypes.byref(res), _lib.stream()))
     runs = [(starts[i], lens[i]) for i in range(res.n_runs)]
     global last_phase_ms
     last_phase_ms = dict(zip(("codes", "scan", "carve", "replay"), (float(x) for x in res.phase_ms)))
@@ -123,7 +137,7 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int):
 last_phase_ms: dict = {}   # device time per phase of the last clip (bench instrumentation)
 
 
-def retarget_video_tensor(clip, config: RetargetConfig):
+def retarget_video_tensor(clip, config: RetargetConfig, out=None):
     """Device-resident variant: clip is a CUDA uint8 tensor (T,H,W[,C]); returns (tensor, RunMetrics)."""
     start = time.perf_counter()
     if clip.dim() not in (3, 4):
@@ -136,26 +150,38 @@ def retarget_video_tensor(clip, config: RetargetConfig):
     H, W = clip.shape[1:3]
     tw = _resolve_target(W, config.target_width, "width")
     th = _resolve_target(H, config.target_height, "height")
-    out, dp, runs = _run_device(clip.contiguous(), config, tw, th)
-    if clip.dim() == 3:
+    out, dp, runs = _run_device(clip.contiguous(), config, tw, th, out=out)
+    if clip.dim() == 3 and out.dim() == 4:
         out = out[..., 0]
     return out, RunMetrics(dp_passes=dp, wall_time=time.perf_counter() - start, frames_out=T, runs=runs)
 
 
-def _retarget_host_tensor(clip, config: RetargetConfig):
-    """Host (ideally pinned) uint8 tensor (T,H,W[,C]) in, host tensor out: H2D, carve, D2H."""
-    torch = _lib.torch_cuda()
+def _retarget_host_tensor(clip, config: RetargetConfig, out=None):
+    """Host (ideally pinned) uint8 tensor (T,H,W[,C]) in, host tensor out (pinned, or `out`).
+
+    The host<->device copies overlap the kernels inside libscpl (scpl_retarget_video_host)."""
     start = time.perf_counter()
-    dev = clip.cuda(non_blocking=clip.is_pinned())
-    out, m = retarget_video_tensor(dev, config)
-    host = torch.empty(out.shape, dtype=torch.uint8, pin_memory=True)
-    host.copy_(out)
-    m.wall_time = time.perf_counter() - start
-    return host, m
+    if clip.dim() not in (3, 4):
+        raise ValueError(f"expected a (T, H, W[, C]) clip, got shape {tuple(clip.shape)}")
+    T = clip.shape[0]
+    if T == 0:
+        return clip[:0], RunMetrics(0, time.perf_counter() - start, 0)
+    _check_carvable(clip[0])
+    _channels(tuple(clip.shape[1:]))
+    H, W = clip.shape[1:3]
+    tw = _resolve_target(W, config.target_width, "width")
+    th = _resolve_target(H, config.target_height, "height")
+    res, dp, runs = _run_device(clip.contiguous(), config, tw, th, out=out)
+    if clip.dim() == 3 and res.dim() == 4:
+        res = res[..., 0]
+    return res, RunMetrics(dp_passes=dp, wall_time=time.perf_counter() - start, frames_out=T, runs=runs)
 
 
-def retarget_video(frames: Iterable[np.ndarray], config: RetargetConfig):
-    """pipeline.py:92-137: carve a stream of frames; output count always equals input count."""
+def retarget_video(frames: Iterable[np.ndarray], config: RetargetConfig, out=None):
+    """pipeline.py:92-137: carve a stream of frames; output count always equals input count.
+
+    `out` (extension): a preallocated output tensor for tensor inputs (pinned host tensor for a
+    host clip, CUDA tensor for a CUDA clip)."""
     torch = None
     try:
         import torch  # noqa: F401
@@ -163,8 +189,8 @@ def retarget_video(frames: Iterable[np.ndarray], config: RetargetConfig):
         pass
     if torch is not None and isinstance(frames, torch.Tensor):
         if frames.is_cuda:
-            return retarget_video_tensor(frames, config)
-        return _retarget_host_tensor(frames, config)
+            return retarget_video_tensor(frames, config, out=out)
+        return _retarget_host_tensor(frames, config, out=out)
     start = time.perf_counter()
     arrs = []
     shape = None
@@ -193,12 +219,9 @@ def retarget_video(frames: Iterable[np.ndarray], config: RetargetConfig):
     hv = host.numpy()
     for t, a in enumerate(arrs):
         hv[t] = a
-    clip = host.cuda(non_blocking=True)
-    if clip.dim() == 3:
-        clip = clip.unsqueeze(-1)
-    out, dp, runs = _run_device(clip, config, tw, th)
-    res = torch.empty(out.shape, dtype=torch.uint8, pin_memory=True)
-    res.copy_(out)
+    if host.dim() == 3:
+        host = host.unsqueeze(-1)
+    res, dp, runs = _run_device(host, config, tw, th)
     rv = res.numpy()
     if arrs[0].ndim == 2:
         rv = rv[..., 0]

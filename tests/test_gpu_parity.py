@@ -217,3 +217,38 @@ def test_config_clip_golden(P, path):
     assert list(host.shape[1:]) == g["out_shape"]
     bad = [t for t in range(host.shape[0]) if sha(host[t]) != g["frames_sha"][t]]
     assert not bad, f"{len(bad)} frames differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("path", _config_golden("C2") + _config_golden("C4_clip0") + _config_golden("C5"))
+def test_config_clip_golden_host_buffers(P, path):
+    """scpl_retarget_video_host (chunked H2D overlapped with the scan, per-run D2H) vs the reference."""
+    from paper_1903_03180_b200.synth import config_clip
+    import torch
+    g = json.load(open(path))
+    clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
+    host_in = torch.from_numpy(clip).pin_memory()
+    out = torch.full((clip.shape[0],) + tuple(g["out_shape"]), 7, dtype=torch.uint8).pin_memory()
+    res, m = P.retarget_video(host_in, P.RetargetConfig(target_width=tw, target_height=th, mode="buffered"), out=out)
+    assert res.data_ptr() == out.data_ptr() and not res.is_cuda
+    assert [list(r) for r in m.runs] == g["runs"]
+    assert m.dp_passes == g["dp_passes"]
+    host = res.numpy()
+    bad = [t for t in range(host.shape[0]) if sha(host[t]) != g["frames_sha"][t]]
+    assert not bad, f"{len(bad)} frames differ, first {bad[:5]}"
+
+
+def test_host_buffers_unpinned_and_odd_chunks(P):
+    """Unpinned host clip whose length is not a multiple of the 16-frame H2D chunk."""
+    import torch
+    rng = np.random.default_rng(77)
+    clip = rng.integers(0, 256, size=(37, 24, 40, 3), dtype=np.uint8)
+    clip[10:20] = clip[10]
+    cfg = P.RetargetConfig(target_width=29, target_height=21, mode="buffered")
+    a, ma = P.retarget_video(torch.from_numpy(clip), cfg)
+    b, mb = P.retarget_video_tensor(torch.from_numpy(clip).cuda(), cfg)
+    assert ma.runs == mb.runs and ma.dp_passes == mb.dp_passes
+    assert torch.equal(a, b.cpu())
+    from oracle import scpl_oracle as O
+    r = O.retarget_video(list(clip), target_width=29, target_height=21, mode="buffered")
+    assert r.dp_passes == ma.dp_passes
+    assert all(np.array_equal(a[t].numpy(), r.frames[t]) for t in range(len(clip)))
