@@ -44,6 +44,14 @@ struct scpl_ctx {
   double* h_asde = nullptr;  // pinned
   int h_asde_cap = 0;
   std::map<long, PwPlan> plans;
+  // device-side buffer scan
+  ScanState* scan = nullptr;                       // device
+  ScanState* h_scan = nullptr;                     // pinned readback
+  int* h_runs = nullptr;                           // pinned, 2 * h_runs_cap ints
+  int h_runs_cap = 0;
+  double* phi_d = nullptr;
+  std::vector<double> phi_h;                       // contents of phi_d
+  std::map<std::pair<long, int>, cudaGraphExec_t> scan_graphs;  // (N, spec)
 };
 
 namespace {
@@ -118,59 +126,81 @@ double* pinned_asde(scpl_ctx* ctx, int n) {
 }
 
 // ------------------------------------------------------------------ buffer scan
-// SpatioTemporalBuffer.push/flush over the whole clip (buffering.py:93-138).
-template <class Ready>
+// SpatioTemporalBuffer.push/flush over the whole clip (buffering.py:93-138), decided on
+// the device: one graph launch runs the scan as far as the frames whose codes are on the
+// device allow (a conditional while node around stats -> fold -> decide), so the host
+// never waits on an ASDE.  feed(c) makes chunk c's codes visible to `st` and returns the
+// number of frames available; chunks = number of feed calls (1 for a device clip).
+template <class Feed>
 std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* codes, int T, int H, int W,
-                                             const scpl_video_params& P, cudaStream_t st, Ready&& ensure_codes) {
+                                             const scpl_video_params& P, cudaStream_t st, int chunks,
+                                             Feed&& feed) {
   std::vector<std::pair<int, int>> runs;
   if (T == 0) return runs;
   const long N = (long)H * W;
   const PwPlan& plan = plan_for(ctx, N);
-  int spec = P.spec_len > 0 ? P.spec_len : 8;
+  const int spec = P.spec_len > 0 ? P.spec_len : 8;
+  SCPL_ARG(spec <= 64, "spec_len must be <= 64");
+  if (!ctx->scan) {
+    SCPL_CUDA(cudaMalloc(&ctx->scan, sizeof(ScanState)));
+    SCPL_CUDA(cudaMallocHost(&ctx->h_scan, sizeof(ScanState)));
+  }
+  if (ctx->h_runs_cap < T) {
+    if (ctx->h_runs) cudaFreeHost(ctx->h_runs);
+    ctx->h_runs = nullptr;
+    SCPL_CUDA(cudaMallocHost(&ctx->h_runs, sizeof(int) * 2 * T));
+    ctx->h_runs_cap = T;
+  }
+  std::vector<double> phi(P.phi, P.phi + P.max_len + 1);
+  if (phi != ctx->phi_h) {
+    if (ctx->phi_h.size() < phi.size()) {
+      if (ctx->phi_d) cudaFree(ctx->phi_d);
+      ctx->phi_d = nullptr;
+      SCPL_CUDA(cudaMalloc(&ctx->phi_d, sizeof(double) * phi.size()));
+    }
+    SCPL_CUDA(cudaMemcpy(ctx->phi_d, phi.data(), sizeof(double) * phi.size(), cudaMemcpyHostToDevice));
+    ctx->phi_h = phi;
+  }
+  auto key = std::make_pair(N, spec);
+  auto it = ctx->scan_graphs.find(key);
+  if (it == ctx->scan_graphs.end())
+    it = ctx->scan_graphs.emplace(key, build_scan_graph(ctx->scan, plan.leaves, plan.nleaves, plan.vnodes, spec))
+             .first;
   DBuf ck(sizeof(double) * 2 * N, st);
   DBuf leafsum(sizeof(double) * spec * plan.nleaves, st);
-  DBuf asde_d(sizeof(double) * spec, st);
-  double* h = pinned_asde(ctx, spec);
-  int s = 0, n_acc = 1;
-  bool init = true;
-  while (true) {
-    int remaining = T - (s + n_acc);
-    if (remaining == 0) {
-      runs.push_back({s, n_acc});
-      break;
-    }
-    if (n_acc >= P.max_len) {  // the next push would exceed the cap: flush (buffering.py:119)
-      runs.push_back({s, n_acc});
-      s += n_acc;
-      n_acc = 1;
-      init = true;
-      continue;
-    }
-    int L = std::min(spec, std::min(remaining, P.max_len - n_acc));
-    ensure_codes(s + n_acc + L - 1);  // codes of every frame this launch reads are on the stream
-    launch_window_stats(codes, N, plan.leaves, plan.nleaves, s, n_acc, L, 1, init ? 1 : 0, P.w_motion,
-                        P.w_grad, ck.as<double>(), ck.as<double>() + N, leafsum.as<double>(), plan.vnodes,
-                        asde_d.as<double>(), st);
-    SCPL_CUDA(cudaMemcpyAsync(h, asde_d.p, sizeof(double) * L, cudaMemcpyDeviceToHost, st));
-    SCPL_CUDA(cudaStreamSynchronize(st));
-    int breach = -1;
-    for (int c = 0; c < L; ++c) {
-      int n = n_acc + c + 1;
-      if (!(h[c] <= P.phi[n])) {  // asde <= threshold(n) and n <= max_len (buffering.py:119)
-        breach = c;
-        break;
-      }
-    }
-    if (breach < 0) {
-      n_acc += L;
-      init = false;
-    } else {
-      runs.push_back({s, n_acc + breach});
-      s = s + n_acc + breach;
-      n_acc = 1;
-      init = true;
-    }
+  DBuf partial(sizeof(double) * spec * kPwFoldCtas, st);
+  DBuf runs_d(sizeof(int) * 2 * T, st);
+  ScanState init{};
+  init.codes = codes;
+  init.N = N;
+  init.ckS = ck.as<double>();
+  init.ckQ = ck.as<double>() + N;
+  init.leafsum = leafsum.as<double>();
+  init.partial = partial.as<double>();
+  init.phi = ctx->phi_d;
+  init.runs = runs_d.as<int>();
+  init.wm = P.w_motion;
+  init.wg = P.w_grad;
+  init.T = T;
+  init.max_len = P.max_len;
+  init.spec = spec;
+  init.avail = 0;
+  init.s = 0;
+  init.n_acc = 1;
+  init.init = 1;
+  launch_scan_reset(ctx->scan, init, st);
+  for (int c = 0; c < chunks; ++c) {
+    const int avail = feed(c);
+    launch_scan_avail(ctx->scan, avail, st);
+    SCPL_CUDA(cudaGraphLaunch(it->second, st));
   }
+  SCPL_CUDA(cudaMemcpyAsync(ctx->h_scan, ctx->scan, sizeof(ScanState), cudaMemcpyDeviceToHost, st));
+  SCPL_CUDA(cudaMemcpyAsync(ctx->h_runs, runs_d.p, sizeof(int) * 2 * T, cudaMemcpyDeviceToHost, st));
+  SCPL_CUDA(cudaStreamSynchronize(st));
+  const ScanState& R = *ctx->h_scan;
+  if (!(R.done == 1 && R.nruns >= 1 && R.nruns <= T)) throw Error{2, "buffer scan did not finish"};
+  g_launches.fetch_add((long)chunks + 3L * R.steps, std::memory_order_relaxed);
+  for (int r = 0; r < R.nruns; ++r) runs.push_back({ctx->h_runs[2 * r], ctx->h_runs[2 * r + 1]});
   return runs;
 }
 
@@ -319,6 +349,11 @@ void scpl_destroy(scpl_ctx* ctx) {
     cudaFree(kv.second.vnodes);
   }
   if (ctx->h_asde) cudaFreeHost(ctx->h_asde);
+  for (auto& kv : ctx->scan_graphs) cudaGraphExecDestroy(kv.second);
+  if (ctx->scan) cudaFree(ctx->scan);
+  if (ctx->h_scan) cudaFreeHost(ctx->h_scan);
+  if (ctx->h_runs) cudaFreeHost(ctx->h_runs);
+  if (ctx->phi_d) cudaFree(ctx->phi_d);
   for (cudaStream_t x : {ctx->s_h2d, ctx->s_codes, ctx->s_d2h})
     if (x) cudaStreamDestroy(x);
   delete ctx;
@@ -363,9 +398,11 @@ int scpl_window_asde(scpl_ctx* ctx, const uint16_t* codes, int T, int h, int w, 
     const long N = (long)h * w;
     const PwPlan& plan = plan_for(ctx, N);
     DBuf leafsum(sizeof(double) * count * plan.nleaves, st);
+    DBuf partial(sizeof(double) * count * kPwFoldCtas, st);
     DBuf asde_d(sizeof(double) * count, st);
     launch_window_stats(codes, N, plan.leaves, plan.nleaves, start, n_acc, count, 1, init, w_motion, w_grad,
-                        state, state + N, leafsum.as<double>(), plan.vnodes, asde_d.as<double>(), st);
+                        state, state + N, leafsum.as<double>(), plan.vnodes, partial.as<double>(),
+                        asde_d.as<double>(), st);
     SCPL_CUDA(cudaMemcpyAsync(asde_out, asde_d.p, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
     SCPL_CUDA(cudaStreamSynchronize(st));
   });
@@ -517,11 +554,16 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     const int c = std::min(nchunk - 1, t_max / chunk);
     while (codes_ready < c) SCPL_CUDA(cudaStreamWaitEvent(st, ev_codes[++codes_ready], 0));
   };
+  auto feed = [&](int c) {  // chunk c of the scan: frames [0, avail) have codes on st
+    if (!host_in) return T;
+    ensure_codes(c * chunk);
+    return std::min(T, (c + 1) * chunk);
+  };
   SCPL_CUDA(cudaEventRecord(ev[1], st));
   // 2. runs
   std::vector<std::pair<int, int>> runs;
   if (P.mode == 2) {
-    runs = buffer_scan(ctx, codes.as<uint16_t>(), T, h, w, P, st, ensure_codes);
+    runs = buffer_scan(ctx, codes.as<uint16_t>(), T, h, w, P, st, host_in ? nchunk : 1, feed);
   } else {
     for (int t = 0; t < T; ++t) runs.push_back({t, 1});
   }
@@ -702,8 +744,10 @@ int scpl_asde_from_sums(scpl_ctx* ctx, const double* S, const double* Q, long N,
     SCPL_ARG(N >= 1 && n >= 1, "empty buffer");
     const PwPlan& plan = plan_for(ctx, N);
     DBuf leafsum(sizeof(double) * plan.nleaves, st);
+    DBuf partial(sizeof(double) * kPwFoldCtas, st);
     DBuf d(sizeof(double), st);
-    launch_asde_sums(S, Q, N, n, plan.leaves, plan.nleaves, plan.vnodes, leafsum.as<double>(), d.as<double>(), st);
+    launch_asde_sums(S, Q, N, n, plan.leaves, plan.nleaves, plan.vnodes, leafsum.as<double>(), partial.as<double>(),
+                     d.as<double>(), st);
     SCPL_CUDA(cudaMemcpyAsync(out, d.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     SCPL_CUDA(cudaStreamSynchronize(st));
   });

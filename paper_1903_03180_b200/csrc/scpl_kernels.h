@@ -8,7 +8,8 @@
 
 namespace scpl {
 
-constexpr int kPwDepth = 10;   // virtual complete tree depth for the pairwise fold
+constexpr int kPwDepth = 14;   // virtual complete tree depth for the pairwise fold
+constexpr int kPwFoldCtas = 16;  // CTAs per candidate folding one depth-10 subtree each
 constexpr int kBlockRows = 16; // DP rows per 32-bit path word (2 bits per row)
 
 struct PwVnode {
@@ -27,7 +28,27 @@ void launch_sobel_f64(const uint8_t* luma, int H, int W, double* out, cudaStream
 
 void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int nleaves, int s, int n_acc,
                          int L, int first_pure, int init, double wm, double wg, double* ckS, double* ckQ,
-                         double* leafsum, const PwVnode* vnodes, double* asde_out, cudaStream_t st);
+                         double* leafsum, const PwVnode* vnodes, double* partial, double* asde_out,
+                         cudaStream_t st);
+// leaf sums (L x nleaves) -> L ASDE values; partial holds L x kPwFoldCtas doubles
+void launch_pairwise_fold(const double* leafsum, int nleaves, const PwVnode* vnodes, long N, int L,
+                          double* partial, double* out, cudaStream_t st);
+
+// Device-side buffer scan state (scpl_stats.cu).  runs holds (start, len) pairs.
+struct ScanState {
+  const uint16_t* codes;
+  long N;
+  double *ckS, *ckQ, *leafsum, *partial;
+  const double* phi;  // threshold(n), n = 0..max_len
+  int* runs;
+  double wm, wg;
+  int T, max_len, spec, avail;
+  int s, n_acc, init, L, done, nruns;
+  int steps;  // loop-body executions (3 kernels each)
+};
+cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec);
+void launch_scan_reset(ScanState* S, const ScanState& init, cudaStream_t st);
+void launch_scan_avail(ScanState* S, int avail, cudaStream_t st);
 void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
                     int transposed, double* out, cudaStream_t st, int pitch = 0);
 
@@ -85,6 +106,6 @@ void launch_sums(const double* e, long N, const double* S_in, const double* Q_in
                  cudaStream_t st);
 void launch_sums_map(const double* S, const double* Q, long N, int n, int what, double* out, cudaStream_t st);
 void launch_asde_sums(const double* S, const double* Q, long N, int n, const int2* leaves, int nleaves,
-                      const PwVnode* vnodes, double* leafsum, double* out, cudaStream_t st);
+                      const PwVnode* vnodes, double* leafsum, double* partial, double* out, cudaStream_t st);
 
 }  // namespace scpl

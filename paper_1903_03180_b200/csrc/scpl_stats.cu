@@ -67,7 +67,7 @@ void build_pairwise_plan(long N, std::vector<int2>& leaves, std::vector<PwVnode>
 // ------------------------------------------------------------ device: leaf sums
 constexpr int kMaxPerLane = 16;  // 128 / 8
 
-__global__ void __launch_bounds__(256) window_stats_kernel(const uint16_t* __restrict__ codes, long N,
+__device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ codes, long N,
                                                            const int2* __restrict__ leaves, int nleaves,
                                                            int s, int n_acc, int L, int first_pure, int init,
                                                            double wm, double wg, double* __restrict__ ckS,
@@ -160,7 +160,30 @@ __global__ void __launch_bounds__(256) window_stats_kernel(const uint16_t* __res
   }
 }
 
+__global__ void __launch_bounds__(256) window_stats_kernel(const uint16_t* __restrict__ codes, long N,
+                                                           const int2* __restrict__ leaves, int nleaves,
+                                                           int s, int n_acc, int L, int first_pure, int init,
+                                                           double wm, double wg, double* __restrict__ ckS,
+                                                           double* __restrict__ ckQ,
+                                                           double* __restrict__ leafsum) {
+  window_stats_body(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init, wm, wg, ckS, ckQ, leafsum);
+}
+
+// Scan variant: the window comes from the device-side scan state (no host round trip).
+__global__ void __launch_bounds__(256) window_stats_scan_kernel(const ScanState* __restrict__ S,
+                                                                const int2* __restrict__ leaves, int nleaves) {
+  const int L = S->L;
+  if (L <= 0) return;
+  window_stats_body(S->codes, S->N, leaves, nleaves, S->s, S->n_acc, L, 1, S->init, S->wm, S->wg, S->ckS,
+                    S->ckQ, S->leafsum);
+}
+
 // ------------------------------------------------------------ device: tree fold
+// The leaf sums are folded along a virtual complete tree of depth kPwDepth over numpy's
+// recursion (build_pairwise_plan): node v's value is the pairwise sum of its subtree, an
+// empty node adds +0.0 (exact for the non-negative sums here).  kPwFoldCtas CTAs per
+// candidate each fold one complete subtree of depth kPwDepth - kPwTop to a partial; the
+// root folds the kPwFoldCtas partials (again a complete tree, so the bracketing is numpy's).
 __device__ double pw_eval(long n, const double* __restrict__ ls, int& li) {
   if (n <= 128) return ls[li++];
   long h = n / 2;
@@ -170,14 +193,23 @@ __device__ double pw_eval(long n, const double* __restrict__ ls, int& li) {
   return __dadd_rn(a, b);
 }
 
-__global__ void __launch_bounds__(1024) pairwise_fold_kernel(const double* __restrict__ leafsum, int nleaves,
-                                                             const PwVnode* __restrict__ vnodes, long N,
-                                                             double* __restrict__ asde_out) {
-  __shared__ double v[1 << kPwDepth];
-  const int c = blockIdx.x;
+constexpr int kPwSub = (1 << kPwDepth) / kPwFoldCtas;  // vnodes per CTA
+
+// grid (kPwFoldCtas, L or max L); Lp (device) overrides the candidate count when given
+__global__ void __launch_bounds__(256) fold_partial_kernel(const double* leafsum, int nleaves,
+                                                           const PwVnode* __restrict__ vnodes, double* partial,
+                                                           const ScanState* Sp) {
+  __shared__ double v[kPwSub];
+  const int c = blockIdx.y;
+  if (Sp != nullptr) {
+    if (c >= Sp->L) return;
+    leafsum = Sp->leafsum;
+    partial = Sp->partial;
+  }
   const double* ls = leafsum + (size_t)c * nleaves;
-  for (int t = threadIdx.x; t < (1 << kPwDepth); t += blockDim.x) {
-    PwVnode vn = vnodes[t];
+  const int v0 = blockIdx.x * kPwSub;
+  for (int t = threadIdx.x; t < kPwSub; t += blockDim.x) {
+    PwVnode vn = vnodes[v0 + t];
     double x = 0.0;
     if (vn.n > 0) {
       int li = vn.first_leaf;
@@ -186,24 +218,171 @@ __global__ void __launch_bounds__(1024) pairwise_fold_kernel(const double* __res
     v[t] = x;
   }
   __syncthreads();
-  // fold the complete tree in place at the left child's slot: v[2ts] = v[2ts] + v[2ts+s]
-  for (int s = 1; s < (1 << kPwDepth); s <<= 1) {
-    for (int t = threadIdx.x; t < ((1 << kPwDepth) >> 1) / s; t += blockDim.x)
+  // fold in place at the left child's slot: v[2ts] = v[2ts] + v[2ts+s]
+  for (int s = 1; s < kPwSub; s <<= 1) {
+    for (int t = threadIdx.x; t < (kPwSub >> 1) / s; t += blockDim.x)
       v[2 * t * s] = __dadd_rn(v[2 * t * s], v[2 * t * s + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) asde_out[c] = __ddiv_rn(__dadd_rn(0.0, v[0]), (double)N);
+  if (threadIdx.x == 0) partial[(size_t)c * kPwFoldCtas + blockIdx.x] = v[0];
+}
+
+__device__ __forceinline__ double fold_root(const double* partial, int c, long N) {
+  double v[kPwFoldCtas];
+#pragma unroll
+  for (int k = 0; k < kPwFoldCtas; ++k) v[k] = partial[(size_t)c * kPwFoldCtas + k];
+#pragma unroll
+  for (int s = 1; s < kPwFoldCtas; s <<= 1)
+#pragma unroll
+    for (int k = 0; k < kPwFoldCtas; k += 2 * s) v[k] = __dadd_rn(v[k], v[k + s]);
+  return __ddiv_rn(__dadd_rn(0.0, v[0]), (double)N);
+}
+
+__global__ void fold_root_kernel(const double* __restrict__ partial, int L, long N, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < L) out[c] = fold_root(partial, c, N);
+}
+
+void launch_pairwise_fold(const double* leafsum, int nleaves, const PwVnode* vnodes, long N, int L,
+                          double* partial, double* out, cudaStream_t st) {
+  fold_partial_kernel<<<dim3(kPwFoldCtas, L), 256, 0, st>>>(leafsum, nleaves, vnodes, partial, nullptr);
+  SCPL_CHECK_LAUNCH();
+  fold_root_kernel<<<cdiv(L, 64), 64, 0, st>>>(partial, L, N, out);
+  SCPL_CHECK_LAUNCH();
 }
 
 void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int nleaves, int s, int n_acc,
                          int L, int first_pure, int init, double wm, double wg, double* ckS, double* ckQ,
-                         double* leafsum, const PwVnode* vnodes, double* asde_out, cudaStream_t st) {
+                         double* leafsum, const PwVnode* vnodes, double* partial, double* asde_out,
+                         cudaStream_t st) {
   int threads = 256;
   int blocks = cdiv((long)nleaves * 8, threads);
   window_stats_kernel<<<blocks, threads, 0, st>>>(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init, wm,
                                                   wg, ckS, ckQ, leafsum);
   SCPL_CHECK_LAUNCH();
-  pairwise_fold_kernel<<<L, 1024, 0, st>>>(leafsum, nleaves, vnodes, N, asde_out);
+  launch_pairwise_fold(leafsum, nleaves, vnodes, N, L, partial, asde_out, st);
+}
+
+// ------------------------------------------------------------ device-side buffer scan
+// SpatioTemporalBuffer.push/flush (buffering.py:93-138) as a state machine in device
+// memory: plan the next window of candidates, or consume the latest ASDEs and decide.
+// Candidate n is accepted while asde(n) <= threshold(n) (buffering.py:119); a breach
+// closes the run before the offending frame, which starts the next run.  A window never
+// reaches past `avail` (frames whose codes are on the device), so the host can feed the
+// clip in chunks; the ASDE of a length is independent of how the lengths were chunked.
+__device__ void scan_plan(ScanState* S) {
+  while (!S->done) {
+    const int remaining = S->T - (S->s + S->n_acc);
+    if (remaining == 0) {  // end of clip: flush (pipeline.py:131-133)
+      S->runs[2 * S->nruns] = S->s;
+      S->runs[2 * S->nruns + 1] = S->n_acc;
+      S->nruns++;
+      S->done = 1;
+      break;
+    }
+    if (S->n_acc >= S->max_len) {  // the next push would exceed the cap: flush
+      S->runs[2 * S->nruns] = S->s;
+      S->runs[2 * S->nruns + 1] = S->n_acc;
+      S->nruns++;
+      S->s += S->n_acc;
+      S->n_acc = 1;
+      S->init = 1;
+      continue;
+    }
+    int L = min(S->spec, min(remaining, S->max_len - S->n_acc));
+    L = min(L, S->avail - (S->s + S->n_acc));
+    if (L <= 0) break;  // wait for more frames
+    S->L = L;
+    return;
+  }
+  S->L = 0;
+}
+
+// One thread per candidate folds its root; thread 0 then decides and plans the next window.
+__global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, int decide) {
+  __shared__ double asde[64];
+  const int L = S->L;
+  if (decide && L > 0) {
+    for (int c = threadIdx.x; c < L; c += blockDim.x) asde[c] = fold_root(S->partial, c, S->N);
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  if (decide && L > 0) {
+    int breach = -1;
+    for (int c = 0; c < L; ++c) {
+      if (!(asde[c] <= S->phi[S->n_acc + c + 1])) {
+        breach = c;
+        break;
+      }
+    }
+    if (breach < 0) {
+      S->n_acc += L;
+      S->init = 0;
+    } else {
+      S->runs[2 * S->nruns] = S->s;
+      S->runs[2 * S->nruns + 1] = S->n_acc + breach;
+      S->nruns++;
+      S->s += S->n_acc + breach;
+      S->n_acc = 1;
+      S->init = 1;
+    }
+    S->L = 0;
+    S->steps++;
+  }
+  scan_plan(S);
+  cudaGraphSetConditional(loop, S->L > 0 ? 1u : 0u);
+}
+
+__global__ void scan_reset_kernel(ScanState* S, ScanState init) { *S = init; }
+__global__ void scan_avail_kernel(ScanState* S, int avail) { S->avail = avail; }
+
+// graph: step(plan) -> while (L > 0) { stats -> fold partials -> step(decide + plan) }
+cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes,
+                                 int spec) {
+  SCPL_ARG(spec >= 1 && spec <= 64, "spec_len must be in 1..64");
+  cudaGraph_t g;
+  SCPL_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  SCPL_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  cudaStream_t cs;
+  SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  // head: plan
+  SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 0);
+  SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
+  SCPL_CUDA(cudaStreamEndCapture(cs, &g));
+  cudaGraphNode_t head;
+  size_t nn = 1;
+  SCPL_CUDA(cudaGraphGetNodes(g, &head, &nn));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond;
+  SCPL_CUDA(cudaGraphAddNode(&cond, g, &head, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  window_stats_scan_kernel<<<cdiv((long)nleaves * 8, 256), 256, 0, cs>>>(S, leaves, nleaves);
+  SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
+  fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, cs>>>(nullptr, nleaves, vnodes, nullptr, S);
+  SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
+  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 1);
+  SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
+  SCPL_CUDA(cudaStreamEndCapture(cs, &body));
+  cudaGraphExec_t ex;
+  SCPL_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return ex;
+}
+
+void launch_scan_reset(ScanState* S, const ScanState& init, cudaStream_t st) {
+  scan_reset_kernel<<<1, 1, 0, st>>>(S, init);
+  SCPL_CHECK_LAUNCH();
+}
+void launch_scan_avail(ScanState* S, int avail, cudaStream_t st) {
+  scan_avail_kernel<<<1, 1, 0, st>>>(S, avail);
   SCPL_CHECK_LAUNCH();
 }
 

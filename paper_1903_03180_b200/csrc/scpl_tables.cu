@@ -248,44 +248,11 @@ __global__ void sums_leaf_kernel(const double* __restrict__ S, const double* __r
   if (active && sub == 0) leafsum[leaf] = x;
 }
 
-__device__ double pw_eval2(long n, const double* __restrict__ ls, int& li) {
-  if (n <= 128) return ls[li++];
-  long h = n / 2;
-  h -= h % 8;
-  double a = pw_eval2(h, ls, li);
-  double b = pw_eval2(n - h, ls, li);
-  return __dadd_rn(a, b);
-}
-
-__global__ void __launch_bounds__(1024) fold_one_kernel(const double* __restrict__ leafsum,
-                                                        const PwVnode* __restrict__ vnodes, long N,
-                                                        double* __restrict__ out) {
-  __shared__ double v[1 << kPwDepth];
-  for (int t = threadIdx.x; t < (1 << kPwDepth); t += blockDim.x) {
-    PwVnode vn = vnodes[t];
-    double x = 0.0;
-    if (vn.n > 0) {
-      int li = vn.first_leaf;
-      x = pw_eval2(vn.n, leafsum, li);
-    }
-    v[t] = x;
-  }
-  __syncthreads();
-  // fold the complete tree in place at the left child's slot: v[2ts] = v[2ts] + v[2ts+s]
-  for (int s = 1; s < (1 << kPwDepth); s <<= 1) {
-    for (int t = threadIdx.x; t < ((1 << kPwDepth) >> 1) / s; t += blockDim.x)
-      v[2 * t * s] = __dadd_rn(v[2 * t * s], v[2 * t * s + s]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = __ddiv_rn(__dadd_rn(0.0, v[0]), (double)N);
-}
-
 void launch_asde_sums(const double* S, const double* Q, long N, int n, const int2* leaves, int nleaves,
-                      const PwVnode* vnodes, double* leafsum, double* out, cudaStream_t st) {
+                      const PwVnode* vnodes, double* leafsum, double* partial, double* out, cudaStream_t st) {
   sums_leaf_kernel<<<cdiv((long)nleaves * 8, 256), 256, 0, st>>>(S, Q, leaves, nleaves, n, leafsum);
   SCPL_CHECK_LAUNCH();
-  fold_one_kernel<<<1, 1024, 0, st>>>(leafsum, vnodes, N, out);
-  SCPL_CHECK_LAUNCH();
+  launch_pairwise_fold(leafsum, nleaves, vnodes, N, 1, partial, out, st);
 }
 
 }  // namespace scpl
