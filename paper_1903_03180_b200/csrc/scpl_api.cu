@@ -378,7 +378,7 @@ int scpl_energy_codes(scpl_ctx* ctx, const uint8_t* frames, const uint8_t* prev,
   return guarded(ctx, [&] {
     SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
     SCPL_ARG(h >= 3 && w >= 3, "frame too small for 3x3 Sobel");
-    launch_codes(frames, prev, T, h, w, channels, codes, ctx->num_sms, (cudaStream_t)stream);
+    launch_codes(frames, prev, 0, T, h, w, channels, codes, ctx->num_sms, (cudaStream_t)stream);
   });
 }
 
@@ -540,14 +540,13 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
       SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, e, 0));
       if (P.mode != 0)
-        launch_codes(frames + fbytes0 * t0, t0 > 0 ? frames + fbytes0 * (t0 - 1) : nullptr, n, h, w, C,
-                     codes.as<uint16_t>() + (size_t)t0 * h * w, ctx->num_sms, ctx->s_codes);
+        launch_codes(frames, nullptr, t0, n, h, w, C, codes.as<uint16_t>(), ctx->num_sms, ctx->s_codes);
       cudaEvent_t ec = new_event(false);
       SCPL_CUDA(cudaEventRecord(ec, ctx->s_codes));
       ev_codes.push_back(ec);
     }
   } else if (P.mode != 0) {
-    launch_codes(frames, nullptr, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, st);
+    launch_codes(frames, nullptr, 0, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, st);
   }
   int codes_ready = host_in ? -1 : nchunk - 1;  // chunks st already waits for
   auto ensure_codes = [&](int t_max) {

@@ -19,7 +19,9 @@ struct PwVnode {
 
 void build_pairwise_plan(long N, std::vector<int2>& leaves, std::vector<PwVnode>& vnodes);
 
-void launch_codes(const uint8_t* frames, const uint8_t* prev_frame, int T, int H, int W, int C,
+// codes of frames t0 .. t0+n-1 of the clip starting at `frames` into codes (frame 0 based);
+// the frame before t0 is frames[t0-1], or prev_frame (nullable) when t0 == 0
+void launch_codes(const uint8_t* frames, const uint8_t* prev_frame, int t0, int n, int H, int W, int C,
                   uint16_t* codes, int num_sms, cudaStream_t st);
 void launch_luma(const uint8_t* rgb, long npx, int C, uint8_t* out, cudaStream_t st);
 void launch_decode(const uint16_t* codes, long per_frame, int T, int first_pure, double wm, double wg,

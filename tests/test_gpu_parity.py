@@ -72,6 +72,34 @@ def test_energy_codes_random_frames_vs_oracle(P):
         assert np.array_equal(P.motion_energy(a, None), O.motion_energy(a, None)), (h, w)
 
 
+def test_energy_codes_clip_tiles_vs_oracle(P):
+    """RGB clips through the tiled codes kernel (TMA rows: W*3 % 16 == 0, and plain rows),
+    frame 0 pure gradient, then motion against the previous frame; also a chunk whose
+    previous frame comes from a separate pointer."""
+    import torch
+    from oracle import scpl_oracle as O
+    from paper_1903_03180_b200 import _lib
+    lib, cx, st = _lib.load(), _lib.ctx(), _lib.stream()
+    rng = np.random.default_rng(6)
+    for T, h, w in [(7, 70, 272), (5, 33, 130), (3, 161, 400), (4, 32, 128)]:
+        clip = rng.integers(0, 256, size=(T, h, w, 3), dtype=np.uint8)
+        clip[2] = clip[1] // 2 + 7  # some structure between frames
+        dev = torch.from_numpy(clip).cuda()
+        codes = torch.empty((T, h, w), dtype=torch.int16, device="cuda")
+        _lib.check(lib.scpl_energy_codes(cx, dev.data_ptr(), None, T, h, w, 3, codes.data_ptr(), st))
+        out = torch.empty((T, h, w), dtype=torch.float64, device="cuda")
+        _lib.check(lib.scpl_decode_energy(cx, codes.data_ptr(), T, h, w, 1, 0.6, 0.4, out.data_ptr(), st))
+        got = out.cpu().numpy()
+        for t in range(T):
+            ref = O.motion_energy(clip[t], clip[t - 1] if t else None)
+            assert np.array_equal(got[t], ref), (T, h, w, t)
+        # frames 2.. with the previous frame given separately
+        sub = dev[2:].contiguous()
+        c2 = torch.empty((T - 2, h, w), dtype=torch.int16, device="cuda")
+        _lib.check(lib.scpl_energy_codes(cx, sub.data_ptr(), dev[1].data_ptr(), T - 2, h, w, 3, c2.data_ptr(), st))
+        assert torch.equal(c2, codes[2:]), (T, h, w)
+
+
 # ------------------------------------------------------------------ DP / labels / batches
 def test_dp_labels_batches_golden(P, small):
     for s in cases.MAP_SEEDS:
