@@ -55,95 +55,140 @@ __device__ __forceinline__ int raw_off(int k, int x) {
   return b * G::kRegion + k * G::kBox + (x - b * G::kBox);
 }
 
-// luma of raw tile -> lum[kCRows][kLumStride], replicating the frame border
+// luma of 4 RGB pixels packed in 12 bytes (a, b, c), energy.py:35 exactly: X + 500 =
+// 256 (r + 2g) + (43 r + 75 g + 114 b) + 500 by byte dot products, the nearest integer of
+// X / 1000 is floor((X + 500) / 1000) = umulhi(X + 500, 4294968) (exact for X + 500 <
+// 256001, checked exhaustively); the rare ties X % 1000 == 500 take luma_of's fp64 path.
+__device__ __forceinline__ uint32_t luma_t(uint32_t px, uint32_t c_hi, uint32_t c_lo, uint32_t& rem) {
+  const uint32_t t = (__dp4a(px, c_hi, 0u) << 8) + __dp4a(px, c_lo, 500u);
+  const uint32_t q = __umulhi(t, 4294968u);
+  rem = t - q * 1000u;
+  return q;
+}
+__device__ __forceinline__ uint32_t luma4_rgb(uint32_t a, uint32_t b, uint32_t c) {
+  const uint32_t p1 = __byte_perm(a, b, 0x0543);  // r1 g1 b1 (a3 b0 b1)
+  const uint32_t p2 = __byte_perm(b, c, 0x0432);  // r2 g2 b2 (b2 b3 c0)
+  uint32_t m0, m1, m2, m3;
+  uint32_t q0 = luma_t(a, 0x00000201u, 0x00724B2Bu, m0);
+  uint32_t q1 = luma_t(p1, 0x00000201u, 0x00724B2Bu, m1);
+  uint32_t q2 = luma_t(p2, 0x00000201u, 0x00724B2Bu, m2);
+  uint32_t q3 = luma_t(c, 0x00020100u, 0x724B2B00u, m3);  // r3 g3 b3 = c1 c2 c3
+  if (__builtin_expect(m0 == 0u || m1 == 0u || m2 == 0u || m3 == 0u, 0)) {  // X % 1000 == 500
+    if (m0 == 0u) q0 = luma_of(a & 255u, (a >> 8) & 255u, (a >> 16) & 255u);
+    if (m1 == 0u) q1 = luma_of(a >> 24, b & 255u, (b >> 8) & 255u);
+    if (m2 == 0u) q2 = luma_of((b >> 16) & 255u, b >> 24, c & 255u);
+    if (m3 == 0u) q3 = luma_of((c >> 8) & 255u, (c >> 16) & 255u, c >> 24);
+  }
+  return __byte_perm(__byte_perm(q0, q1, 0x0040), __byte_perm(q2, q3, 0x0040), 0x5410);
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+}
+
+// luma of the pixel at raw column rp (0 .. kRawPx-1) of raw row rk
 template <int C>
-__device__ __forceinline__ void codes_luma(const uint8_t* raw, uint8_t* lum, int r0, int c0, int H, int W) {
-  constexpr int kGroups = kLumW / 4;  // 34 groups of 4 luma columns per row
-  for (int q = threadIdx.x; q < kCRows * kGroups; q += kCodesThreads) {
-    const int k = q / kGroups, g = q - k * kGroups;
-    const int gr = min(max(r0 - 1 + k, 0), H - 1);  // clamped frame row
-    const int rk = gr - (r0 - 1);                   // its raw row
-    const int px0 = c0 - 4 + 4 * g;                 // first pixel of the group
-    uint32_t word;
-    if (px0 >= 0 && px0 + 3 < W) {
-      const int x = (px0 - (c0 - 16)) * C;  // 4-byte aligned, never straddles a box
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(raw + raw_off<C>(rk, x));
-      if (C == 3) {
-        const uint32_t a = src[0], b = src[1], c = src[2];
-        const uint32_t l0 = luma_of(a & 255u, (a >> 8) & 255u, (a >> 16) & 255u);
-        const uint32_t l1 = luma_of(a >> 24, b & 255u, (b >> 8) & 255u);
-        const uint32_t l2 = luma_of((b >> 16) & 255u, b >> 24, c & 255u);
-        const uint32_t l3 = luma_of((c >> 8) & 255u, (c >> 16) & 255u, c >> 24);
-        word = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
-      } else {
-        word = src[0];
-      }
-    } else {  // frame border: clamped columns
-      word = 0;
-      for (int u = 0; u < 4; ++u) {
-        const int px = min(max(px0 + u, 0), W - 1);
-        const int x = (px - (c0 - 16)) * C;
-        uint32_t l;
-        if (px - (c0 - 16) < 0 || px - (c0 - 16) >= kRawPx) {
-          l = 0;  // outside the loaded box: never read by an in-frame output
-        } else if (C == 3) {
-          l = luma_of(raw[raw_off<C>(rk, x)], raw[raw_off<C>(rk, x + 1)], raw[raw_off<C>(rk, x + 2)]);
-        } else {
-          l = raw[raw_off<C>(rk, x)];
-        }
-        word |= l << (8 * u);
-      }
+__device__ __forceinline__ uint32_t raw_luma1(uint32_t raw_s, int rk, int rp) {
+  const int x = rp * C;
+  if (C == 3)
+    return luma_of(lds8(raw_s + raw_off<C>(rk, x)), lds8(raw_s + raw_off<C>(rk, x + 1)),
+                   lds8(raw_s + raw_off<C>(rk, x + 2)));
+  return lds8(raw_s + raw_off<C>(rk, x));
+}
+
+// luma of a raw tile -> lum[kCRows][kLumStride] (column index = pixel - (c0 - 4)):
+// warp = rows, lane = 4 columns c0 + 4 lane ..; then threads 0 .. 2*kCRows-1 add the halo
+// pixels c0 - 1 and c0 + 128 of every row.  Frame borders replicate: rows and columns are
+// clamped into the frame.  src0 = this lane's group in raw row 0 of the slot.
+template <int C>
+__device__ __forceinline__ void codes_luma(uint32_t raw_s, uint32_t src0, uint32_t lum_s, int r0, int c0, int H,
+                                           int W) {
+  using G = RawGeo<C>;
+  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+  const int px0 = c0 + 4 * lane;
+  const uint32_t dst0 = lum_s + 4 * lane + 4;
+  if (px0 + 3 < W) {
+#pragma unroll 1
+    for (int k = wy; k < kCRows; k += kCodesThreads / 32) {
+      const int rk = min(max(r0 - 1 + k, 0), H - 1) - (r0 - 1);  // clamped frame row
+      const uint32_t src = src0 + rk * G::kBox;
+      sts32(dst0 + k * kLumStride, C == 3 ? luma4_rgb(lds32(src), lds32(src + 4), lds32(src + 8)) : lds32(src));
     }
-    *reinterpret_cast<uint32_t*>(lum + k * kLumStride + 4 * g) = word;
+  } else {  // right frame border: clamped columns
+#pragma unroll 1
+    for (int k = wy; k < kCRows; k += kCodesThreads / 32) {
+      const int rk = min(max(r0 - 1 + k, 0), H - 1) - (r0 - 1);
+      uint32_t word = 0;
+      for (int u = 0; u < 4; ++u) word |= raw_luma1<C>(raw_s, rk, min(px0 + u, W - 1) - (c0 - 16)) << (8 * u);
+      sts32(dst0 + k * kLumStride, word);
+    }
+  }
+  if (threadIdx.x < 2 * kCRows) {
+    const int k = threadIdx.x >> 1, side = threadIdx.x & 1;
+    const int rk = min(max(r0 - 1 + k, 0), H - 1) - (r0 - 1);
+    const int px = min(max(side == 0 ? c0 - 1 : c0 + kCW, 0), W - 1);
+    sts8(lum_s + k * kLumStride + (side == 0 ? 3 : kCW + 4), raw_luma1<C>(raw_s, rk, px - (c0 - 16)));
   }
 }
 
-// codes of one frame for this thread's 4 rows x 4 columns; prev[i] = previous luma word
-__device__ __forceinline__ void codes_tile(const uint8_t* lum, uint32_t (&prev)[4], bool emit, bool have_prev,
+// codes of one frame for this thread's 4 rows x 4 columns; prev[i] = previous luma word.
+// Sobel in 16-bit lane pairs (even / odd columns): per luma row k, S_k = l + 2m + r
+// (horizontal smoothing) and D_k = r - l (+256 bias); then gx = D_a + 2 D_b + D_c and
+// gy = S_c - S_a (+1024 bias each), |g| = max(g', 2048 - g') - 1024 lane-wise, and
+// min(|gx| + |gy|, 255) -- the same integers as gradient_energy's int32 Sobel.
+// |dL| for 4 pixels is one byte-SIMD absolute difference.
+__device__ __forceinline__ void codes_tile(uint32_t lum_s, uint32_t (&prev)[4], bool emit, bool have_prev,
                                            int r0, int c0, int H, int W, uint16_t* __restrict__ out,
                                            bool vec_out) {
   const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
-  int v[6][6];  // [lum row 4wy .. 4wy+5][col -1 .. 4]
+  uint32_t SE[6], SO[6], DE[6], DO[6], M[6];  // rows stream through: at most 3 live at once
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
-    const uint32_t* row = reinterpret_cast<const uint32_t*>(lum + (4 * wy + k) * kLumStride);
-    const uint32_t lo = row[lane], mid = row[lane + 1], hi = row[lane + 2];
-    v[k][0] = lo >> 24;
-    v[k][1] = mid & 255;
-    v[k][2] = (mid >> 8) & 255;
-    v[k][3] = (mid >> 16) & 255;
-    v[k][4] = mid >> 24;
-    v[k][5] = hi & 255;
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int cs[6], cd[6];
-#pragma unroll
-    for (int u = 0; u < 6; ++u) {
-      cs[u] = v[i][u] + 2 * v[i + 1][u] + v[i + 2][u];
-      cd[u] = v[i + 2][u] - v[i][u];
-    }
-    const uint32_t cur = (uint32_t)v[i + 1][1] | ((uint32_t)v[i + 1][2] << 8) | ((uint32_t)v[i + 1][3] << 16) |
-                         ((uint32_t)v[i + 1][4] << 24);
-    uint32_t code[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int gx = cs[u + 2] - cs[u];
-      const int gy = cd[u] + 2 * cd[u + 1] + cd[u + 2];
-      const int g = min(abs(gx) + abs(gy), 255);
-      const int d = have_prev ? abs(v[i + 1][u + 1] - (int)((prev[i] >> (8 * u)) & 255u)) : 0;
-      code[u] = ((uint32_t)d << 8) | (uint32_t)g;
-    }
-    prev[i] = cur;
+    const uint32_t row = lum_s + (4 * wy + k) * kLumStride + 4 * lane;
+    const uint32_t lo = lds32(row), mid = lds32(row + 4), hi = lds32(row + 8);
+    const uint32_t wl = __byte_perm(lo, mid, 0x6543);  // columns -1 .. 2
+    const uint32_t wr = __byte_perm(mid, hi, 0x4321);  // columns 1 .. 4
+    const uint32_t le = __byte_perm(wl, 0, 0x4240), lo_ = __byte_perm(wl, 0, 0x4341);
+    const uint32_t me = __byte_perm(mid, 0, 0x4240), mo = __byte_perm(mid, 0, 0x4341);
+    const uint32_t re = __byte_perm(wr, 0, 0x4240), ro = __byte_perm(wr, 0, 0x4341);
+    SE[k] = le + 2u * me + re;
+    SO[k] = lo_ + 2u * mo + ro;
+    DE[k] = re + 0x01000100u - le;
+    DO[k] = ro + 0x01000100u - lo_;
+    M[k] = mid;
+    if (k < 2) continue;
+    const int i = k - 2;
+    const uint32_t gxe = DE[i] + 2u * DE[i + 1] + DE[i + 2], gxo = DO[i] + 2u * DO[i + 1] + DO[i + 2];
+    const uint32_t gye = SE[i + 2] + 0x04000400u - SE[i], gyo = SO[i + 2] + 0x04000400u - SO[i];
+    const uint32_t ae = __vmaxu2(gxe, 0x08000800u - gxe) + __vmaxu2(gye, 0x08000800u - gye) - 0x08000800u;
+    const uint32_t ao = __vmaxu2(gxo, 0x08000800u - gxo) + __vmaxu2(gyo, 0x08000800u - gyo) - 0x08000800u;
+    const uint32_t g = __byte_perm(__vminu2(ae, 0x00FF00FFu), __vminu2(ao, 0x00FF00FFu), 0x6240);
+    const uint32_t d = have_prev ? __vabsdiffu4(M[i + 1], prev[i]) : 0u;
+    prev[i] = M[i + 1];
+    const uint32_t w0 = __byte_perm(g, d, 0x5140), w1 = __byte_perm(g, d, 0x7362);
     const int r = r0 + 4 * wy + i, c = c0 + 4 * lane;
     if (emit && r < H) {
-      uint16_t* o = out + (size_t)r * W + c;
+      uint16_t* o = out + (size_t)i * W;  // out: this thread's first pixel
       if (vec_out && c + 3 < W) {
-        *reinterpret_cast<uint2*>(o) = make_uint2(code[0] | (code[1] << 16), code[2] | (code[3] << 16));
+        *reinterpret_cast<uint2*>(o) = make_uint2(w0, w1);
       } else {
+        const uint32_t v[4] = {w0 & 0xffffu, w0 >> 16, w1 & 0xffffu, w1 >> 16};
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (c + u < W) o[u] = (uint16_t)code[u];
+          if (c + u < W) o[u] = (uint16_t)v[u];
       }
     }
   }
@@ -180,6 +225,9 @@ __global__ void __launch_bounds__(kCodesThreads, 4) codes_kernel(const __grid_co
   __syncthreads();
   const bool vec_out = (W & 3) == 0;
   const size_t fpx = (size_t)H * W;
+  // this lane's 4-pixel group in raw row 0 of slot 0 (a group never straddles two boxes)
+  const int gx_ = (4 * (threadIdx.x & 31) + 16) * C, gb_ = gx_ / G::kBox;
+  const uint32_t src_lane = smem_u32(smem) + gb_ * G::kRegion + (gx_ - gb_ * G::kBox);
   uint32_t phase = 0;  // bit s: parity of slot s
   uint32_t seq = 0;    // frames consumed so far (slot = seq & 1)
 
@@ -222,10 +270,12 @@ __global__ void __launch_bounds__(kCodesThreads, 4) codes_kernel(const __grid_co
         phase ^= 1u << (seq & 1);
       }
       __syncthreads();  // plain fills visible
-      codes_luma<C>(raw(seq), lum, r0, c0, H, W);
+      codes_luma<C>(smem_u32(raw(seq)), src_lane + (seq & 1u) * G::kSlot, smem_u32(lum), r0, c0, H, W);
       __syncthreads();
       const int t = tb + q - 1;
-      codes_tile(lum, prev, q >= 1, q > 1 || have_prev0, r0, c0, H, W, codes + (size_t)t * fpx, vec_out);
+      codes_tile(smem_u32(lum), prev, q >= 1, q > 1 || have_prev0, r0, c0, H, W,
+                 codes + (size_t)t * fpx + (size_t)(r0 + 4 * (threadIdx.x >> 5)) * W + c0 + 4 * (threadIdx.x & 31),
+                 vec_out);
       __syncthreads();  // lum and raw(seq) free
     }
   }
