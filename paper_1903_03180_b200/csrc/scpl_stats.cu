@@ -65,65 +65,123 @@ void build_pairwise_plan(long N, std::vector<int2>& leaves, std::vector<PwVnode>
 }
 
 // ------------------------------------------------------------ device: leaf sums
+// A CTA's 32 leaves cover one contiguous pixel range (<= 4096 pixels).  The codes of every
+// frame a launch reads (the run's first frame when it starts a run, then the L candidates)
+// stream into an 8-stage shared-memory ring by 1-D TMA bulk copies issued up front, so the
+// fp64 work never waits on a global load; lanes then read their strided elements from
+// shared memory.  Rows of N not divisible by 8 fall back to cooperative plain copies.
 constexpr int kMaxPerLane = 16;  // 128 / 8
+constexpr int kStatStages = 8;
+constexpr int kStatStageBytes = 32 * 128 * 2;
+constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatStages;
 
 __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ codes, long N,
-                                                           const int2* __restrict__ leaves, int nleaves,
-                                                           int s, int n_acc, int L, int first_pure, int init,
-                                                           double wm, double wg, double* __restrict__ ckS,
-                                                           double* __restrict__ ckQ,
-                                                           double* __restrict__ leafsum) {
+                                                  const int2* __restrict__ leaves, int nleaves, int s, int n_acc,
+                                                  int L, int first_pure, int init, double wm, double wg,
+                                                  double* __restrict__ ckS, double* __restrict__ ckQ,
+                                                  double* __restrict__ leafsum) {
+  extern __shared__ __align__(128) uint8_t st_ring[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(st_ring + kStatStages * kStatStageBytes);
   __shared__ double A[256], B[256];
   for (int k = threadIdx.x; k < 256; k += blockDim.x) {
     A[k] = __dmul_rn(wm, (double)k);
     B[k] = __dmul_rn(wg, (double)k);
   }
-  __syncthreads();
+  const int first = blockIdx.x * (blockDim.x >> 3);
+  const int last = min(nleaves, first + (int)(blockDim.x >> 3)) - 1;
+  const long p_lo = leaves[first].x;
+  const int2 lf_last = leaves[last];
+  const int npx = (int)(lf_last.x + lf_last.y - p_lo);
+  const uint32_t bytes = (uint32_t)((npx * 2 + 15) & ~15);
+  const bool bulk = (N & 7) == 0;  // frame rows 16-byte aligned (leaf starts are multiples of 8)
+  const int M = L + (init ? 1 : 0);  // frames read: [s if init], s+n_acc .. s+n_acc+L-1
+  auto frame_of = [&](int i) { return init ? (i == 0 ? s : s + n_acc + i - 1) : s + n_acc + i; };
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kStatStages; ++k) mbar_init(&bars[k], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < M && i < kStatStages; ++i) {
+        mbar_arrive_tx(&bars[i], bytes);
+        bulk_g2s(st_ring + i * kStatStageBytes, codes + (size_t)frame_of(i) * N + p_lo, bytes, &bars[i]);
+      }
+    }
+  } else {
+    __syncthreads();
+  }
+  // stage i: wait for it (bulk) or fill it cooperatively (plain); returns its base
+  auto acquire = [&](int i) -> const uint16_t* {
+    uint8_t* st = st_ring + (i % kStatStages) * kStatStageBytes;
+    if (bulk) {
+      mbar_wait(&bars[i % kStatStages], (uint32_t)(i / kStatStages) & 1u);
+    } else {
+      const uint16_t* src = codes + (size_t)frame_of(i) * N + p_lo;
+      for (int q = threadIdx.x; q < npx; q += blockDim.x) reinterpret_cast<uint16_t*>(st)[q] = src[q];
+      __syncthreads();
+    }
+    return reinterpret_cast<const uint16_t*>(st);
+  };
+  // stage i fully consumed: refill it with frame i + kStatStages
+  auto release = [&](int i) {
+    __syncthreads();
+    if (bulk && threadIdx.x == 0 && i + kStatStages < M) {
+      const int j = i + kStatStages;
+      mbar_arrive_tx(&bars[j % kStatStages], bytes);
+      bulk_g2s(st_ring + (j % kStatStages) * kStatStageBytes, codes + (size_t)frame_of(j) * N + p_lo, bytes,
+               &bars[j % kStatStages]);
+    }
+  };
+
   const int lane = threadIdx.x & 31;
   const int sub = lane & 7;
   const int leaf = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const bool active = leaf < nleaves;
-  int2 lf = active ? leaves[leaf] : make_int2(0, 8);
+  int2 lf = active ? leaves[leaf] : make_int2((int)p_lo, 8);
   const int len = lf.y;
   const int nmain = len >> 3;    // elements per lane in the 8-accumulator region
   const int ntail = len & 7;     // sequential tail, element i = 8*nmain + k held by lane k
   const long base = lf.x;
+  const int lb = (int)(base - p_lo);  // leaf start within the CTA range
 
   double S[kMaxPerLane + 1], Q[kMaxPerLane + 1];
+  int ci = 0;  // next stage
+  if (init) {
+    const uint16_t* st = acquire(ci);
 #pragma unroll
-  for (int k = 0; k <= kMaxPerLane; ++k) {
-    long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
-    bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
-    if (valid) {
-      if (init) {
-        uint32_t c = codes[(size_t)s * N + p];
-        double e = energy_of(c, first_pure && s == 0, A, B);
-        S[k] = e;
-        Q[k] = __dmul_rn(e, e);
-      } else {
-        S[k] = ckS[p];
-        Q[k] = ckQ[p];
-      }
-    } else {
-      S[k] = 0.0;
-      Q[k] = 0.0;
+    for (int k = 0; k <= kMaxPerLane; ++k) {
+      const int o = (k < kMaxPerLane) ? lb + sub + 8 * k : lb + 8 * nmain + sub;
+      const bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
+      const double e = valid ? energy_of(st[o], first_pure && s == 0, A, B) : 0.0;
+      S[k] = e;
+      Q[k] = __dmul_rn(e, e);
+    }
+    release(ci++);
+  } else {
+#pragma unroll
+    for (int k = 0; k <= kMaxPerLane; ++k) {
+      const long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
+      const bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
+      S[k] = valid ? ckS[p] : 0.0;
+      Q[k] = valid ? ckQ[p] : 0.0;
     }
   }
 
-  for (int c = 0; c < L; ++c) {
+  for (int c = 0; c < L; ++c, ++ci) {
     const int t = s + n_acc + c;
     const int n = n_acc + c + 1;
     const double dn = (double)n;
     const double rn = __ddiv_rn(1.0, dn);
-    const uint16_t* ct = codes + (size_t)t * N;
+    const uint16_t* ct = acquire(ci);
     const bool pure = first_pure && t == 0;
     double acc = 0.0, tail = 0.0;
 #pragma unroll
     for (int k = 0; k <= kMaxPerLane; ++k) {
-      long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
-      bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
+      const int o = (k < kMaxPerLane) ? lb + sub + 8 * k : lb + 8 * nmain + sub;
+      const bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
       if (valid) {
-        double e = energy_of(ct[p], pure, A, B);
+        double e = energy_of(ct[o], pure, A, B);
         S[k] = __dadd_rn(S[k], e);
         Q[k] = __dadd_rn(Q[k], __dmul_rn(e, e));
         double m = div_small(S[k], dn, rn);
@@ -135,6 +193,7 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
           tail = sd;
       }
     }
+    release(ci);
     // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)): IEEE addition commutes, so xor-shuffles give
     // exactly numpy's bracketing.
     double x = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
@@ -176,6 +235,15 @@ __global__ void __launch_bounds__(256) window_stats_scan_kernel(const ScanState*
   if (L <= 0) return;
   window_stats_body(S->codes, S->N, leaves, nleaves, S->s, S->n_acc, L, 1, S->init, S->wm, S->wg, S->ckS,
                     S->ckQ, S->leafsum);
+}
+
+static void stats_smem_attr() {
+  static bool done = false;
+  if (done) return;
+  SCPL_CUDA(cudaFuncSetAttribute(window_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStatSmem));
+  SCPL_CUDA(cudaFuncSetAttribute(window_stats_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kStatSmem));
+  done = true;
 }
 
 // ------------------------------------------------------------ device: tree fold
@@ -257,8 +325,9 @@ void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int 
                          cudaStream_t st) {
   int threads = 256;
   int blocks = cdiv((long)nleaves * 8, threads);
-  window_stats_kernel<<<blocks, threads, 0, st>>>(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init, wm,
-                                                  wg, ckS, ckQ, leafsum);
+  stats_smem_attr();
+  window_stats_kernel<<<blocks, threads, kStatSmem, st>>>(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init,
+                                                          wm, wg, ckS, ckQ, leafsum);
   SCPL_CHECK_LAUNCH();
   launch_pairwise_fold(leafsum, nleaves, vnodes, N, L, partial, asde_out, st);
 }
@@ -363,7 +432,8 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
   SCPL_CUDA(cudaGraphAddNode(&cond, g, &head, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  window_stats_scan_kernel<<<cdiv((long)nleaves * 8, 256), 256, 0, cs>>>(S, leaves, nleaves);
+  stats_smem_attr();
+  window_stats_scan_kernel<<<cdiv((long)nleaves * 8, 256), 256, kStatSmem, cs>>>(S, leaves, nleaves);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, cs>>>(nullptr, nleaves, vnodes, nullptr, S);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
