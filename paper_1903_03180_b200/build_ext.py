@@ -24,7 +24,7 @@ FLAGS = [
     "--expt-relaxed-constexpr",
     "-fmad=false",          # every fp64 +,* rounds on its own unless written as __fma_rn
     "-Xptxas", "-v",
-]
+] + os.environ.get("SCPL_EXTRA_NVCC_FLAGS", "").split()  # experiments only
 
 
 def _newest(paths):

@@ -303,8 +303,10 @@ void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
     long long c[12];
     SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
     if (getenv("SCPL_PROF"))
-      fprintf(stderr, "carve prof: iters %d rows %d | dp %lld sel %lld | xwait %lld ringwait %lld rows %lld publish %lld\n",
-              R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7]);
+      fprintf(stderr,
+              "carve prof: iters %d rows %d | dp %lld sel %lld | xwait %lld ringwait %lld rows %lld publish %lld"
+              " [bar1 %lld stores %lld bar2 %lld] store_pw %lld\n",
+              R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11]);
     long long tot = c[0] + c[1];
     if (tot > best) {
       best = tot;

@@ -48,6 +48,16 @@ constexpr int kRingW = kWin + 16;                 // ring row: a 16-aligned supe
 constexpr int kIntInf = 0x3fffffff;
 constexpr int kMaxWarps = 12;                    // 384 threads: up to 168 registers per thread
 
+// Fine-grained DP timers (SCPL_CARVE_PROF builds only): clock64 reads and a local-memory
+// accumulator array would otherwise sit on the DP's critical path.
+#ifdef SCPL_CARVE_PROF
+#define DP_CLOCK() clock64()
+#define DP_PROF(i, v) (dprof[i] += (v))
+#else
+#define DP_CLOCK() 0ll
+#define DP_PROF(i, v) ((void)0)
+#endif
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -176,6 +186,8 @@ __device__ __forceinline__ void dp_issue_stage(const CarveRun& Rg, int plane, in
 }
 
 // one DP row for a lane's kC columns (seams.py:54-64): strict '<' in the order -1, 0, +1
+// float64 pass (first pass of a buffered run): ce values with path words pw carried along
+// (2 bits per row of the seam ending in the column).
 template <bool F64, bool EDGE>
 __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t (&pw)[kC],
                                        const uint8_t* erow, const bool (&in)[kC], int lane) {
@@ -226,6 +238,50 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t 
   }
 }
 
+// int32 passes: one packed key per column, K = ce << 8 | dir << 6 | sumdir.  The three
+// candidates of a cell are K[j-1] (dir 0), K[j] + 64 (dir 1) and K[j+1] + 128 (dir 2); their
+// minimum is the minimum cost with ties going to the lower dir -- exactly the reference's
+// strict '<' in the order -1, 0, +1 (seams.py:54-64) -- and carries the predecessor's sum of
+// dirs within the current 16-row block, so the block's landing delta (sumdir - rows) needs
+// no path word.  cw collects this column's own dir per row (the choice word, latest row in
+// the low bits); the trace walks the choice words of the columns a seam visits.
+template <bool EDGE>
+__device__ __forceinline__ void dp_row_key(int (&K)[kC], uint32_t (&cw)[kC], const uint8_t* erow,
+                                           const bool (&in)[kC], int lane) {
+  int e[kC];
+  const uint8_t* p = erow + lane * kC;
+#pragma unroll
+  for (int k = 0; k < kC; ++k) e[k] = (int)p[k];
+  int left = __shfl_up_sync(0xffffffffu, K[kC - 1], 1);
+  int right = __shfl_down_sync(0xffffffffu, K[0], 1);
+  if (lane == 0) left = kIntInf;
+  if (lane == 31) right = kIntInf;
+  int n[kC];
+#pragma unroll
+  for (int k = 0; k < kC; ++k) {
+    const int l = k > 0 ? K[k - 1] : left;
+    const int c = K[k] + 64;
+    const int r = (k + 1 < kC ? K[k + 1] : right) + 128;
+    const int m = min(min(l, c), r);
+    const int dir = (m >> 6) & 3;
+    const int v = m - 63 * dir + (e[k] << 8);
+    n[k] = (!EDGE || in[k]) ? v : kIntInf;
+    cw[k] = (cw[k] << 2) | (uint32_t)dir;
+  }
+#pragma unroll
+  for (int k = 0; k < kC; ++k) K[k] = n[k];
+}
+
+// one row of either pass
+template <bool F64, bool EDGE>
+__device__ __forceinline__ void dp_step(typename Val<F64>::T (&ce)[kC], uint32_t (&pw)[kC], const uint8_t* erow,
+                                        const bool (&in)[kC], int lane) {
+  if constexpr (F64)
+    dp_row<true, EDGE>(ce, pw, erow, in, lane);
+  else
+    dp_row_key<EDGE>(ce, pw, erow, in, lane);
+}
+
 // One DP pass for this warp's window.  ceX: smem exchange rows [2][pitch]; ring: this
 // warp's energy ring; bars: its S ring mbarriers (phase bits in rph); xbar/xc: the
 // neighbour-exchange barriers and exchange counter (buffer = xc & 1, parity = (xc>>1) & 1).
@@ -250,14 +306,16 @@ __device__ __forceinline__ uint32_t halo_bytes_for(int w, int CL, uint32_t rank,
 template <bool F64, bool EDGE>
 __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
                         uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
-                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof) {
+                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage) {
   using V = Val<F64>;
   using T = typename V::T;
   constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
   constexpr int sz = F64 ? 8 : 1;
   static_assert(kXRows % RS == 0 && kBlockRows % RS == 0 || RS == kXRows, "stage layout");
   const int lane = threadIdx.x & 31;
-  const int rows = R.rows, w = g.w;
+  const int rows = R.rows, w = g.w, pitch = R.pitch;
+  uint32_t* const pw_g = R.pw;
+  int8_t* const delta_g = R.delta;
   const bool active = g.own_lo < g.own_hi;
   const int j0 = g.win_lo + lane * kC;
   const bool nb_mode = per_cta >= kXRows;
@@ -274,7 +332,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       if constexpr (F64)
         v = in[k] ? R.U[j0 + k] : 0.0;
       else
-        v = in[k] ? (int)R.grad[plane][j0 + k] : 0;
+        v = in[k] ? (int)R.grad[plane][j0 + k] << 8 : 0;  // key of row 0
       ce[k] = in[k] ? v : V::inf();
     }
     if (lane == 0)
@@ -290,28 +348,44 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
     __syncwarp();
     if (lane == 0 && st + S - 1 < nstage) dp_issue_stage<F64>(Rg, plane, rows, st + S - 1, g.win_lo, ring, bars);
     const int slot = st % S;
-    long long tq = clock64();
+    [[maybe_unused]] long long tq = DP_CLOCK();
     mbar_wait(&bars[slot], (rph >> slot) & 1u);
     __syncwarp();
-    dprof[1] += clock64() - tq;
+    DP_PROF(1, DP_CLOCK() - tq);
     rph ^= 1u << slot;
     return ring + ((size_t)slot * RS * kRingW + (g.win_lo & 15)) * sz;
   };
+  // block-end path words and landing deltas of the owned columns: the lane-contiguous words
+  // are transposed through this warp's staging row so the global stores coalesce
   auto store_pw = [&](int pbi, int nrb) {
+    [[maybe_unused]] long long t7 = DP_CLOCK();
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kC; k += 2) {
+      *reinterpret_cast<uint2*>(&pw_stage[lane * kC + k]) = make_uint2(pw[k], pw[k + 1]);
+      if constexpr (!F64)
+        *reinterpret_cast<int2*>(&pw_stage[kWin + lane * kC + k]) = make_int2(ce[k] & 63, ce[k + 1] & 63);
+    }
+    __syncwarp();
+    uint32_t* gpw = pw_g + (long)pbi * pitch + g.win_lo;
+    int8_t* gdl = delta_g + (long)pbi * pitch + g.win_lo;
 #pragma unroll
     for (int k = 0; k < kC; ++k) {
-      int j = j0 + k;
+      const int c = lane + 32 * k;
+      const int j = g.win_lo + c;
       if (j >= g.own_lo && j < g.own_hi) {
-        int sum = __popc(pw[k] & 0x55555555u) + 2 * __popc(pw[k] & 0xAAAAAAAAu);
-        R.pw[(long)pbi * R.pitch + j] = pw[k];
-        R.delta[(long)pbi * R.pitch + j] = (int8_t)(sum - nrb);
+        const uint32_t word = pw_stage[c];
+        gpw[c] = word;
+        const int sumdir = F64 ? __popc(word & 0x55555555u) + 2 * __popc(word & 0xAAAAAAAAu) : (int)pw_stage[kWin + c];
+        gdl[c] = (int8_t)(sumdir - nrb);
       }
     }
+    DP_PROF(7, DP_CLOCK() - t7);
   };
   int last_pbi = -1, last_nr = 0;
   const int nx = (rows - 1 + kXRows - 1) / kXRows;
   for (int xb = 0; xb < nx; ++xb) {
-    long long tx = clock64();
+    [[maybe_unused]] long long tx = DP_CLOCK();
     if (nb_mode) {
       if (xb > 0) {  // halo of the previous exchange landed (st.async completion)
         const uint32_t e = xm - 1;
@@ -319,10 +393,10 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         __syncwarp();
       }
     }
-    dprof[0] += clock64() - tx;
+    DP_PROF(0, DP_CLOCK() - tx);
     if (active) {
       if (xb > 0) {
-        const T* src = ceX + (size_t)((xc - 1) & 1) * R.pitch;
+        const T* src = ceX + (size_t)((xc - 1) & 1) * pitch;
 #pragma unroll
         for (int k = 0; k < kC; ++k) ce[k] = in[k] ? src[j0 + k] : V::inf();
       }
@@ -334,7 +408,10 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         const int nr = min(kBlockRows, rows - i0);
         if (nr <= 0) break;
 #pragma unroll
-        for (int k = 0; k < kC; ++k) pw[k] = 0u;  // path words restart every 16 rows
+        for (int k = 0; k < kC; ++k) {  // path / choice words and dir sums restart every 16 rows
+          pw[k] = 0u;
+          if constexpr (!F64) ce[k] &= ~63;
+        }
         if (nr == kBlockRows) {
           // 4 rows unrolled per step: short enough for the instruction cache
 #pragma unroll 1
@@ -347,7 +424,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
               ebase = stage_rows((i0 - 1 + r4) / RS);
             }
 #pragma unroll
-            for (int r = 0; r < 4; ++r) dp_row<F64, EDGE>(ce, pw, ebase + (size_t)r * kRingW * sz, in, lane);
+            for (int r = 0; r < 4; ++r) dp_step<F64, EDGE>(ce, pw, ebase + (size_t)r * kRingW * sz, in, lane);
           }
         } else {
 #pragma unroll 1
@@ -360,7 +437,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
               if ((i - 1) % RS == 0) stage = stage_rows((i - 1) / RS);
               erow = stage + (size_t)((i - 1) % RS) * kRingW * sz;
             }
-            dp_row<F64, EDGE>(ce, pw, erow, in, lane);
+            dp_step<F64, EDGE>(ce, pw, erow, in, lane);
           }
         }
         // path-word block end: owned words and landing deltas (read after the pass); the
@@ -369,8 +446,8 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         last_nr = nr;
         if (pb + 1 < kXRows / kBlockRows && i0 + nr < rows) store_pw(last_pbi, last_nr);
       }
-      dprof[2] += clock64() - tx;
-      tx = clock64();
+      DP_PROF(2, DP_CLOCK() - tx);
+      tx = DP_CLOCK();
     }
     // announce the next exchange's bytes, then let the block's data go out (the named
     // barrier orders the announcement before every local warp's sends)
@@ -378,10 +455,11 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
       asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");
     }
+    DP_PROF(4, DP_CLOCK() - tx);
     if (active) {
       // exchange-block end: owned ce into this CTA's buffer; halo columns straight into the
       // adjacent CTAs' buffers with st.async, completing bytes on their exchange barrier
-      T* dst = ceX + (size_t)(xc & 1) * R.pitch;
+      T* dst = ceX + (size_t)(xc & 1) * pitch;
 
 #pragma unroll
       for (int k = 0; k < kC; ++k) {
@@ -403,15 +481,17 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         }
       }
     }
+    DP_PROF(5, DP_CLOCK() - tx);
     if (nb_mode)
       asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");  // this CTA's DP warps' values
     else
       cluster_sync();
+    DP_PROF(6, DP_CLOCK() - tx);
     if (active && last_pbi >= 0) {
       store_pw(last_pbi, last_nr);
       last_pbi = -1;
     }
-    if (active) dprof[3] += clock64() - tx;
+    if (active) DP_PROF(3, DP_CLOCK() - tx);
     ++xc;
     if (nb_mode) ++xm;
   }
@@ -424,7 +504,12 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
 #pragma unroll
     for (int k = 0; k < kC; ++k) {
       int j = j0 + k;
-      if (j >= g.own_lo && j < g.own_hi) R.lastce[j] = V::to_d(ce[k]);
+      if (j >= g.own_lo && j < g.own_hi) {
+        if constexpr (F64)
+          R.lastce[j] = ce[k];
+        else
+          R.lastce[j] = (double)(ce[k] >> 8);
+      }
     }
   }
 }
@@ -432,12 +517,14 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
 template <bool F64>
 __device__ void dp_pass(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
                         uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
-                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof) {
+                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage) {
   // windows lie inside [0, w) unless the plane is narrower than one window
   if (g.w < kWin)
-    dp_rows<F64, true>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof);
+    dp_rows<F64, true>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+                       pw_stage);
   else
-    dp_rows<F64, false>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof);
+    dp_rows<F64, false>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+                        pw_stage);
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -532,7 +619,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
   const uint32_t rank = cluster_rank();
   CarveRun& Rg = runs[blockIdx.x / CL];
-  const CarveRun R = Rg;  // state at entry (written back only after the final cluster barrier)
+  const CarveRun& R = Rg;  // fields read in place; the state fields are copied below
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int w = R.width, iters = R.iters, removed = R.removed;
   if (w <= R.target) {  // done: nothing this iteration
@@ -543,7 +630,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
   const bool stage_dtab = R.stage_dtab != 0;
   const int plane = iters & 1;
-  long long dprof[4] = {0, 0, 0, 0};
+  long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tp = clock64();
 
   const int per = ((w + CL - 1) / CL + 15) & ~15;
@@ -575,12 +662,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     const bool in_dp = wid < ndp || per < kXRows;
     if (in_dp) {
       uint8_t* ring = smem + 2 * sizeof(double) * (size_t)pitch;
+      uint32_t* pw_stage = reinterpret_cast<uint32_t*>(ring + (size_t)ndp * dp_ring_bytes<true>()) + wid * 2 * kWin;
       if (fp64)
         dp_pass<true>(R, Rg, g, plane, reinterpret_cast<double*>(smem), CL, rank, per, s_xbar, xc, xm,
-                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, ndp, dprof);
+                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage);
       else
         dp_pass<false>(R, Rg, g, plane, reinterpret_cast<int*>(smem), CL, rank, per, s_xbar, xc, xm,
-                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, ndp, dprof);
+                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage);
     }
   }
   cluster_sync();  // lastce / pw / delta of all CTAs visible
@@ -713,13 +801,21 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     for (int q = tid; q < b * myblk; q += blockDim.x) {
       int s = q / myblk, bl = (int)rank + (q - s * myblk) * CL;
       int c = R.cend[(long)bl * pitch + s];
-      uint32_t word = R.pw[(long)bl * pitch + c];
+      const uint32_t* pwb = R.pw + (long)bl * pitch;
       int i_start = 1 + bl * kBlockRows;
       int i_end = min(i_start + kBlockRows, rows) - 1;
-      for (int i = i_end; i >= i_start; --i) {
-        log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
-        c += (int)(word & 3u) - 1;
-        word >>= 2;
+      if (fp64) {  // path word of the seam's end column
+        uint32_t word = pwb[c];
+        for (int i = i_end; i >= i_start; --i) {
+          log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
+          c += (int)(word & 3u) - 1;
+          word >>= 2;
+        }
+      } else {  // choice words of the visited columns
+        for (int i = i_end, q = 0; i >= i_start; --i, ++q) {
+          log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
+          c += (int)((pwb[c] >> (2 * q)) & 3u) - 1;
+        }
       }
     }
     if (rank == 0 && R.cols != nullptr)
@@ -737,7 +833,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     if (R.prof) {
       R.prof[0] += t_dp;
       R.prof[1] += clock64() - tp;
-      for (int k = 0; k < 4; ++k) R.prof[4 + k] += dprof[k];
+      for (int k = 0; k < 8; ++k) R.prof[4 + k] += dprof[k];
     }
   }
 }
@@ -1046,7 +1142,7 @@ int carve_comp_warps(int pitch) {
 
 size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps) {
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
-  size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * dp_ring_bytes<true>();
+  size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * (dp_ring_bytes<true>() + 8 * kWin);
   size_t sel = (size_t)pitch * (8 + 8 + 4 * 4) + 16;
   if (stage) sel += (size_t)nblk * pitch;
   const size_t RB = (((size_t)pitch + 15) & ~(size_t)15) + 16;
