@@ -85,6 +85,21 @@ __device__ __forceinline__ void st_async_remote(const double* local_dst, double 
                "l"(__double_as_longlong(v)), "r"(map_rank(local_bar, rank))
                : "memory");
 }
+__device__ __forceinline__ uint32_t map_rank_pure(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void st_async_addr(uint32_t raddr, int v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_addr(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void st_cluster(uint32_t addr, int v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -324,6 +339,11 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   bool in[kC];
 #pragma unroll
   for (int k = 0; k < kC; ++k) in[k] = (j0 + k >= 0) && (j0 + k < w);
+  bool own[kC];
+#pragma unroll
+  for (int k = 0; k < kC; ++k) own[k] = (j0 + k >= g.own_lo) && (j0 + k < g.own_hi);
+  const bool send_lo = nb_mode && active && rank > 0 && g.own_lo < g.cta_lo + kXRows;
+  const bool send_hi = nb_mode && active && (int)rank + 1 < CL && g.own_hi > g.cta_hi - kXRows;
   const int nstage = (rows - 1 + RS - 1) / RS;
   if (active) {
 #pragma unroll
@@ -373,7 +393,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
     for (int k = 0; k < kC; ++k) {
       const int c = lane + 32 * k;
       const int j = g.win_lo + c;
-      if (j >= g.own_lo && j < g.own_hi) {
+      if (j >= g.own_lo && j < g.own_hi) {  // (transposed column: not this lane's own[])
         const uint32_t word = pw_stage[c];
         gpw[c] = word;
         const int sumdir = F64 ? __popc(word & 0x55555555u) + 2 * __popc(word & 0xAAAAAAAAu) : (int)pw_stage[kWin + c];
@@ -460,23 +480,33 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       // exchange-block end: owned ce into this CTA's buffer; halo columns straight into the
       // adjacent CTAs' buffers with st.async, completing bytes on their exchange barrier
       T* dst = ceX + (size_t)(xc & 1) * pitch;
-
 #pragma unroll
-      for (int k = 0; k < kC; ++k) {
-        int j = j0 + k;
-        if (j >= g.own_lo && j < g.own_hi) {
-          dst[j] = ce[k];
-          if (nb_mode) {
-            if (rank > 0 && j < g.cta_lo + kXRows)
-              st_async_remote(&dst[j], ce[k], &xbar[xm & 1], rank - 1);
-            if ((int)rank + 1 < CL && j >= g.cta_hi - kXRows)
-              st_async_remote(&dst[j], ce[k], &xbar[xm & 1], rank + 1);
-          } else {
-            for (int q = 0; q < CL; ++q) {
-              if (q == (int)rank) continue;
-              int lo = min(w, q * per_cta), hi = min(w, lo + per_cta);
-              if (lo < hi && j >= lo - kXRows && j < hi + kXRows) st_cluster(map_rank(&dst[j], q), ce[k]);
-            }
+      for (int k = 0; k < kC; ++k)
+        if (own[k]) dst[j0 + k] = ce[k];
+      if (nb_mode) {
+        // only the CTA's first / last warp owns columns within kXRows of a CTA edge
+        if (send_lo) {
+          const uint32_t rd = map_rank_pure(dst, rank - 1), rb = map_rank_pure(&xbar[xm & 1], rank - 1);
+#pragma unroll
+          for (int k = 0; k < kC; ++k)
+            if (own[k] && j0 + k < g.cta_lo + kXRows) st_async_addr(rd + (uint32_t)((j0 + k) * sizeof(T)), ce[k], rb);
+        }
+        if (send_hi) {
+          const uint32_t rd = map_rank_pure(dst, rank + 1), rb = map_rank_pure(&xbar[xm & 1], rank + 1);
+#pragma unroll
+          for (int k = 0; k < kC; ++k)
+            if (own[k] && j0 + k >= g.cta_hi - kXRows) st_async_addr(rd + (uint32_t)((j0 + k) * sizeof(T)), ce[k], rb);
+        }
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < CL; ++q) {
+          if (q == (int)rank) continue;
+          const int lo = min(w, q * per_cta), hi = min(w, lo + per_cta);
+          const uint32_t rd = map_rank_pure(dst, q);
+#pragma unroll
+          for (int k = 0; k < kC; ++k) {
+            const int j = j0 + k;
+            if (own[k] && lo < hi && j >= lo - kXRows && j < hi + kXRows) st_cluster(rd + (uint32_t)(j * sizeof(T)), ce[k]);
           }
         }
       }
