@@ -358,10 +358,9 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
     if (lane == 0)
       for (int st = 0; st < S - 1 && st < nstage; ++st) dp_issue_stage<F64>(Rg, plane, rows, st, g.win_lo, ring, bars);
   }
-  // Exchange protocol (nb_mode): a CTA announces the bytes of exchange e on its barrier
-  // before it sends its own data of exchange e-1 (end of block e-1) -- or, for a pass's
-  // first exchange, before the cluster barrier that precedes the pass -- so complete_tx
-  // from a neighbour can never precede the matching expect_tx.
+  // Exchange protocol (nb_mode): exchange e alternates between two mbarriers (e & 1); a
+  // CTA announces the bytes of exchange e + 1 once exchange e - 1 has landed (for e = 0,
+  // before the cluster barrier that precedes the pass).
   const uint32_t halo_bytes = nb_mode ? halo_bytes_for(w, CL, rank, (int)sizeof(T)) : 0u;
   // wait for stage st (issuing the one S-1 ahead first) and return its ring rows
   auto stage_rows = [&](int st) -> const uint8_t* {
@@ -412,6 +411,10 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         mbar_wait(&xbar[e & 1], (e >> 1) & 1);
         __syncwarp();
       }
+      // announce exchange xm + 1 on the barrier exchange xm - 1 just released; a neighbour
+      // can only send it after receiving this CTA's exchange xm, and an early complete_tx
+      // would merely take the phase's tx-count below zero until this arrive
+      if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
     }
     DP_PROF(0, DP_CLOCK() - tx);
     if (active) {
@@ -468,12 +471,6 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       }
       DP_PROF(2, DP_CLOCK() - tx);
       tx = DP_CLOCK();
-    }
-    // announce the next exchange's bytes, then let the block's data go out (the named
-    // barrier orders the announcement before every local warp's sends)
-    if (nb_mode) {
-      if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
-      asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");
     }
     DP_PROF(4, DP_CLOCK() - tx);
     if (active) {
