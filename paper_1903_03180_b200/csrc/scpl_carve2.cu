@@ -644,6 +644,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   __shared__ int ws[32];
   __shared__ __align__(8) uint64_t s_xbar[2];
   __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
+  __shared__ __align__(8) uint64_t s_dbar;  // delta-table staging (select phase)
   const uint32_t rank = cluster_rank();
   CarveRun& Rg = runs[blockIdx.x / CL];
   const CarveRun& R = Rg;  // fields read in place; the state fields are copied below
@@ -666,6 +667,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   if (tid == 0) {
     mbar_init(&s_xbar[0], 1);
     mbar_init(&s_xbar[1], 1);
+    mbar_init(&s_dbar, 1);
     if (rows > 1 && per >= kXRows)  // the pass's first exchange, announced before it can start
       mbar_arrive_tx(&s_xbar[0], halo_bytes_for(w, CL, rank, fp64 ? 8 : 4));
   }
@@ -720,19 +722,21 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
       p += 4 * (size_t)pitch;
       S.dtab = stage_dtab ? reinterpret_cast<int8_t*>(p) : nullptr;
     }
+    const int8_t* dsrc = R.delta;
+    if (stage_dtab && tid == 0) {
+      // one bulk copy of the whole landing-delta table; the DP's generic-proxy stores (every
+      // CTA, published by the cluster barrier) are ordered before the async-proxy read
+      fence_proxy_async_global();
+      mbar_arrive_tx(&s_dbar, (uint32_t)((size_t)nblk * pitch));
+      bulk_g2s(S.dtab, R.delta, (uint32_t)((size_t)nblk * pitch), &s_dbar);
+    }
     for (int j = tid; j < w; j += blockDim.x) {
       S.lce[j] = R.lastce[j];
       S.segmin[j] = ~0ull;
       S.segarg[j] = INT_MAX;
     }
-    const int8_t* dsrc = R.delta;
     if (stage_dtab) {
-      const int per_row = (w + 15) >> 4;  // 16-byte copies; pitch is a multiple of 16
-      for (int q = tid; q < nblk * per_row; q += blockDim.x) {
-        int bl = q / per_row, c = (q - bl * per_row) << 4;
-        *reinterpret_cast<uint4*>(S.dtab + (size_t)bl * pitch + c) =
-            *reinterpret_cast<const uint4*>(R.delta + (size_t)bl * pitch + c);
-      }
+      mbar_wait(&s_dbar, 0);
       dsrc = S.dtab;
     }
     __syncthreads();
