@@ -212,22 +212,29 @@ struct CarveSet {
   DBuf mem, runs_d;
   std::vector<CarveRun> runs;
   int rows = 0, cols = 0, pitch = 0, target = 0, cl = 1;
+  size_t planes_bytes = 0;  // luma + gradient planes of every run, at the start of mem
   long long prof[4] = {0, 0, 0, 0};
 };
 
 void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
                  int cl, cudaStream_t st) {
+  SCPL_ARG(cols <= 4096, "frames wider than 4096 columns (in the carve orientation) are not supported");
   const int pitch = (cols + 15) & ~15;
   const int nblk = std::max(1, (rows - 1 + kBlockRows - 1) / kBlockRows);
   const int rem_cap = std::max(1, cols - target);
   const int alive_pitch = ((cols + 31) / 32 + 3) & ~3;
   const size_t plane = (size_t)rows * pitch;
-  size_t per = align256(plane) * 4 + align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
+  // every run's luma and gradient plane first (compacted in place; one contiguous range for
+  // the L2 persistence window), then each run's tables
+  const size_t plane_al = align256(plane);
+  const size_t planes_bytes = (size_t)nruns * 2 * plane_al;
+  size_t per = align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
                align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
                align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(256) +
                (with_U ? align256(plane * 8) : 0) + align256((size_t)cols * 4) +
                (dbg ? align256((size_t)cols * 2) + align256((size_t)cols * 8) : 0);
-  S.mem = DBuf(per * nruns, st);
+  S.mem = DBuf(planes_bytes + per * nruns, st);
+  S.planes_bytes = planes_bytes;
   S.rows = rows;
   S.cols = cols;
   S.pitch = pitch;
@@ -237,7 +244,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   uint8_t* base = S.mem.as<uint8_t>();
   const int stage = carve_stage_dtab(rows, pitch, cl) ? 1 : 0;
   for (int r = 0; r < nruns; ++r) {
-    uint8_t* p = base + per * r;
+    uint8_t* p = base + planes_bytes + per * r;
     auto take = [&](size_t bytes) {
       uint8_t* q = p;
       p += align256(bytes);
@@ -250,10 +257,8 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.target = target;
     R.kmax = kmax;
     R.stage_dtab = stage;
-    R.luma[0] = take(plane);
-    R.luma[1] = take(plane);
-    R.grad[0] = take(plane);
-    R.grad[1] = take(plane);
+    R.luma[0] = R.luma[1] = base + (size_t)(2 * r) * plane_al;
+    R.grad[0] = R.grad[1] = base + (size_t)(2 * r + 1) * plane_al;
     R.width = cols;
     R.idx = reinterpret_cast<int16_t*>(take(plane * 2));
     R.pw = reinterpret_cast<uint32_t*>(take((size_t)nblk * pitch * 4));

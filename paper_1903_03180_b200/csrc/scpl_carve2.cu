@@ -637,8 +637,7 @@ __device__ __forceinline__ int alive_select(const uint32_t* wv, const int* pre, 
 }
 
 // One DP pass + select + trace for every active run (one cluster per run).  Per-run state
-// (width, iters, removed) is read at entry and written back at exit; the gradient plane of
-// this pass is the ping-pong plane `iters & 1`.
+// (width, iters, removed) is read at entry and written back at exit.
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun* __restrict__ runs, int CL) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int ws[32];
@@ -657,7 +656,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   const int rows = R.rows, pitch = R.pitch;
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
   const bool stage_dtab = R.stage_dtab != 0;
-  const int plane = iters & 1;
+  const int plane = 0;  // planes are compacted in place
   long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tp = clock64();
 
@@ -870,75 +869,99 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
 }
 
 // ------------------------------------------------------------------ row kernels
-// Compact one row of luma and gradient (remove_batch, batching.py:76-107) from the ping-pong
-// plane `iters_before & 1` into the other one.  Output byte y reads input byte y + s(y),
-// s(y) = #{t : a_t <= y} with a_t = rem[t] - t (non-decreasing).  Lanes hold the a_t and
-// every lane counts, for its output words q = lane + 32k, the a_t <= 4q through shuffles;
-// a word with one shift is a funnel shift of two input words, the few words with a shift
-// change inside (a_t % 4 != 0) are then rewritten byte by byte.
+// Compact one row of luma and gradient in place (remove_batch, batching.py:76-107).  Output
+// byte y reads input byte y + s(y), s(y) = #{t : a_t <= y}, a_t = rem[t] - t.  The warp
+// stages the source row in shared memory (TMA bulk copy, so the in-place writes cannot race
+// the reads), counts a_t per output word in a packed histogram (low half: a_t <= 4q, high
+// half: a_t <= 4q + 3), prefix-sums it, and writes each output word as one funnel shift of
+// two source words -- or byte by byte when its shift changes inside the word.
 constexpr int kRowWarps = 8;
+constexpr int kMaxRowWords = 1024;  // widths up to 4096
+
+size_t carve_compact_smem(int pitch) { return (size_t)kRowWarps * (2 * (size_t)pitch + 4 * kMaxRowWords + 16); }
 
 __global__ void __launch_bounds__(kRowWarps * 32) carve_compact_kernel(CarveRun* __restrict__ runs) {
+  extern __shared__ __align__(16) uint8_t csm[];
   const CarveRun& R = runs[blockIdx.y];
   const int b = R.b;
-  if (b == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (b == 0 || R.width <= R.target) return;  // nothing removed / no further pass reads the planes
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int i = blockIdx.x * kRowWarps + wl;
   if (i >= R.rows) return;
+  const int pitch = R.pitch;
   const int wn = R.width, w0 = wn + b;
-  const int src = (R.iters - 1) & 1, dst = src ^ 1;  // iters already counts this batch
-  const int16_t* rg = R.rem + (long)i * R.rem_cap + (R.removed - b);
-  const uint32_t* Li = reinterpret_cast<const uint32_t*>(R.luma[src] + (long)i * R.pitch);
-  const uint32_t* Gi = reinterpret_cast<const uint32_t*>(R.grad[src] + (long)i * R.pitch);
-  uint32_t* Lo = reinterpret_cast<uint32_t*>(R.luma[dst] + (long)i * R.pitch);
-  uint32_t* Go = reinterpret_cast<uint32_t*>(R.grad[dst] + (long)i * R.pitch);
+  uint8_t* base = csm + (size_t)wl * (2 * (size_t)pitch + 4 * kMaxRowWords + 16);
+  uint8_t* sL = base;
+  uint8_t* sG = base + pitch;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(base + 2 * (size_t)pitch);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(hist + kMaxRowWords);
+  uint8_t* L = R.luma[0] + (long)i * pitch;
+  uint8_t* G = R.grad[0] + (long)i * pitch;
+  const uint32_t rbytes = (uint32_t)(((w0 + 15) >> 4) << 4);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_tx(bar, 2 * rbytes);
+    bulk_g2s(sL, L, rbytes, bar);
+    bulk_g2s(sG, G, rbytes, bar);
+  }
   const int nwo = (wn + 3) >> 2;
-  const int nwi = (w0 + 3) >> 2;
-  constexpr int KG = 8;
-  for (int g0 = 0; g0 * 32 < nwo; g0 += KG) {
-    int sk[KG];
-#pragma unroll
-    for (int k = 0; k < KG; ++k) sk[k] = 0;
-    for (int c = 0; c < b; c += 32) {
-      const int av = (c + lane < b) ? rg[c + lane] - (c + lane) : 0x7fffffff;
-      const int nt = min(32, b - c);
-      for (int tt = 0; tt < nt; ++tt) {
-        const int a = __shfl_sync(0xffffffffu, av, tt);
-#pragma unroll
-        for (int k = 0; k < KG; ++k) sk[k] += (a <= 4 * ((g0 + k) * 32 + lane)) ? 1 : 0;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < KG; ++k) {
-      const int q = (g0 + k) * 32 + lane;
-      if (q < nwo) {
-        const int x0 = 4 * q + sk[k];
-        const int wq = x0 >> 2;
-        const uint32_t sh = (uint32_t)(x0 & 3) * 8u;
-        const uint32_t l0 = Li[wq], g0v = Gi[wq];
-        const uint32_t l1 = wq + 1 < nwi ? Li[wq + 1] : 0u, g1v = wq + 1 < nwi ? Gi[wq + 1] : 0u;
-        Lo[q] = __funnelshift_r(l0, l1, sh);
-        Go[q] = __funnelshift_r(g0v, g1v, sh);
-      }
-    }
+  for (int q = lane; q <= nwo; q += 32) hist[q] = 0u;
+  __syncwarp();
+  const int16_t* rg = R.rem + (long)i * R.rem_cap + (R.removed - b);
+  for (int t = lane; t < b; t += 32) {
+    const int at = rg[t] - t;  // >= 0
+    const int q1 = (at + 3) >> 2, q2 = at >> 2;  // a_t <= 4q  <=>  q >= q1;  a_t <= 4q+3  <=>  q >= q2
+    if (q1 <= nwo) atomicAdd(&hist[q1], 1u);
+    if (q2 <= nwo) atomicAdd(&hist[q2], 0x10000u);
   }
   __syncwarp();
-  const uint8_t* Lb = R.luma[src] + (long)i * R.pitch;
-  const uint8_t* Gb = R.grad[src] + (long)i * R.pitch;
-  for (int t = lane; t < b; t += 32) {
-    const int at = rg[t] - t;
-    if ((at & 3) == 0 || (at >> 2) >= nwo) continue;
-    const int q = at >> 2, y0 = 4 * q;
-    uint32_t lv = 0u, gv = 0u;
-    for (int u = 0; u < 4; ++u) {
-      int su = 0;
-      for (int t2 = 0; t2 < b; ++t2) su += (rg[t2] - t2 <= y0 + u) ? 1 : 0;
-      const int x = y0 + u + su;
-      lv |= (uint32_t)(x < w0 ? Lb[x] : 0) << (8 * u);
-      gv |= (uint32_t)(x < w0 ? Gb[x] : 0) << (8 * u);
+  // inclusive prefix over q = 0 .. nwo-1: lane owns a contiguous segment
+  const int per = (nwo + 31) >> 5;
+  const int q0 = min(nwo, lane * per), q1 = min(nwo, q0 + per);
+  uint32_t run = 0;
+  for (int q = q0; q < q1; ++q) run += hist[q];
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  run = incl - run;
+  for (int q = q0; q < q1; ++q) {
+    run += hist[q];
+    hist[q] = run;
+  }
+  mbar_wait(bar, 0);
+  __syncwarp();
+  const uint32_t* Lw = reinterpret_cast<const uint32_t*>(sL);
+  const uint32_t* Gw = reinterpret_cast<const uint32_t*>(sG);
+  const int nwi = (w0 + 3) >> 2;
+  for (int q = lane; q < nwo; q += 32) {
+    const uint32_t h = hist[q];
+    const int s0 = (int)(h & 0xffffu), s3 = (int)(h >> 16);
+    uint32_t lv, gv;
+    if (s0 == s3) {
+      const int x0 = 4 * q + s0, wq = x0 >> 2;
+      const uint32_t sh = (uint32_t)(x0 & 3) * 8u;
+      const bool nx = wq + 1 < nwi;
+      lv = __funnelshift_r(Lw[wq], nx ? Lw[wq + 1] : 0u, sh);
+      gv = __funnelshift_r(Gw[wq], nx ? Gw[wq + 1] : 0u, sh);
+    } else {  // s(4q + u) for u = 0..3 from the removed list
+      int t = s0;
+      lv = 0u;
+      gv = 0u;
+      for (int u = 0; u < 4; ++u) {
+        while (t < b && rg[t] - t <= 4 * q + u) ++t;
+        const int x = 4 * q + u + t;
+        if (x < w0) {
+          lv |= (uint32_t)sL[x] << (8 * u);
+          gv |= (uint32_t)sG[x] << (8 * u);
+        }
+      }
     }
-    Lo[q] = lv;
-    Go[q] = gv;
+    reinterpret_cast<uint32_t*>(L)[q] = lv;
+    reinterpret_cast<uint32_t*>(G)[q] = gv;
   }
 }
 
@@ -953,7 +976,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) carve_dirty_kernel(CarveRun* _
   const int rows = R.rows;
   if (i >= rows) return;
   const int wn = R.width, w0 = wn + b;
-  const int dst = R.iters & 1;
+  const int dst = 0;  // planes are compacted in place
   uint8_t* gr = R.grad[dst] + (long)i * R.pitch;
   if (rows < 3 || wn < 3) {
     for (int y = lane; y < wn; y += 32) gr[y] = 0;
@@ -1211,7 +1234,9 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl));
   SCPL_CHECK_LAUNCH();
   dim3 rgrid(cdiv(rows, kRowWarps), nruns);
-  carve_compact_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
+  const size_t csmem = carve_compact_smem(pitch);
+  SCPL_CUDA(cudaFuncSetAttribute(carve_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  carve_compact_kernel<<<rgrid, kRowWarps * 32, csmem, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();
   carve_dirty_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();
