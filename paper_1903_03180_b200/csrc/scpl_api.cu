@@ -287,22 +287,30 @@ void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
   const int nruns = (int)S.runs.size();
   if (nruns == 0) return;
   for (auto& R : S.runs) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, 256, st));
-  S.runs_d = DBuf(sizeof(CarveRun) * nruns, st);
+  S.runs_d = DBuf(sizeof(CarveRun) * nruns + 16, st);
   SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, S.runs.data(), sizeof(CarveRun) * nruns, cudaMemcpyHostToDevice, st));
-  if (S.cols > S.target) {
-    while (true) {
-      for (int k = 0; k < 8; ++k)
-        launch_carve_iteration(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st);
-      SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
-      SCPL_CUDA(cudaStreamSynchronize(st));
-      bool all = true;
-      for (auto& R : S.runs) all &= R.width <= R.target;
-      if (all) break;
+  int* iters_d = reinterpret_cast<int*>(S.runs_d.as<uint8_t>() + sizeof(CarveRun) * nruns);
+  SCPL_CUDA(cudaMemsetAsync(iters_d, 0, sizeof(int), st));
+  cudaGraphExec_t loop = nullptr;
+  struct ExecGuard {
+    cudaGraphExec_t& e;
+    ~ExecGuard() {
+      if (e) cudaGraphExecDestroy(e);
     }
+  } eg{loop};
+  if (S.cols > S.target) {
+    loop = build_carve_loop(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1,
+                            iters_d);
+    SCPL_CUDA(cudaGraphLaunch(loop, st));
   }
   launch_carve_index(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
   SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
+  int iters_h = 0;
+  SCPL_CUDA(cudaMemcpyAsync(&iters_h, iters_d, sizeof(int), cudaMemcpyDeviceToHost, st));
   SCPL_CUDA(cudaStreamSynchronize(st));
+  g_launches.fetch_add(4L * iters_h, std::memory_order_relaxed);
+  for (auto& R : S.runs)
+    if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;
   for (auto& R : S.runs) {
     long long c[12];

@@ -1242,6 +1242,54 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   SCPL_CHECK_LAUNCH();
 }
 
+// Loop condition of the device-side carve loop: another iteration while any run is above its
+// target (bounded by max_iters: every pass removes at least one seam).
+__global__ void carve_check_kernel(const CarveRun* __restrict__ runs, int nruns, int max_iters, int* iters,
+                                   cudaGraphConditionalHandle loop) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < nruns; r += blockDim.x)
+    if (runs[r].width > runs[r].target) any = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int n = ++*iters;
+    cudaGraphSetConditional(loop, (any && n < max_iters) ? 1u : 0u);
+  }
+}
+
+// carve every run to its target in ONE graph launch: while (any run above target)
+// { pass; compact; gradient } -- no host round trip per iteration.
+cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
+                                 int* iters_d) {
+  cudaGraph_t g;
+  SCPL_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  SCPL_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond;
+  SCPL_CUDA(cudaGraphAddNode(&cond, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t cs;
+  SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  const long before = g_launches.load();
+  SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs);
+  carve_check_kernel<<<1, 256, 0, cs>>>(runs_d, nruns, max_iters, iters_d, h);
+  SCPL_CUDA(cudaGetLastError());
+  SCPL_CUDA(cudaStreamEndCapture(cs, &body));
+  g_launches.store(before);  // counted per executed iteration by the caller
+  cudaGraphExec_t ex;
+  SCPL_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return ex;
+}
+
 void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st) {
   if (nruns == 0) return;
   carve_index_kernel<<<dim3(cdiv(rows, kRowWarps), nruns), kRowWarps * 32, 0, st>>>(runs_d);
