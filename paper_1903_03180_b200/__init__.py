@@ -5,6 +5,13 @@ retargeting path; the compute runs in libscpl.so (include/scpl.h) with no CPU fa
 Out of scope: media I/O, CLI, plots and the bench corpus helpers.
 """
 
+import os as _os
+
+# The streamed pipeline keeps up to ~13 streams busy at once (copies in/out, codes + scan,
+# concurrent carve groups); with the default 8 hardware work queues, streams would share
+# queues and serialise behind each other.  Takes effect if CUDA is not initialised yet.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .batching import SeamBatch, batch_carve, default_energy, label_parents, remove_batch, select_batch
 from .buffering import BufferPolicy, FixedRun, SpatioTemporalBuffer, threshold
 from .energy import MAXVAL, gradient_energy, motion_energy, to_luma

@@ -12,10 +12,15 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
+#include <list>
 #include <map>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -28,6 +33,20 @@ using namespace scpl;
 namespace scpl {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+void smem_optin(const void* kernel) {
+  static std::mutex mu;
+  static std::set<const void*> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(kernel)) return;
+  int dev = 0, optin = 0;
+  SCPL_CUDA(cudaGetDevice(&dev));
+  SCPL_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  SCPL_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  SCPL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - (int)fa.sharedSizeBytes));
+  done.insert(kernel);
+}
 std::atomic<long> g_launches{0};
 }  // namespace scpl
 
@@ -40,18 +59,18 @@ struct PwPlan {
 struct scpl_ctx {
   int device = 0;
   int num_sms = 148;
-  cudaStream_t s_h2d = nullptr, s_codes = nullptr, s_d2h = nullptr;  // host-buffer pipeline
+  cudaStream_t s_h2d = nullptr, s_codes = nullptr, s_d2h = nullptr, s_scan = nullptr;  // pipeline streams
   double* h_asde = nullptr;  // pinned
   int h_asde_cap = 0;
   std::map<long, PwPlan> plans;
   // device-side buffer scan
   ScanState* scan = nullptr;                       // device
-  ScanState* h_scan = nullptr;                     // pinned readback
-  int* h_runs = nullptr;                           // pinned, 2 * h_runs_cap ints
-  int h_runs_cap = 0;
   double* phi_d = nullptr;
   std::vector<double> phi_h;                       // contents of phi_d
   std::map<std::pair<long, int>, cudaGraphExec_t> scan_graphs;  // (N, spec)
+  uint8_t* pin = nullptr;  // pinned scratch (pinned_scratch)
+  size_t pin_cap = 0;
+  std::vector<cudaStream_t> s_carve;  // concurrent run groups
 };
 
 namespace {
@@ -125,32 +144,40 @@ double* pinned_asde(scpl_ctx* ctx, int n) {
   return ctx->h_asde;
 }
 
+// grow-only pinned scratch (one user at a time: the current C-ABI call)
+uint8_t* pinned_scratch(scpl_ctx* ctx, size_t bytes) {
+  if (ctx->pin_cap < bytes) {
+    if (ctx->pin) cudaFreeHost(ctx->pin);
+    ctx->pin = nullptr;
+    ctx->pin_cap = 0;
+    SCPL_CUDA(cudaMallocHost(&ctx->pin, bytes));
+    ctx->pin_cap = bytes;
+  }
+  return ctx->pin;
+}
+
 // ------------------------------------------------------------------ buffer scan
 // SpatioTemporalBuffer.push/flush over the whole clip (buffering.py:93-138), decided on
-// the device: one graph launch runs the scan as far as the frames whose codes are on the
-// device allow (a conditional while node around stats -> fold -> decide), so the host
-// never waits on an ASDE.  feed(c) makes chunk c's codes visible to `st` and returns the
-// number of frames available; chunks = number of feed calls (1 for a device clip).
-template <class Feed>
-std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* codes, int T, int H, int W,
-                                             const scpl_video_params& P, cudaStream_t st, int chunks,
-                                             Feed&& feed) {
-  std::vector<std::pair<int, int>> runs;
-  if (T == 0) return runs;
+// the device: each scan_chunk launch runs the scan as far as the frames whose codes are on
+// the device allow (a conditional while node around stats -> fold -> decide), then copies
+// the run count (and the append-only run list) to pinned memory, so the host can hand
+// closed runs to the carve while the scan goes on -- it never waits on an ASDE.
+struct ScanStream {
+  DBuf ck, leafsum, partial, runs_d;
+  cudaGraphExec_t graph = nullptr;
+  int T = 0;
+  int* h_n = nullptr;     // pinned: run count after each chunk
+  int* h_runs = nullptr;  // pinned: (start, len) pairs, 2T ints
+  ScanState* h_state = nullptr;
+};
+
+void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int H, int W,
+                const scpl_video_params& P, cudaStream_t st) {
   const long N = (long)H * W;
   const PwPlan& plan = plan_for(ctx, N);
   const int spec = P.spec_len > 0 ? P.spec_len : 8;
   SCPL_ARG(spec <= 64, "spec_len must be <= 64");
-  if (!ctx->scan) {
-    SCPL_CUDA(cudaMalloc(&ctx->scan, sizeof(ScanState)));
-    SCPL_CUDA(cudaMallocHost(&ctx->h_scan, sizeof(ScanState)));
-  }
-  if (ctx->h_runs_cap < T) {
-    if (ctx->h_runs) cudaFreeHost(ctx->h_runs);
-    ctx->h_runs = nullptr;
-    SCPL_CUDA(cudaMallocHost(&ctx->h_runs, sizeof(int) * 2 * T));
-    ctx->h_runs_cap = T;
-  }
+  if (!ctx->scan) SCPL_CUDA(cudaMalloc(&ctx->scan, sizeof(ScanState)));
   std::vector<double> phi(P.phi, P.phi + P.max_len + 1);
   if (phi != ctx->phi_h) {
     if (ctx->phi_h.size() < phi.size()) {
@@ -166,19 +193,21 @@ std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* code
   if (it == ctx->scan_graphs.end())
     it = ctx->scan_graphs.emplace(key, build_scan_graph(ctx->scan, plan.leaves, plan.nleaves, plan.vnodes, spec))
              .first;
-  DBuf ck(sizeof(double) * 2 * N, st);
-  DBuf leafsum(sizeof(double) * spec * plan.nleaves, st);
-  DBuf partial(sizeof(double) * spec * kPwFoldCtas, st);
-  DBuf runs_d(sizeof(int) * 2 * T, st);
+  S.graph = it->second;
+  S.T = T;
+  S.ck = DBuf(sizeof(double) * 2 * N, st);
+  S.leafsum = DBuf(sizeof(double) * spec * plan.nleaves, st);
+  S.partial = DBuf(sizeof(double) * spec * kPwFoldCtas, st);
+  S.runs_d = DBuf(sizeof(int) * 2 * T, st);
   ScanState init{};
   init.codes = codes;
   init.N = N;
-  init.ckS = ck.as<double>();
-  init.ckQ = ck.as<double>() + N;
-  init.leafsum = leafsum.as<double>();
-  init.partial = partial.as<double>();
+  init.ckS = S.ck.as<double>();
+  init.ckQ = S.ck.as<double>() + N;
+  init.leafsum = S.leafsum.as<double>();
+  init.partial = S.partial.as<double>();
   init.phi = ctx->phi_d;
-  init.runs = runs_d.as<int>();
+  init.runs = S.runs_d.as<int>();
   init.wm = P.w_motion;
   init.wg = P.w_grad;
   init.T = T;
@@ -189,19 +218,25 @@ std::vector<std::pair<int, int>> buffer_scan(scpl_ctx* ctx, const uint16_t* code
   init.n_acc = 1;
   init.init = 1;
   launch_scan_reset(ctx->scan, init, st);
-  for (int c = 0; c < chunks; ++c) {
-    const int avail = feed(c);
-    launch_scan_avail(ctx->scan, avail, st);
-    SCPL_CUDA(cudaGraphLaunch(it->second, st));
-  }
-  SCPL_CUDA(cudaMemcpyAsync(ctx->h_scan, ctx->scan, sizeof(ScanState), cudaMemcpyDeviceToHost, st));
-  SCPL_CUDA(cudaMemcpyAsync(ctx->h_runs, runs_d.p, sizeof(int) * 2 * T, cudaMemcpyDeviceToHost, st));
-  SCPL_CUDA(cudaStreamSynchronize(st));
-  const ScanState& R = *ctx->h_scan;
-  if (!(R.done == 1 && R.nruns >= 1 && R.nruns <= T)) throw Error{2, "buffer scan did not finish"};
+}
+
+void scan_chunk(scpl_ctx* ctx, ScanStream& S, int c, int avail, cudaStream_t st) {
+  launch_scan_avail(ctx->scan, avail, st);
+  SCPL_CUDA(cudaGraphLaunch(S.graph, st));
+  SCPL_CUDA(cudaMemcpyAsync(&S.h_n[c], reinterpret_cast<uint8_t*>(ctx->scan) + offsetof(ScanState, nruns),
+                            sizeof(int), cudaMemcpyDeviceToHost, st));
+  SCPL_CUDA(cudaMemcpyAsync(S.h_runs, S.runs_d.p, sizeof(int) * 2 * S.T, cudaMemcpyDeviceToHost, st));
+}
+
+void scan_end(scpl_ctx* ctx, ScanStream& S, cudaStream_t st) {
+  SCPL_CUDA(cudaMemcpyAsync(S.h_state, ctx->scan, sizeof(ScanState), cudaMemcpyDeviceToHost, st));
+}
+
+// after the stream is done
+void scan_finish(ScanStream& S, int chunks) {
+  const ScanState& R = *S.h_state;
+  if (!(R.done == 1 && R.nruns >= 1 && R.nruns <= S.T)) throw Error{2, "buffer scan did not finish"};
   g_launches.fetch_add((long)chunks + 3L * R.steps, std::memory_order_relaxed);
-  for (int r = 0; r < R.nruns; ++r) runs.push_back({ctx->h_runs[2 * r], ctx->h_runs[2 * r + 1]});
-  return runs;
 }
 
 // ------------------------------------------------------------------ carve driver
@@ -214,6 +249,15 @@ struct CarveSet {
   int rows = 0, cols = 0, pitch = 0, target = 0, cl = 1;
   size_t planes_bytes = 0;  // luma + gradient planes of every run, at the start of mem
   long long prof[4] = {0, 0, 0, 0};
+  cudaGraphExec_t loop = nullptr;  // device-side iteration loop (alive until the work completes)
+  CarveRun* h_runs = nullptr;      // pinned: run state after the carve (read once the stream is done)
+  int* h_iters = nullptr;          // pinned: loop iterations executed
+  CarveSet() = default;
+  CarveSet(const CarveSet&) = delete;
+  CarveSet& operator=(const CarveSet&) = delete;
+  ~CarveSet() {
+    if (loop) cudaGraphExecDestroy(loop);
+  }
 };
 
 void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
@@ -280,35 +324,38 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   }
 }
 
-// carve every run to its target: per iteration one cluster pass (DP + select + trace) and
-// the row kernels (compaction, gradient update); the host checks completion every 8 passes
-void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
-  (void)ctx;
+// Carve every run of a set to its target, asynchronously on st: one graph launch runs the
+// iteration loop on the device (pass, compaction, gradient until every run is done), then
+// the index kernel; the final run states land in pinned memory (h_runs / h_iters must hold
+// nruns CarveRuns and one int; they are read by carve_finish once the stream is done).
+void carve_launch(CarveSet& S, CarveRun* h_runs, int* h_iters, cudaStream_t st) {
   const int nruns = (int)S.runs.size();
+  S.h_runs = h_runs;
+  S.h_iters = h_iters;
+  *h_iters = 0;
   if (nruns == 0) return;
   for (auto& R : S.runs) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, 256, st));
+  std::memcpy(h_runs, S.runs.data(), sizeof(CarveRun) * nruns);
   S.runs_d = DBuf(sizeof(CarveRun) * nruns + 16, st);
-  SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, S.runs.data(), sizeof(CarveRun) * nruns, cudaMemcpyHostToDevice, st));
+  SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, h_runs, sizeof(CarveRun) * nruns, cudaMemcpyHostToDevice, st));
   int* iters_d = reinterpret_cast<int*>(S.runs_d.as<uint8_t>() + sizeof(CarveRun) * nruns);
   SCPL_CUDA(cudaMemsetAsync(iters_d, 0, sizeof(int), st));
-  cudaGraphExec_t loop = nullptr;
-  struct ExecGuard {
-    cudaGraphExec_t& e;
-    ~ExecGuard() {
-      if (e) cudaGraphExecDestroy(e);
-    }
-  } eg{loop};
   if (S.cols > S.target) {
-    loop = build_carve_loop(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1,
-                            iters_d);
-    SCPL_CUDA(cudaGraphLaunch(loop, st));
+    S.loop = build_carve_loop(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1,
+                              iters_d);
+    SCPL_CUDA(cudaGraphLaunch(S.loop, st));
   }
   launch_carve_index(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
-  SCPL_CUDA(cudaMemcpyAsync(S.runs.data(), S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
-  int iters_h = 0;
-  SCPL_CUDA(cudaMemcpyAsync(&iters_h, iters_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-  SCPL_CUDA(cudaStreamSynchronize(st));
-  g_launches.fetch_add(4L * iters_h, std::memory_order_relaxed);
+  SCPL_CUDA(cudaMemcpyAsync(h_runs, S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
+  SCPL_CUDA(cudaMemcpyAsync(h_iters, iters_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+// after the stream is done: run states back into S.runs, launch accounting, profile
+void carve_finish(CarveSet& S) {
+  const int nruns = (int)S.runs.size();
+  if (nruns == 0) return;
+  std::memcpy(S.runs.data(), S.h_runs, sizeof(CarveRun) * nruns);
+  g_launches.fetch_add(4L * *S.h_iters, std::memory_order_relaxed);
   for (auto& R : S.runs)
     if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;
@@ -318,7 +365,7 @@ void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
     if (getenv("SCPL_PROF"))
       fprintf(stderr,
               "carve prof: iters %d rows %d | dp %lld sel %lld | xwait %lld ringwait %lld rows %lld publish %lld"
-              " [bar1 %lld stores %lld bar2 %lld] store_pw %lld\n",
+              " [bar1 %lld stores %lld bar2 %lld] store_pw %lld\\n",
               R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11]);
     long long tot = c[0] + c[1];
     if (tot > best) {
@@ -326,6 +373,14 @@ void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
       for (int k = 0; k < 4; ++k) S.prof[k] = c[k];
     }
   }
+}
+
+void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
+  const int nruns = (int)S.runs.size();
+  uint8_t* pin = pinned_scratch(ctx, sizeof(CarveRun) * (size_t)std::max(nruns, 1) + 64);
+  carve_launch(S, reinterpret_cast<CarveRun*>(pin + 64), reinterpret_cast<int*>(pin), st);
+  SCPL_CUDA(cudaStreamSynchronize(st));
+  carve_finish(S);
 }
 
 }  // namespace
@@ -364,12 +419,12 @@ void scpl_destroy(scpl_ctx* ctx) {
     cudaFree(kv.second.vnodes);
   }
   if (ctx->h_asde) cudaFreeHost(ctx->h_asde);
+  if (ctx->pin) cudaFreeHost(ctx->pin);
+  for (cudaStream_t x : ctx->s_carve) cudaStreamDestroy(x);
   for (auto& kv : ctx->scan_graphs) cudaGraphExecDestroy(kv.second);
   if (ctx->scan) cudaFree(ctx->scan);
-  if (ctx->h_scan) cudaFreeHost(ctx->h_scan);
-  if (ctx->h_runs) cudaFreeHost(ctx->h_runs);
   if (ctx->phi_d) cudaFree(ctx->phi_d);
-  for (cudaStream_t x : {ctx->s_h2d, ctx->s_codes, ctx->s_d2h})
+  for (cudaStream_t x : {ctx->s_h2d, ctx->s_codes, ctx->s_d2h, ctx->s_scan})
     if (x) cudaStreamDestroy(x);
   delete ctx;
 }
@@ -481,10 +536,20 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
 
 namespace {
 
-// retarget_video (pipeline.py:92-137).  Device buffers (frames, out) or, when frames_host /
-// out_host are given, pinned host buffers: the clip then arrives in chunks on a copy stream
-// while the energy codes and the buffer scan start on the first chunks, and every run's
-// output frames leave on a second copy stream as soon as that run is replayed.
+// retarget_video (pipeline.py:92-137), streamed.  The clip (device buffer, or pinned host
+// buffer copied in 16-frame chunks on a copy stream) gets its energy codes and the device-
+// side buffer scan chunk by chunk; whenever the scan has closed enough runs, the host hands
+// them as one group to a carve stream: per phase (width, then height, or the reverse) a
+// run set is carved by the device-side iteration loop and replayed into the output, and
+// with host buffers the group's output frames leave on a second copy stream.  Groups carve
+// concurrently with the scan, the copies and each other (each carve is latency bound on a
+// few SMs).  Runs are independent, so the results do not depend on the grouping.
+struct Group {
+  std::list<CarveSet> sets;
+  std::list<DBuf> bufs;
+  cudaStream_t st = nullptr;
+};
+
 void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* frames_host, int T, int h, int w,
                    int channels, const scpl_video_params& P, uint8_t* out_dev, uint8_t* out_host,
                    scpl_video_result* result, cudaStream_t st) {
@@ -505,10 +570,41 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   const int tw = P.target_width, th = P.target_height;
   const size_t fbytes0 = (size_t)h * w * C;
   const bool host_in = frames_host != nullptr, host_out = out_host != nullptr;
-  if (host_in || host_out) {
-    for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_codes, &ctx->s_d2h})
-      if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
+  const bool buffered = P.mode == 2;
+  // the scan is the critical path (it releases the runs): codes and scan get the highest
+  // stream priority, the carve groups the lowest
+  int prio_lo = 0, prio_hi = 0;
+  SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_d2h})
+    if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
+  for (cudaStream_t* x : {&ctx->s_codes, &ctx->s_scan})
+    if (!*x) SCPL_CUDA(cudaStreamCreateWithPriority(x, cudaStreamNonBlocking, prio_hi));
+  const int kCarveStreams = 8;
+  while ((int)ctx->s_carve.size() < kCarveStreams) {
+    cudaStream_t x;
+    SCPL_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_lo));
+    ctx->s_carve.push_back(x);
   }
+  std::vector<int> phases;  // 0 width, 1 height (pipeline.py:192-193, 246-277)
+  for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
+    if (ax == 0 && tw < w) phases.push_back(0);
+    if (ax == 1 && th < h) phases.push_back(1);
+  }
+  const int chunk = 16;
+  const int nchunk = (T + chunk - 1) / chunk;
+
+  // pinned scratch: scan readbacks, then per group and phase the carve-run states
+  const size_t scan_pin = 64 + ((sizeof(int) * (nchunk + 2 * (size_t)T) + 63) & ~(size_t)63) + sizeof(ScanState);
+  const size_t need = scan_pin + (phases.size() + 1) * (size_t)T * (sizeof(CarveRun) + 64) + 4096;
+  uint8_t* pin = pinned_scratch(ctx, need);
+  size_t pin_used = 0;
+  auto pin_take = [&](size_t bytes) {
+    uint8_t* q = pin + pin_used;
+    pin_used += (bytes + 63) & ~(size_t)63;
+    SCPL_ARG(pin_used <= need, "internal: pinned scratch exhausted");
+    return q;
+  };
+
   std::vector<cudaEvent_t> events;
   struct EvGuard {
     std::vector<cudaEvent_t>& e;
@@ -522,162 +618,234 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     events.push_back(e);
     return e;
   };
-  cudaEvent_t ev[5];
-  for (auto& e : ev) e = new_event(true);
-  float carve_ms = 0.f, replay_ms = 0.f;
-  SCPL_CUDA(cudaEventRecord(ev[0], st));
+  cudaEvent_t ev_start = new_event(true), ev_codes = new_event(true), ev_scan = new_event(true),
+              ev_end = new_event(true);
+  SCPL_CUDA(cudaEventRecord(ev_start, st));
 
-  // 0. frames (host: chunked H2D on the copy stream)
-  DBuf frames_buf;
+  // buffers (stream-ordered on st; every other stream waits for ev_alloc)
+  DBuf frames_buf, codes, out_buf;
   const uint8_t* frames = frames_dev;
-  const int chunk = 16;
-  const int nchunk = (T + chunk - 1) / chunk;
-  std::vector<cudaEvent_t> ev_codes;
   if (host_in) {
-    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev[0], 0));  // after earlier work on st
     frames_buf = DBuf(fbytes0 * T, st);
-    SCPL_CUDA(cudaEventRecord(ev[1], st));
-    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev[1], 0));  // the allocation is ordered on st
     frames = frames_buf.as<uint8_t>();
   }
-  // 1. energy codes (not needed by raw mode: gradient only)
-  DBuf codes;
   if (P.mode != 0) codes = DBuf(sizeof(uint16_t) * (size_t)T * h * w, st);
+  uint8_t* out = out_dev;
+  if (host_out) {
+    out_buf = DBuf((size_t)T * th * tw * C, st);
+    out = out_buf.as<uint8_t>();
+  }
+  ScanStream scan;
+  if (buffered) {
+    scan.h_n = reinterpret_cast<int*>(pin_take(sizeof(int) * nchunk));
+    scan.h_runs = reinterpret_cast<int*>(pin_take(sizeof(int) * 2 * (size_t)T));
+    scan.h_state = reinterpret_cast<ScanState*>(pin_take(sizeof(ScanState)));
+    scan_start(ctx, scan, codes.as<uint16_t>(), T, h, w, P, st);
+  }
+  std::list<Group> groups;
+  const bool timeline = getenv("SCPL_TIMELINE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;  // (label, timing event)
+  const auto t_host0 = std::chrono::steady_clock::now();
+  auto hmark = [&](const std::string& label) {
+    if (!timeline) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    fprintf(stderr, "host %8.3f ms  %s\n", ms, label.c_str());
+  };
+  auto mark = [&](const std::string& label, cudaStream_t sm) {
+    if (!timeline) return;
+    cudaEvent_t e = new_event(true);
+    SCPL_CUDA(cudaEventRecord(e, sm));
+    marks.push_back({label, e});
+  };
+  // from here on, anything that unwinds must first let the queued work finish
+  struct DrainGuard {
+    bool armed = true;
+    ~DrainGuard() {
+      if (armed) cudaDeviceSynchronize();
+    }
+  } drain;
+  cudaEvent_t ev_alloc = new_event(false);
+  SCPL_CUDA(cudaEventRecord(ev_alloc, st));
+
+  // 1. frames in (host) and energy codes, chunk by chunk
+  std::vector<cudaEvent_t> ev_chunk_codes(nchunk, nullptr);
   if (host_in) {
-    cudaEvent_t ready_codes = new_event(false);
-    SCPL_CUDA(cudaEventRecord(ready_codes, st));
-    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ready_codes, 0));
+    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
+    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ev_alloc, 0));
     for (int c = 0; c < nchunk; ++c) {
       const int t0 = c * chunk, n = std::min(chunk, T - t0);
       SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
                                 fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
+      mark("h2d " + std::to_string(c), ctx->s_h2d);
       cudaEvent_t e = new_event(false);
       SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
       SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, e, 0));
       if (P.mode != 0)
         launch_codes(frames, nullptr, t0, n, h, w, C, codes.as<uint16_t>(), ctx->num_sms, ctx->s_codes);
-      cudaEvent_t ec = new_event(false);
-      SCPL_CUDA(cudaEventRecord(ec, ctx->s_codes));
-      ev_codes.push_back(ec);
+      ev_chunk_codes[c] = new_event(false);
+      SCPL_CUDA(cudaEventRecord(ev_chunk_codes[c], ctx->s_codes));
     }
-  } else if (P.mode != 0) {
-    launch_codes(frames, nullptr, 0, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, st);
   }
-  int codes_ready = host_in ? -1 : nchunk - 1;  // chunks st already waits for
-  auto ensure_codes = [&](int t_max) {
-    const int c = std::min(nchunk - 1, t_max / chunk);
-    while (codes_ready < c) SCPL_CUDA(cudaStreamWaitEvent(st, ev_codes[++codes_ready], 0));
-  };
-  auto feed = [&](int c) {  // chunk c of the scan: frames [0, avail) have codes on st
-    if (!host_in) return T;
-    ensure_codes(c * chunk);
-    return std::min(T, (c + 1) * chunk);
-  };
-  SCPL_CUDA(cudaEventRecord(ev[1], st));
-  // 2. runs
+  cudaStream_t ss = ctx->s_scan;
+  SCPL_CUDA(cudaStreamWaitEvent(ss, ev_alloc, 0));
+  if (!host_in && P.mode != 0) launch_codes(frames, nullptr, 0, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, ss);
+  SCPL_CUDA(cudaEventRecord(ev_codes, ss));
+
+  // 2. buffer scan, chunk by chunk (fixed one-frame runs for scpl / raw)
+  std::vector<cudaEvent_t> ev_chunk(nchunk, nullptr);
+  if (buffered) {
+    for (int c = 0; c < nchunk; ++c) {
+      if (host_in) SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[c], 0));
+      scan_chunk(ctx, scan, c, std::min(T, (c + 1) * chunk), ss);
+      mark("scan " + std::to_string(c), ss);
+      ev_chunk[c] = new_event(false);
+      SCPL_CUDA(cudaEventRecord(ev_chunk[c], ss));
+    }
+    scan_end(ctx, scan, ss);
+  } else if (host_in) {
+    SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[nchunk - 1], 0));
+  }
+  SCPL_CUDA(cudaEventRecord(ev_scan, ss));
+
+  // 3. carve + replay, one run group at a time as runs close
   std::vector<std::pair<int, int>> runs;
-  if (P.mode == 2) {
-    runs = buffer_scan(ctx, codes.as<uint16_t>(), T, h, w, P, st, host_in ? nchunk : 1, feed);
+  int next_stream = 0;
+  auto dispatch = [&](int r0, int r1, cudaEvent_t ready) {
+    if (r1 <= r0) return;
+    Group& G = groups.emplace_back();
+    G.st = ctx->s_carve[next_stream++ % kCarveStreams];
+    cudaStream_t gs = G.st;
+    SCPL_CUDA(cudaStreamWaitEvent(gs, ev_alloc, 0));
+    SCPL_CUDA(cudaStreamWaitEvent(gs, ready, 0));
+    const int nr = r1 - r0;
+    const int ta = runs[r0].first, tb = runs[r1 - 1].first + runs[r1 - 1].second;
+    mark("group " + std::to_string(groups.size() - 1) + " start", gs);
+    auto ship = [&](size_t off, size_t bytes) {  // D2H of finished output frames
+      if (!host_out) return;
+      cudaEvent_t e = new_event(false);
+      SCPL_CUDA(cudaEventRecord(e, gs));
+      SCPL_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
+      SCPL_CUDA(cudaMemcpyAsync(out_host + off, out + off, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    };
+    if (phases.empty()) {
+      SCPL_CUDA(cudaMemcpyAsync(out + fbytes0 * ta, frames + fbytes0 * ta, fbytes0 * (tb - ta),
+                                cudaMemcpyDeviceToDevice, gs));
+      ship(fbytes0 * ta, fbytes0 * (tb - ta));
+      return;
+    }
+    const uint8_t* cur = frames;
+    int cur_t0 = 0, curH = h, curW = w;
+    for (size_t ph = 0; ph < phases.size(); ++ph) {
+      const bool height = phases[ph] == 1;
+      const int rows = height ? curW : curH, cols = height ? curH : curW;
+      const int target = height ? th : tw;
+      const bool with_U = (ph == 0) && P.mode != 0;
+      CarveSet& S = G.sets.emplace_back();
+      hmark("group alloc");
+      carve_alloc(S, nr, rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
+                  carve_cluster_size(nr, cols, ctx->num_sms), gs);
+      hmark("group setup");
+      const size_t fbytes = (size_t)curH * curW * C;
+      for (int r = r0; r < r1; ++r) {
+        CarveRun& R = S.runs[r - r0];
+        const int s0 = runs[r].first;
+        // the first carved axis works on the original frames, whose energy codes carry the
+        // Sobel gradient of every frame (so the carve's gradient plane needs no recompute)
+        const uint16_t* fcodes = (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)s0 * h * w : nullptr;
+        launch_run_setup(cur + fbytes * (s0 - cur_t0), curH, curW, C, height ? 1 : 0, fcodes, R, gs);
+        if (with_U)
+          launch_uniform(codes.as<uint16_t>(), h, w, s0, runs[r].second, 1, P.w_motion, P.w_grad, height ? 1 : 0,
+                         const_cast<double*>(R.U), gs, R.pitch);
+      }
+      mark("group " + std::to_string(groups.size() - 1) + " setup done", gs);
+      hmark("group carve_launch");
+      carve_launch(S, reinterpret_cast<CarveRun*>(pin_take(sizeof(CarveRun) * nr)),
+                   reinterpret_cast<int*>(pin_take(sizeof(int))), gs);
+      hmark("group replay");
+      mark("group " + std::to_string(groups.size() - 1) + " carve done", gs);
+      const int nH = height ? th : curH, nW = height ? curW : tw;
+      const bool last = ph + 1 == phases.size();
+      uint8_t* dst = out;
+      int dst_t0 = 0;
+      if (!last) {
+        dst = G.bufs.emplace_back((size_t)(tb - ta) * nH * nW * C, gs).as<uint8_t>();
+        dst_t0 = ta;
+      }
+      const size_t obytes = (size_t)nH * nW * C;
+      for (int r = r0; r < r1; ++r) {
+        const CarveRun& R = S.runs[r - r0];
+        const int s0 = runs[r].first, n = runs[r].second;
+        launch_replay(cur + fbytes * (s0 - cur_t0), dst + obytes * (s0 - dst_t0), n, curH, curW, C, R.idx, R.pitch,
+                      target, height ? 1 : 0, gs);
+        if (last) ship(obytes * s0, obytes * n);
+      }
+      mark("group " + std::to_string(groups.size() - 1) + " phase " + std::to_string(ph) + " runs " +
+               std::to_string(nr), gs);
+      cur = dst;
+      cur_t0 = dst_t0;
+      curH = nH;
+      curW = nW;
+    }
+    if (host_out) mark("d2h group " + std::to_string(groups.size() - 1), ctx->s_d2h);
+  };
+  if (buffered) {
+    int min_group = 4;
+    if (const char* e = getenv("SCPL_GROUP_MIN")) min_group = std::max(1, atoi(e));
+    int done = 0;
+    for (int c = 0; c < nchunk; ++c) {
+      hmark("wait chunk " + std::to_string(c));
+      SCPL_CUDA(cudaEventSynchronize(ev_chunk[c]));
+      const int n = scan.h_n[c];
+      for (int r = (int)runs.size(); r < n; ++r) runs.push_back({scan.h_runs[2 * r], scan.h_runs[2 * r + 1]});
+      if (n - done >= min_group || (c + 1 == nchunk && n > done)) {
+        dispatch(done, n, ev_chunk[c]);
+        done = n;
+      }
+    }
   } else {
     for (int t = 0; t < T; ++t) runs.push_back({t, 1});
+    dispatch(0, T, ev_scan);
   }
-  ensure_codes(T - 1);  // every frame and code is on the device from here on
-  SCPL_CUDA(cudaEventRecord(ev[2], st));
-  SCPL_CUDA(cudaEventSynchronize(ev[2]));
-  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[0], ev[0], ev[1]));
-  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[1], ev[1], ev[2]));
+  SCPL_CUDA(cudaStreamWaitEvent(st, ev_scan, 0));
+  for (Group& G : groups) {
+    cudaEvent_t e = new_event(false);
+    SCPL_CUDA(cudaEventRecord(e, G.st));
+    SCPL_CUDA(cudaStreamWaitEvent(st, e, 0));
+  }
+  if (host_out) {
+    cudaEvent_t e = new_event(false);
+    SCPL_CUDA(cudaEventRecord(e, ctx->s_d2h));
+    SCPL_CUDA(cudaStreamWaitEvent(st, e, 0));
+  }
+  SCPL_CUDA(cudaEventRecord(ev_end, st));
+  SCPL_CUDA(cudaStreamSynchronize(st));
+  drain.armed = false;
+
+  // 4. results
+  if (buffered) scan_finish(scan, nchunk);
   result->n_runs = (int)runs.size();
   if (result->run_start && result->run_len)
     for (size_t r = 0; r < runs.size(); ++r) {
       result->run_start[r] = runs[r].first;
       result->run_len[r] = runs[r].second;
     }
-
-  // 3. phases (pipeline.py:192-193, 246-277)
-  std::vector<int> phases;  // 0 width, 1 height
-  for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
-    if (ax == 0 && tw < w) phases.push_back(0);
-    if (ax == 1 && th < h) phases.push_back(1);
-  }
-  DBuf out_buf;
-  uint8_t* out = out_dev;
-  if (host_out) {
-    out_buf = DBuf((size_t)T * th * tw * C, st);
-    out = out_buf.as<uint8_t>();
-  }
-  auto ship = [&](size_t off, size_t bytes) {  // D2H of finished output frames
-    if (!host_out) return;
-    cudaEvent_t e = new_event(false);
-    SCPL_CUDA(cudaEventRecord(e, st));
-    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
-    SCPL_CUDA(cudaMemcpyAsync(out_host + off, out + off, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
-  };
-  if (phases.empty()) {
-    SCPL_CUDA(cudaMemcpyAsync(out, frames, (size_t)T * h * w * C, cudaMemcpyDeviceToDevice, st));
-    ship(0, (size_t)T * h * w * C);
-  }
-  const uint8_t* cur = frames;
-  int curH = h, curW = w;
-  DBuf tmp;
   long dp = 0;
-  for (size_t ph = 0; ph < phases.size(); ++ph) {
-    const bool height = phases[ph] == 1;
-    const int rows = height ? curW : curH, cols = height ? curH : curW;
-    const int target = height ? th : tw;
-    const bool with_U = (ph == 0) && P.mode != 0;
-    CarveSet S;
-    carve_alloc(S, (int)runs.size(), rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
-                carve_cluster_size((int)runs.size(), cols, ctx->num_sms), st);
-    const size_t fbytes = (size_t)curH * curW * C;
-    for (size_t r = 0; r < runs.size(); ++r) {
-      CarveRun& R = S.runs[r];
-      // the first carved axis works on the original frames, whose energy codes carry the
-      // Sobel gradient of every frame (so the carve's gradient plane needs no recompute)
-      const uint16_t* fcodes = (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)runs[r].first * h * w
-                                                         : nullptr;
-      launch_run_setup(cur + fbytes * runs[r].first, curH, curW, C, height ? 1 : 0, fcodes, R, st);
-      if (with_U)
-        launch_uniform(codes.as<uint16_t>(), h, w, runs[r].first, runs[r].second, 1, P.w_motion, P.w_grad,
-                       height ? 1 : 0, const_cast<double*>(R.U), st, R.pitch);
+  for (Group& G : groups)
+    for (CarveSet& S : G.sets) {
+      carve_finish(S);
+      for (auto& R : S.runs) dp += R.iters;
+      for (int k = 0; k < 4; ++k) result->carve_cycles[k] = std::max(result->carve_cycles[k], S.prof[k]);
+      result->carve_cluster = S.cl;
     }
-    SCPL_CUDA(cudaEventRecord(ev[3], st));
-    carve_run_all(ctx, S, st);
-    SCPL_CUDA(cudaEventRecord(ev[4], st));
-    for (auto& R : S.runs) dp += R.iters;
-    for (int k = 0; k < 4; ++k) result->carve_cycles[k] += S.prof[k];
-    result->carve_cluster = S.cl;
-    const int nH = height ? th : curH, nW = height ? curW : tw;
-    const bool last = ph + 1 == phases.size();
-    DBuf next;
-    uint8_t* dst = out;
-    if (!last) {
-      next = DBuf((size_t)T * nH * nW * C, st);
-      dst = next.as<uint8_t>();
-    }
-    const size_t obytes = (size_t)nH * nW * C;
-    for (size_t r = 0; r < runs.size(); ++r) {
-      const CarveRun& R = S.runs[r];
-      launch_replay(cur + fbytes * runs[r].first, dst + obytes * runs[r].first, runs[r].second, curH, curW, C,
-                    R.idx, R.pitch, target, height ? 1 : 0, st);
-      if (last) ship(obytes * runs[r].first, obytes * runs[r].second);
-    }
-    SCPL_CUDA(cudaEventRecord(ev[2], st));
-    SCPL_CUDA(cudaEventSynchronize(ev[2]));
-    float a = 0.f, b = 0.f;
-    SCPL_CUDA(cudaEventElapsedTime(&a, ev[3], ev[4]));
-    SCPL_CUDA(cudaEventElapsedTime(&b, ev[4], ev[2]));
-    carve_ms += a;
-    replay_ms += b;
-    cur = dst;
-    curH = nH;
-    curW = nW;
-    tmp = std::move(next);
-  }
   result->dp_passes = dp;
-  if (host_out) SCPL_CUDA(cudaStreamSynchronize(ctx->s_d2h));
-  SCPL_CUDA(cudaStreamSynchronize(st));
-  result->phase_ms[2] = carve_ms;
-  result->phase_ms[3] = replay_ms;
+  for (auto& m : marks) {
+    float ms = 0.f;
+    SCPL_CUDA(cudaEventElapsedTime(&ms, ev_start, m.second));
+    fprintf(stderr, "timeline %8.3f ms  %s\n", ms, m.first.c_str());
+  }
+  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[0], ev_start, ev_codes));
+  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[1], ev_codes, ev_scan));
+  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[2], ev_scan, ev_end));
 }
 
 }  // namespace

@@ -1218,7 +1218,7 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   const bool stage = carve_stage_dtab(rows, pitch, cl);
   size_t smem = carve_smem_bytes(rows, pitch, stage, 0, dpw);
   SCPL_ARG(smem <= 227 * 1024, "carve plane too large for shared memory");
-  SCPL_CUDA(cudaFuncSetAttribute(carve_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin(reinterpret_cast<const void*>(carve_pass_kernel));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nruns * cl);
   cfg.blockDim = dim3(kMaxWarps * 32);
@@ -1235,7 +1235,7 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   SCPL_CHECK_LAUNCH();
   dim3 rgrid(cdiv(rows, kRowWarps), nruns);
   const size_t csmem = carve_compact_smem(pitch);
-  SCPL_CUDA(cudaFuncSetAttribute(carve_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  smem_optin(reinterpret_cast<const void*>(carve_compact_kernel));
   carve_compact_kernel<<<rgrid, kRowWarps * 32, csmem, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();
   carve_dirty_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);

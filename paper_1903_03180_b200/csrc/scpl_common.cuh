@@ -34,6 +34,10 @@ struct Error {
 
 static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 
+// Opt a kernel into the full 227 KB of dynamic shared memory, once per process: setting a
+// function attribute while that kernel runs on another stream can serialise the host.
+void smem_optin(const void* kernel);
+
 // ---------------------------------------------------------------- exact arithmetic
 // energy.py:35 -- luma = rint(fma(b,.114, fma(r,.299, g*.587))).  Outside the exact
 // half cases (299r+587g+114b == 500 mod 1000) the rounded value is the nearest integer

@@ -314,10 +314,12 @@ static void launch_codes_c(const uint8_t* frames, const uint8_t* prev_frame, int
   const size_t smem = 2 * (size_t)G::kSlot + (size_t)kCRows * kLumStride + 16;
   const int tiles_x = cdiv(W, kCW), tiles = tiles_x * cdiv(H, kCH);
   const long units = (long)tiles * n;
-  int per_sm = 0;
-  SCPL_CUDA(cudaFuncSetAttribute(codes_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SCPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, codes_kernel<C>, kCodesThreads, smem));
-  if (per_sm < 1) per_sm = 1;
+  static int per_sm = 0;  // resident CTAs per SM (queried once)
+  if (per_sm == 0) {
+    smem_optin(reinterpret_cast<const void*>(codes_kernel<C>));
+    SCPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, codes_kernel<C>, kCodesThreads, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
   const long grid = std::min<long>(units, (long)num_sms * per_sm);
   codes_kernel<C><<<(int)grid, kCodesThreads, smem, st>>>(tm, frames, prev_frame, t0, n, H, W, tiles_x, units,
                                                            tma ? 1 : 0, codes);

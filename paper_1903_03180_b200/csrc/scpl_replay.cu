@@ -91,10 +91,10 @@ void launch_replay(const uint8_t* in, uint8_t* out, int T, int H, int W, int C, 
     SCPL_ARG(smem <= 227 * 1024, "frame too wide for the replay kernel");
     dim3 grid(cdiv(H, kReplayRows), T);
     if (C == 3) {
-      SCPL_CUDA(cudaFuncSetAttribute(replay_rows_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_optin(reinterpret_cast<const void*>(replay_rows_kernel<3>));
       replay_rows_kernel<3><<<grid, 256, smem, st>>>(in, out, H, W, idx, stride, target, vec ? 1 : 0);
     } else {
-      SCPL_CUDA(cudaFuncSetAttribute(replay_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_optin(reinterpret_cast<const void*>(replay_rows_kernel<1>));
       replay_rows_kernel<1><<<grid, 256, smem, st>>>(in, out, H, W, idx, stride, target, vec ? 1 : 0);
     }
   } else {

@@ -240,9 +240,8 @@ __global__ void __launch_bounds__(256) window_stats_scan_kernel(const ScanState*
 static void stats_smem_attr() {
   static bool done = false;
   if (done) return;
-  SCPL_CUDA(cudaFuncSetAttribute(window_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStatSmem));
-  SCPL_CUDA(cudaFuncSetAttribute(window_stats_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kStatSmem));
+  smem_optin(reinterpret_cast<const void*>(window_stats_kernel));
+  smem_optin(reinterpret_cast<const void*>(window_stats_scan_kernel));
   done = true;
 }
 

@@ -135,7 +135,7 @@ void launch_select_tables(const double* last, const long* labels, int w, int k, 
                           cudaStream_t st) {
   size_t smem = (size_t)w * (8 + 4 + 4);
   SCPL_ARG(smem <= 227 * 1024, "map too wide for select_batch");
-  SCPL_CUDA(cudaFuncSetAttribute(select_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin(reinterpret_cast<const void*>(select_tables_kernel));
   select_tables_kernel<<<1, 1024, smem, st>>>(last, labels, w, k, cols, costs, nb);
   SCPL_CHECK_LAUNCH();
 }
