@@ -223,13 +223,13 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int 
 void scan_chunk(scpl_ctx* ctx, ScanStream& S, int c, int avail, cudaStream_t st) {
   launch_scan_avail(ctx->scan, avail, st);
   SCPL_CUDA(cudaGraphLaunch(S.graph, st));
-  SCPL_CUDA(cudaMemcpyAsync(&S.h_n[c], reinterpret_cast<uint8_t*>(ctx->scan) + offsetof(ScanState, nruns),
-                            sizeof(int), cudaMemcpyDeviceToHost, st));
-  SCPL_CUDA(cudaMemcpyAsync(S.h_runs, S.runs_d.p, sizeof(int) * 2 * S.T, cudaMemcpyDeviceToHost, st));
+  // (SM copies into mapped pinned memory: no copy-engine queueing behind the clip's copies)
+  launch_word_copy(&S.h_n[c], reinterpret_cast<uint8_t*>(ctx->scan) + offsetof(ScanState, nruns), sizeof(int), st);
+  launch_word_copy(S.h_runs, S.runs_d.p, sizeof(int) * 2 * S.T, st);
 }
 
 void scan_end(scpl_ctx* ctx, ScanStream& S, cudaStream_t st) {
-  SCPL_CUDA(cudaMemcpyAsync(S.h_state, ctx->scan, sizeof(ScanState), cudaMemcpyDeviceToHost, st));
+  launch_word_copy(S.h_state, ctx->scan, sizeof(ScanState), st);
 }
 
 // after the stream is done
@@ -337,7 +337,7 @@ void carve_launch(CarveSet& S, CarveRun* h_runs, int* h_iters, cudaStream_t st) 
   for (auto& R : S.runs) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, 256, st));
   std::memcpy(h_runs, S.runs.data(), sizeof(CarveRun) * nruns);
   S.runs_d = DBuf(sizeof(CarveRun) * nruns + 16, st);
-  SCPL_CUDA(cudaMemcpyAsync(S.runs_d.p, h_runs, sizeof(CarveRun) * nruns, cudaMemcpyHostToDevice, st));
+  launch_word_copy(S.runs_d.p, h_runs, sizeof(CarveRun) * nruns, st);  // from mapped pinned memory
   int* iters_d = reinterpret_cast<int*>(S.runs_d.as<uint8_t>() + sizeof(CarveRun) * nruns);
   SCPL_CUDA(cudaMemsetAsync(iters_d, 0, sizeof(int), st));
   if (S.cols > S.target) {
@@ -346,8 +346,8 @@ void carve_launch(CarveSet& S, CarveRun* h_runs, int* h_iters, cudaStream_t st) 
     SCPL_CUDA(cudaGraphLaunch(S.loop, st));
   }
   launch_carve_index(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
-  SCPL_CUDA(cudaMemcpyAsync(h_runs, S.runs_d.p, sizeof(CarveRun) * nruns, cudaMemcpyDeviceToHost, st));
-  SCPL_CUDA(cudaMemcpyAsync(h_iters, iters_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  launch_word_copy(h_runs, S.runs_d.p, sizeof(CarveRun) * nruns, st);
+  launch_word_copy(h_iters, iters_d, sizeof(int), st);
 }
 
 // after the stream is done: run states back into S.runs, launch accounting, profile
@@ -575,6 +575,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   // stream priority, the carve groups the lowest
   int prio_lo = 0, prio_hi = 0;
   SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  if (getenv("SCPL_NO_PRIO")) prio_lo = prio_hi = 0;
   for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_d2h})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
   for (cudaStream_t* x : {&ctx->s_codes, &ctx->s_scan})
@@ -672,10 +673,15 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   if (host_in) {
     SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
     SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ev_alloc, 0));
+    const bool oneshot = getenv("SCPL_H2D_ONESHOT") != nullptr;  // experiment
+    if (oneshot)
+      SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames), frames_host, fbytes0 * T, cudaMemcpyHostToDevice,
+                                ctx->s_h2d));
     for (int c = 0; c < nchunk; ++c) {
       const int t0 = c * chunk, n = std::min(chunk, T - t0);
-      SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
-                                fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
+      if (!oneshot)
+        SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
+                                  fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
       mark("h2d " + std::to_string(c), ctx->s_h2d);
       cudaEvent_t e = new_event(false);
       SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));

@@ -31,6 +31,7 @@
 //     pixel of rows i-1..i+1 lay within one column of it; only those are recomputed.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 
@@ -1239,6 +1240,22 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   carve_compact_kernel<<<rgrid, kRowWarps * 32, csmem, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();
   carve_dirty_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
+  SCPL_CHECK_LAUNCH();
+}
+
+// Word copy by the SMs.  Small control transfers between device memory and mapped pinned
+// host memory go through here instead of the copy engines, so they never queue behind the
+// clip's bulk host<->device copies.
+__global__ void word_copy_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  const size_t n = (bytes + 3) / 4;
+  word_copy_kernel<<<(int)std::min<size_t>(cdiv((long)n, 256), 64), 256, 0, st>>>(
+      reinterpret_cast<uint32_t*>(dst), reinterpret_cast<const uint32_t*>(src), n);
   SCPL_CHECK_LAUNCH();
 }
 

@@ -90,6 +90,8 @@ int carve_cluster_size(int nruns, int width, int num_sms);
 void encode_carve_tensor_maps(CarveRun& R);
 void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st);
 void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st);
+// dst/src: device or mapped pinned host memory; bytes rounded up to whole words (4-aligned)
+void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // 4 kernels per executed iteration (pass, compact, gradient, check); iters_d counts them
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
                                  int* iters_d);
