@@ -575,12 +575,11 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   // stream priority, the carve groups the lowest
   int prio_lo = 0, prio_hi = 0;
   SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  if (getenv("SCPL_NO_PRIO")) prio_lo = prio_hi = 0;
   for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_d2h})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
   for (cudaStream_t* x : {&ctx->s_codes, &ctx->s_scan})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithPriority(x, cudaStreamNonBlocking, prio_hi));
-  const int kCarveStreams = 8;
+  const int kCarveStreams = 16;
   while ((int)ctx->s_carve.size() < kCarveStreams) {
     cudaStream_t x;
     SCPL_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_lo));
@@ -673,15 +672,10 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   if (host_in) {
     SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
     SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ev_alloc, 0));
-    const bool oneshot = getenv("SCPL_H2D_ONESHOT") != nullptr;  // experiment
-    if (oneshot)
-      SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames), frames_host, fbytes0 * T, cudaMemcpyHostToDevice,
-                                ctx->s_h2d));
     for (int c = 0; c < nchunk; ++c) {
       const int t0 = c * chunk, n = std::min(chunk, T - t0);
-      if (!oneshot)
-        SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
-                                  fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
+      SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
+                                fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
       mark("h2d " + std::to_string(c), ctx->s_h2d);
       cudaEvent_t e = new_event(false);
       SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
@@ -795,7 +789,9 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     if (host_out) mark("d2h group " + std::to_string(groups.size() - 1), ctx->s_d2h);
   };
   if (buffered) {
-    int min_group = 4;
+    // host clips: every closed run goes out at once (the copies are the bottleneck); device
+    // clips: groups of >= 4 runs (fewer, larger carve sets)
+    int min_group = host_in ? 1 : 4;
     if (const char* e = getenv("SCPL_GROUP_MIN")) min_group = std::max(1, atoi(e));
     int done = 0;
     for (int c = 0; c < nchunk; ++c) {

@@ -280,3 +280,23 @@ def test_host_buffers_unpinned_and_odd_chunks(P):
     r = O.retarget_video(list(clip), target_width=29, target_height=21, mode="buffered")
     assert r.dp_passes == ma.dp_passes
     assert all(np.array_equal(a[t].numpy(), r.frames[t]) for t in range(len(clip)))
+
+
+@pytest.mark.parametrize("group_min", ["1", "3", "1000"])
+@pytest.mark.parametrize("host", [False, True])
+def test_run_grouping_does_not_change_results(P, group_min, host, monkeypatch):
+    """Runs are carved in groups dispatched as the scan closes them; any grouping (one run per
+    group, a few, or one group after the whole scan) must give the reference's frames."""
+    from paper_1903_03180_b200.synth import config_clip
+    import torch
+    path = _config_golden("C4_clip0")[0]
+    g = json.load(open(path))
+    clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
+    monkeypatch.setenv("SCPL_GROUP_MIN", group_min)
+    cfg = P.RetargetConfig(target_width=tw, target_height=th, mode="buffered")
+    t = torch.from_numpy(clip)
+    out, m = P.retarget_video(t.pin_memory() if host else t.cuda(), cfg)
+    host_out = out.cpu().numpy()
+    assert [list(r) for r in m.runs] == g["runs"] and m.dp_passes == g["dp_passes"]
+    bad = [i for i in range(host_out.shape[0]) if sha(host_out[i]) != g["frames_sha"][i]]
+    assert not bad, f"{len(bad)} frames differ"
