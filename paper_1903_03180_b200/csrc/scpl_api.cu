@@ -144,6 +144,10 @@ double* pinned_asde(scpl_ctx* ctx, int n) {
   return ctx->h_asde;
 }
 
+// SCPL_HOST_LOOPS=1: drive the scan and carve loops from the host instead of conditional
+// graphs (identical results; lets a profiler see every kernel)
+bool host_loops() { return getenv("SCPL_HOST_LOOPS") != nullptr; }
+
 // grow-only pinned scratch (one user at a time: the current C-ABI call)
 uint8_t* pinned_scratch(scpl_ctx* ctx, size_t bytes) {
   if (ctx->pin_cap < bytes) {
@@ -165,6 +169,9 @@ uint8_t* pinned_scratch(scpl_ctx* ctx, size_t bytes) {
 struct ScanStream {
   DBuf ck, leafsum, partial, runs_d;
   cudaGraphExec_t graph = nullptr;
+  const PwPlan* plan = nullptr;
+  int spec = 8;
+  int* h_L = nullptr;  // pinned (host-driven loops)
   int T = 0;
   int* h_n = nullptr;     // pinned: run count after each chunk
   int* h_runs = nullptr;  // pinned: (start, len) pairs, 2T ints
@@ -194,6 +201,8 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int 
     it = ctx->scan_graphs.emplace(key, build_scan_graph(ctx->scan, plan.leaves, plan.nleaves, plan.vnodes, spec))
              .first;
   S.graph = it->second;
+  S.plan = &plan;
+  S.spec = spec;
   S.T = T;
   S.ck = DBuf(sizeof(double) * 2 * N, st);
   S.leafsum = DBuf(sizeof(double) * spec * plan.nleaves, st);
@@ -222,7 +231,10 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int 
 
 void scan_chunk(scpl_ctx* ctx, ScanStream& S, int c, int avail, cudaStream_t st) {
   launch_scan_avail(ctx->scan, avail, st);
-  SCPL_CUDA(cudaGraphLaunch(S.graph, st));
+  if (host_loops())
+    run_scan_host(ctx->scan, S.plan->leaves, S.plan->nleaves, S.plan->vnodes, S.spec, S.h_L, st);
+  else
+    SCPL_CUDA(cudaGraphLaunch(S.graph, st));
   // (SM copies into mapped pinned memory: no copy-engine queueing behind the clip's copies)
   launch_word_copy(&S.h_n[c], reinterpret_cast<uint8_t*>(ctx->scan) + offsetof(ScanState, nruns), sizeof(int), st);
   launch_word_copy(S.h_runs, S.runs_d.p, sizeof(int) * 2 * S.T, st);
@@ -340,7 +352,18 @@ void carve_launch(CarveSet& S, CarveRun* h_runs, int* h_iters, cudaStream_t st) 
   launch_word_copy(S.runs_d.p, h_runs, sizeof(CarveRun) * nruns, st);  // from mapped pinned memory
   int* iters_d = reinterpret_cast<int*>(S.runs_d.as<uint8_t>() + sizeof(CarveRun) * nruns);
   SCPL_CUDA(cudaMemsetAsync(iters_d, 0, sizeof(int), st));
-  if (S.cols > S.target) {
+  if (S.cols > S.target && host_loops()) {  // bursts of 8 iterations, host checks the widths
+    int done_iters = 0;
+    while (true) {
+      for (int k = 0; k < 8; ++k) launch_carve_iteration(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st);
+      done_iters += 8;
+      launch_word_copy(h_runs, S.runs_d.p, sizeof(CarveRun) * nruns, st);
+      SCPL_CUDA(cudaStreamSynchronize(st));
+      bool all = true;
+      for (int r = 0; r < nruns; ++r) all &= h_runs[r].width <= h_runs[r].target;
+      if (all || done_iters > S.cols) break;
+    }
+  } else if (S.cols > S.target) {
     S.loop = build_carve_loop(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1,
                               iters_d);
     SCPL_CUDA(cudaGraphLaunch(S.loop, st));
@@ -640,6 +663,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     scan.h_n = reinterpret_cast<int*>(pin_take(sizeof(int) * nchunk));
     scan.h_runs = reinterpret_cast<int*>(pin_take(sizeof(int) * 2 * (size_t)T));
     scan.h_state = reinterpret_cast<ScanState*>(pin_take(sizeof(ScanState)));
+    scan.h_L = reinterpret_cast<int*>(pin_take(sizeof(int)));
     scan_start(ctx, scan, codes.as<uint16_t>(), T, h, w, P, st);
   }
   std::list<Group> groups;

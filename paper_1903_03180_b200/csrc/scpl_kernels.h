@@ -51,6 +51,8 @@ struct ScanState {
 cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec);
 void launch_scan_reset(ScanState* S, const ScanState& init, cudaStream_t st);
 void launch_scan_avail(ScanState* S, int avail, cudaStream_t st);
+void run_scan_host(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec, int* h_L,
+                   cudaStream_t st);
 void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
                     int transposed, double* out, cudaStream_t st, int pitch = 0);
 

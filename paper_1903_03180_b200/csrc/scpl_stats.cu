@@ -13,6 +13,7 @@
 // candidates.  A second kernel folds the leaf sums with the same tree (one CTA per
 // candidate).  The per-pixel S,Q after the chunk are checkpointed so the next chunk of
 // the same run resumes without re-reading earlier frames.
+#include <cstddef>
 #include <vector>
 
 #include "scpl_common.cuh"
@@ -367,7 +368,7 @@ __device__ void scan_plan(ScanState* S) {
 }
 
 // One thread per candidate folds its root; thread 0 then decides and plans the next window.
-__global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, int decide) {
+__global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, int decide, int in_graph) {
   __shared__ double asde[64];
   const int L = S->L;
   if (decide && L > 0) {
@@ -398,7 +399,7 @@ __global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, 
     S->steps++;
   }
   scan_plan(S);
-  cudaGraphSetConditional(loop, S->L > 0 ? 1u : 0u);
+  if (in_graph) cudaGraphSetConditional(loop, S->L > 0 ? 1u : 0u);
 }
 
 __global__ void scan_reset_kernel(ScanState* S, ScanState init) { *S = init; }
@@ -416,7 +417,7 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
   SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   // head: plan
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 0);
+  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 0, 1);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   SCPL_CUDA(cudaStreamEndCapture(cs, &g));
   cudaGraphNode_t head;
@@ -436,7 +437,7 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, cs>>>(nullptr, nleaves, vnodes, nullptr, S);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
-  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 1);
+  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 1, 1);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
   cudaGraphExec_t ex;
@@ -444,6 +445,27 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
   cudaGraphDestroy(g);
   cudaStreamDestroy(cs);
   return ex;
+}
+
+// Host-driven equivalent of one scan graph launch (SCPL_HOST_LOOPS: profiling, where the
+// conditional graph would hide the kernels from the profiler): the host reads L back.
+void run_scan_host(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec, int* h_L,
+                   cudaStream_t st) {
+  scan_step_kernel<<<1, 64, 0, st>>>(S, 0, 0, 0);
+  SCPL_CHECK_LAUNCH();
+  stats_smem_attr();
+  while (true) {
+    SCPL_CUDA(cudaMemcpyAsync(h_L, reinterpret_cast<uint8_t*>(S) + offsetof(ScanState, L), sizeof(int),
+                              cudaMemcpyDeviceToHost, st));
+    SCPL_CUDA(cudaStreamSynchronize(st));
+    if (*h_L <= 0) break;
+    window_stats_scan_kernel<<<cdiv((long)nleaves * 8, 256), 256, kStatSmem, st>>>(S, leaves, nleaves);
+    SCPL_CHECK_LAUNCH();
+    fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, st>>>(nullptr, nleaves, vnodes, nullptr, S);
+    SCPL_CHECK_LAUNCH();
+    scan_step_kernel<<<1, 64, 0, st>>>(S, 0, 1, 0);
+    SCPL_CHECK_LAUNCH();
+  }
 }
 
 void launch_scan_reset(ScanState* S, const ScanState& init, cudaStream_t st) {

@@ -282,6 +282,22 @@ def test_host_buffers_unpinned_and_odd_chunks(P):
     assert all(np.array_equal(a[t].numpy(), r.frames[t]) for t in range(len(clip)))
 
 
+def test_host_driven_loops_match(P, monkeypatch):
+    """SCPL_HOST_LOOPS (profiling mode: scan and carve loops driven from the host instead of
+    conditional graphs) gives the same runs, passes and frames as the graph loops."""
+    from paper_1903_03180_b200.synth import config_clip
+    import torch
+    path = _config_golden("C4_clip0")[0]
+    g = json.load(open(path))
+    clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
+    monkeypatch.setenv("SCPL_HOST_LOOPS", "1")
+    out, m = P.retarget_video_tensor(torch.from_numpy(clip).cuda(),
+                                     P.RetargetConfig(target_width=tw, target_height=th, mode="buffered"))
+    assert [list(r) for r in m.runs] == g["runs"] and m.dp_passes == g["dp_passes"]
+    host_out = out.cpu().numpy()
+    assert all(sha(host_out[i]) == g["frames_sha"][i] for i in range(host_out.shape[0]))
+
+
 @pytest.mark.parametrize("group_min", ["1", "3", "1000"])
 @pytest.mark.parametrize("host", [False, True])
 def test_run_grouping_does_not_change_results(P, group_min, host, monkeypatch):
