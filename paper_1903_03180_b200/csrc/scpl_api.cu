@@ -388,7 +388,7 @@ void carve_finish(CarveSet& S) {
     if (getenv("SCPL_PROF"))
       fprintf(stderr,
               "carve prof: iters %d rows %d | dp %lld sel %lld | xwait %lld ringwait %lld rows %lld publish %lld"
-              " [bar1 %lld stores %lld bar2 %lld] store_pw %lld\\n",
+              " [bar1 %lld stores %lld bar2 %lld] store_pw %lld\n",
               R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11]);
     long long tot = c[0] + c[1];
     if (tot > best) {
