@@ -134,6 +134,20 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -360,8 +374,8 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       for (int st = 0; st < S - 1 && st < nstage; ++st) dp_issue_stage<F64>(Rg, plane, rows, st, g.win_lo, ring, bars);
   }
   // Exchange protocol (nb_mode): exchange e alternates between two mbarriers (e & 1); a
-  // CTA announces the bytes of exchange e + 1 once exchange e - 1 has landed (for e = 0,
-  // before the cluster barrier that precedes the pass).
+  // CTA announces the bytes of exchange e + 1 at the end of block e, before its own sends
+  // (for e = 0, before the cluster barrier that precedes the pass).
   const uint32_t halo_bytes = nb_mode ? halo_bytes_for(w, CL, rank, (int)sizeof(T)) : 0u;
   // wait for stage st (issuing the one S-1 ahead first) and return its ring rows
   auto stage_rows = [&](int st) -> const uint8_t* {
@@ -375,6 +389,8 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
     rph ^= 1u << slot;
     return ring + ((size_t)slot * RS * kRingW + (g.win_lo & 15)) * sz;
   };
+  // block-end path words and landing deltas of the owned columns: the lane-contiguous words
+  // are transposed through this warp's staging row so the global stores coalesce
   // block-end path words and landing deltas of the owned columns: the lane-contiguous words
   // are transposed through this warp's staging row so the global stores coalesce
   auto store_pw = [&](int pbi, int nrb) {
@@ -412,10 +428,6 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         mbar_wait(&xbar[e & 1], (e >> 1) & 1);
         __syncwarp();
       }
-      // announce exchange xm + 1 on the barrier exchange xm - 1 just released; a neighbour
-      // can only send it after receiving this CTA's exchange xm, and an early complete_tx
-      // would merely take the phase's tx-count below zero until this arrive
-      if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
     }
     DP_PROF(0, DP_CLOCK() - tx);
     if (active) {
@@ -472,6 +484,15 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       }
       DP_PROF(2, DP_CLOCK() - tx);
       tx = DP_CLOCK();
+    }
+    // announce the next exchange's bytes, then let the block's data go out.  The named
+    // barrier orders the announcement (a) after every local warp's wait on the exchange that
+    // last used this mbarrier -- otherwise a phase that completes at once (no halo bytes, or
+    // bytes already in) could advance the barrier twice past a slow waiter's parity -- and
+    // (b) before any local warp's sends, so a neighbour's complete_tx follows the expect_tx
+    if (nb_mode) {
+      if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
+      asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");
     }
     DP_PROF(4, DP_CLOCK() - tx);
     if (active) {
