@@ -111,8 +111,10 @@ typedef struct {
   int n_runs;
   int* run_start;      /* host, capacity T (nullable) */
   int* run_len;        /* host, capacity T (nullable) */
-  float phase_ms[4];   /* device time of: energy codes, buffer scan, carve, replay */
-  long long carve_cycles[4]; /* SM cycles of the slowest run's carve: dp, select, compact, gradient */
+  float phase_ms[4];   /* device ms: start -> codes done, -> scan done, scan done -> all carved and
+                          replayed (groups overlap the scan), unused */
+  long long carve_cycles[4]; /* slowest run (SCPL_PROF builds fill the cycle counters): dp cycles,
+                                select cycles, its pass count, unused */
   int carve_cluster;   /* CTAs per run cluster used by the carve */
 } scpl_video_result;
 

@@ -393,7 +393,10 @@ void carve_finish(CarveSet& S) {
     long long tot = c[0] + c[1];
     if (tot > best) {
       best = tot;
-      for (int k = 0; k < 4; ++k) S.prof[k] = c[k];
+      S.prof[0] = c[0];
+      S.prof[1] = c[1];
+      S.prof[2] = R.iters;  // passes of that run
+      S.prof[3] = 0;
     }
   }
 }
@@ -860,7 +863,8 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     for (CarveSet& S : G.sets) {
       carve_finish(S);
       for (auto& R : S.runs) dp += R.iters;
-      for (int k = 0; k < 4; ++k) result->carve_cycles[k] = std::max(result->carve_cycles[k], S.prof[k]);
+      if (S.prof[0] + S.prof[1] > result->carve_cycles[0] + result->carve_cycles[1])
+        for (int k = 0; k < 4; ++k) result->carve_cycles[k] = S.prof[k];
       result->carve_cluster = S.cl;
     }
   result->dp_passes = dp;

@@ -127,9 +127,12 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
                   ctypes.byref(res), _lib.stream()))
     runs = [(starts[i], lens[i]) for i in range(res.n_runs)]
     global last_phase_ms
-    last_phase_ms = dict(zip(("codes", "scan", "carve", "replay"), (float(x) for x in res.phase_ms)))
-    last_phase_ms.update({f"carve_{k}_Mcyc": c / 1e6 for k, c in zip(("dp", "select", "compact", "grad"),
-                                                                      res.carve_cycles)})
+    # device time from the call's start: codes done, scan done, every group carved + replayed
+    # (the groups overlap the scan; the last one finishes carve_after_scan ms after it)
+    last_phase_ms = dict(zip(("codes", "scan", "carve_after_scan"), (float(x) for x in res.phase_ms[:3])))
+    # device clock cycles of the slowest run's pass kernels (dp rows / select+trace), summed
+    last_phase_ms.update({f"carve_{k}_Mcyc": c / 1e6 for k, c in zip(("dp", "select"), res.carve_cycles[:2])})
+    last_phase_ms["slowest_run_iters"] = int(res.carve_cycles[2])
     last_phase_ms["carve_cluster"] = res.carve_cluster
     return out, int(res.dp_passes), runs
 
