@@ -383,13 +383,15 @@ void carve_finish(CarveSet& S) {
     if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;
   for (auto& R : S.runs) {
-    long long c[12];
+    long long c[17];
     SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
     if (getenv("SCPL_PROF"))
       fprintf(stderr,
               "carve prof: iters %d rows %d | dp %lld sel %lld | xwait %lld ringwait %lld rows %lld publish %lld"
-              " [bar1 %lld stores %lld bar2 %lld] store_pw %lld\n",
-              R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11]);
+              " [bar1 %lld stores %lld bar2 %lld] store_pw %lld | sel: labels %lld min %lld cand %lld trunc %lld"
+              " trace %lld (x CTAs)\n",
+              R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11], c[12], c[13], c[14],
+              c[15], c[16]);
     long long tot = c[0] + c[1];
     if (tot > best) {
       best = tot;

@@ -58,6 +58,19 @@ constexpr int kMaxWarps = 12;                    // 384 threads: up to 168 regis
 #define DP_CLOCK() 0ll
 #define DP_PROF(i, v) ((void)0)
 #endif
+// select sub-phase timers (thread 0 of each CTA; SCPL_CARVE_PROF builds): slots 12..16
+#ifdef SCPL_CARVE_PROF
+#define SEL_PROF(k)                                   \
+  do {                                                \
+    if (tid == 0 && R.prof) {                         \
+      const long long t_ = clock64();                 \
+      atomicAdd((unsigned long long*)&R.prof[12 + (k)], (unsigned long long)(t_ - ts)); \
+      ts = t_;                                        \
+    }                                                 \
+  } while (0)
+#else
+#define SEL_PROF(k) ((void)0)
+#endif
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -85,6 +98,16 @@ __device__ __forceinline__ void st_async_remote(const double* local_dst, double 
                    map_rank(local_dst, rank)),
                "l"(__double_as_longlong(v)), "r"(map_rank(local_bar, rank))
                : "memory");
+}
+__device__ __forceinline__ uint32_t lds32_u(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_s8(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
 }
 __device__ __forceinline__ uint32_t map_rank_pure(const void* p, uint32_t rank) {
   uint32_t out;
@@ -761,22 +784,37 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
       dsrc = S.dtab;
     }
     __syncthreads();
+    [[maybe_unused]] long long ts = DP_CLOCK();
     // labels (batching.py:39-46): chain the block landing deltas, 8 columns per thread in flight
+    // (shared-memory table: 32-bit shared addresses, no generic-address resolution per step)
     for (int jb = tid; jb < w; jb += 8 * blockDim.x) {
       int c[8];
+      bool ok[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = jb + u * (int)blockDim.x;
-      for (int bl = nblk - 1; bl >= 0; --bl) {
-        const int8_t* drow = dsrc + (size_t)bl * pitch;
+      for (int u = 0; u < 8; ++u) {
+        c[u] = jb + u * (int)blockDim.x;
+        ok[u] = c[u] < w;
+        if (!ok[u]) c[u] = 0;
+      }
+      if (stage_dtab) {
+        uint32_t row = smem_u32(S.dtab) + (uint32_t)(nblk - 1) * (uint32_t)pitch;
+        for (int bl = nblk - 1; bl >= 0; --bl, row -= (uint32_t)pitch) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (jb + u * (int)blockDim.x < w) c[u] += drow[c[u]];
+          for (int u = 0; u < 8; ++u) c[u] += lds_s8(row + (uint32_t)c[u]);
+        }
+      } else {
+        for (int bl = nblk - 1; bl >= 0; --bl) {
+          const int8_t* drow = dsrc + (size_t)bl * pitch;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) c[u] += drow[c[u]];
+        }
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (jb + u * (int)blockDim.x < w) S.lab[jb + u * blockDim.x] = c[u];
+        if (ok[u]) S.lab[jb + u * blockDim.x] = c[u];
     }
     __syncthreads();
+    SEL_PROF(0);
     int b;
     if (R.kmax == 1) {  // raw mode: min_seam, leftmost global minimum (seams.py:84-89)
       for (int j = tid; j < w; j += blockDim.x)
@@ -796,6 +834,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
         if ((unsigned long long)__double_as_longlong(S.lce[j]) == S.segmin[S.lab[j]])
           atomicMin(&S.segarg[S.lab[j]], j);
       __syncthreads();
+      SEL_PROF(1);
       const int perq0 = (w + blockDim.x - 1) / blockDim.x;
       int cnt = 0;
       for (int u = 0; u < perq0; ++u) {
@@ -809,6 +848,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
         if (l < w && S.segarg[l] != INT_MAX) S.cand[pos++] = S.segarg[l];
       }
       __syncthreads();
+      SEL_PROF(2);
       const int k = w - R.target;
       if (P <= k) {
         for (int q = tid; q < P; q += blockDim.x) S.sel[q] = S.cand[q];
@@ -836,24 +876,44 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
       }
     }
     __syncthreads();
+    SEL_PROF(3);
     // trace (seams.py:68-81): walk each seam's block-end columns through the staged deltas,
     // keeping those of this CTA's blocks (bl % CL == rank); then decode (seam, block) pairs
     // in parallel into the removed-column log
     int16_t* log = R.rem;  // rows x rem_cap, this batch's columns at [removed, removed + b)
     for (int s = tid; s < b; s += blockDim.x) {
       int c = S.sel[s];
+      int next_mine = (nblk - 1) - ((nblk - 1 - (int)rank) % CL + CL) % CL;  // highest block with bl % CL == rank
       for (int bl = nblk - 1; bl >= 0; --bl) {
-        if (bl % CL == (int)rank) R.cend[(long)bl * pitch + s] = (int16_t)c;
-        c += dsrc[(size_t)bl * pitch + c];
+        if (bl == next_mine) {
+          R.cend[(long)bl * pitch + s] = (int16_t)c;
+          next_mine -= CL;
+        }
+        c += stage_dtab ? lds_s8(smem_u32(S.dtab) + (uint32_t)bl * (uint32_t)pitch + (uint32_t)c)
+                        : (int)dsrc[(size_t)bl * pitch + c];
       }
       if (rank == 0) log[removed + s] = (int16_t)c;  // row 0 (== the seam's label)
     }
     __syncthreads();
     const int myblk = nblk > (int)rank ? (nblk - 1 - (int)rank) / CL + 1 : 0;
+    // int passes: this CTA's blocks of choice words move into shared memory (the landing-
+    // delta table is no longer needed) with bulk copies, so the walk below reads smem
+    const bool stage_cw = !fp64 && stage_dtab && CL >= 4 && b > 0 && myblk > 0;
+    if (stage_cw) {
+      if (tid == 0) {
+        fence_proxy_async_global();
+        mbar_arrive_tx(&s_dbar, (uint32_t)(myblk * pitch * 4));
+        for (int m = 0; m < myblk; ++m)
+          bulk_g2s(S.dtab + (size_t)m * pitch * 4, R.pw + (long)((int)rank + m * CL) * pitch, (uint32_t)pitch * 4u,
+                   &s_dbar);
+      }
+      mbar_wait(&s_dbar, 1);
+    }
     for (int q = tid; q < b * myblk; q += blockDim.x) {
       int s = q / myblk, bl = (int)rank + (q - s * myblk) * CL;
       int c = R.cend[(long)bl * pitch + s];
       const uint32_t* pwb = R.pw + (long)bl * pitch;
+      const uint32_t cws = smem_u32(S.dtab) + (uint32_t)((q - s * myblk) * pitch) * 4u;
       int i_start = 1 + bl * kBlockRows;
       int i_end = min(i_start + kBlockRows, rows) - 1;
       if (fp64) {  // path word of the seam's end column
@@ -863,13 +923,19 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
           c += (int)(word & 3u) - 1;
           word >>= 2;
         }
-      } else {  // choice words of the visited columns
+      } else if (stage_cw) {  // choice words of the visited columns (shared memory)
+        for (int i = i_end, q = 0; i >= i_start; --i, ++q) {
+          log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
+          c += (int)((lds32_u(cws + 4u * (uint32_t)c) >> (2 * q)) & 3u) - 1;
+        }
+      } else {
         for (int i = i_end, q = 0; i >= i_start; --i, ++q) {
           log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
           c += (int)((pwb[c] >> (2 * q)) & 3u) - 1;
         }
       }
     }
+    SEL_PROF(4);
     if (rank == 0 && R.cols != nullptr)
       for (int s = tid; s < b; s += blockDim.x) {
         R.cols[removed + s] = (int16_t)S.sel[s];
@@ -1220,7 +1286,7 @@ size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
   size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * (dp_ring_bytes<true>() + 8 * kWin);
   size_t sel = (size_t)pitch * (8 + 8 + 4 * 4) + 16;
-  if (stage) sel += (size_t)nblk * pitch;
+  if (stage) sel += (size_t)(nblk + 3) * pitch;  // delta table, later this CTA's choice-word rows
   const size_t RB = (((size_t)pitch + 15) & ~(size_t)15) + 16;
   size_t comp = (size_t)warps * (4 * RB + kWarpScratch);
   size_t m = dp > sel ? dp : sel;
