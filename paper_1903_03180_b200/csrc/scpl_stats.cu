@@ -359,6 +359,10 @@ __device__ void scan_plan(ScanState* S) {
       continue;
     }
     int L = min(S->spec, min(remaining, S->max_len - S->n_acc));
+    // a run's first window stops where the previous run broke (runs tend to repeat their
+    // length; an evaluated candidate past the breach is wasted work); the ASDE of a length
+    // does not depend on how the lengths are split into windows
+    if (S->n_acc == 1 && S->nruns > 0) L = min(L, max(2, S->runs[2 * S->nruns - 1]));
     L = min(L, S->avail - (S->s + S->n_acc));
     if (L <= 0) break;  // wait for more frames
     S->L = L;
