@@ -71,11 +71,18 @@ void build_pairwise_plan(long N, std::vector<int2>& leaves, std::vector<PwVnode>
 // stream into an 8-stage shared-memory ring by 1-D TMA bulk copies issued up front, so the
 // fp64 work never waits on a global load; lanes then read their strided elements from
 // shared memory.  Rows of N not divisible by 8 fall back to cooperative plain copies.
-constexpr int kMaxPerLane = 16;  // 128 / 8
+constexpr int kLeafLanes = 16;     // lanes per leaf: accumulator j = lanes j (first half) and j + 8
+constexpr int kHalfMax = 8;        // elements per lane and accumulator half (a leaf has <= 16 per accumulator)
 constexpr int kStatStages = 8;
-constexpr int kStatStageBytes = 32 * 128 * 2;
+constexpr int kStatStageBytes = (256 / kLeafLanes) * 128 * 2;  // one CTA's pixels of one frame
 constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatStages;
 
+// numpy's leaf sum (pairwise_sum, n <= 128): r[j] = a[j] + a[j+8] + ... (sequential), then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail elements in order.  Here lane
+// (h, j) of a leaf's 16 lanes holds accumulator j's elements m in [h ? m0 : 0, h ? nmain : m0)
+// (m0 = ceil(nmain/2)): the first half sums its part, hands the partial to the second half,
+// which continues the same sequential sum -- the bracketing is numpy's exactly, with half the
+// registers per lane (so twice the resident warps hide the fp64 latency).
 __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ codes, long N,
                                                   const int2* __restrict__ leaves, int nleaves, int s, int n_acc,
                                                   int L, int first_pure, int init, double wm, double wg,
@@ -88,8 +95,9 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
     A[k] = __dmul_rn(wm, (double)k);
     B[k] = __dmul_rn(wg, (double)k);
   }
-  const int first = blockIdx.x * (blockDim.x >> 3);
-  const int last = min(nleaves, first + (int)(blockDim.x >> 3)) - 1;
+  const int leaves_per_cta = blockDim.x / kLeafLanes;
+  const int first = blockIdx.x * leaves_per_cta;
+  const int last = min(nleaves, first + leaves_per_cta) - 1;
   const long p_lo = leaves[first].x;
   const int2 lf_last = leaves[last];
   const int npx = (int)(lf_last.x + lf_last.y - p_lo);
@@ -136,39 +144,42 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
   };
 
   const int lane = threadIdx.x & 31;
-  const int sub = lane & 7;
-  const int leaf = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int sub = lane & 15, j = sub & 7, h = sub >> 3;
+  const int leaf = (blockIdx.x * blockDim.x + threadIdx.x) / kLeafLanes;
   const bool active = leaf < nleaves;
   int2 lf = active ? leaves[leaf] : make_int2((int)p_lo, 8);
   const int len = lf.y;
-  const int nmain = len >> 3;    // elements per lane in the 8-accumulator region
-  const int ntail = len & 7;     // sequential tail, element i = 8*nmain + k held by lane k
+  const int nmain = len >> 3;     // elements per accumulator
+  const int ntail = len & 7;      // sequential tail: element 8*nmain + t held by lane (0, t)
+  const int m0 = (nmain + 1) >> 1;
+  const int mb = h ? m0 : 0, cnt = h ? nmain - m0 : m0;  // this lane's elements
   const long base = lf.x;
   const int lb = (int)(base - p_lo);  // leaf start within the CTA range
+  const bool has_tail = active && h == 0 && j < ntail;
+  auto off = [&](int k) { return k < kHalfMax ? lb + 8 * (mb + k) + j : lb + 8 * nmain + j; };
+  auto valid = [&](int k) { return k < kHalfMax ? (active && k < cnt) : has_tail; };
 
-  double S[kMaxPerLane + 1], Q[kMaxPerLane + 1];
+  double S[kHalfMax + 1], Q[kHalfMax + 1];
   int ci = 0;  // next stage
   if (init) {
     const uint16_t* st = acquire(ci);
 #pragma unroll
-    for (int k = 0; k <= kMaxPerLane; ++k) {
-      const int o = (k < kMaxPerLane) ? lb + sub + 8 * k : lb + 8 * nmain + sub;
-      const bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
-      const double e = valid ? energy_of(st[o], first_pure && s == 0, A, B) : 0.0;
+    for (int k = 0; k <= kHalfMax; ++k) {
+      const double e = valid(k) ? energy_of(st[off(k)], first_pure && s == 0, A, B) : 0.0;
       S[k] = e;
       Q[k] = __dmul_rn(e, e);
     }
     release(ci++);
   } else {
 #pragma unroll
-    for (int k = 0; k <= kMaxPerLane; ++k) {
-      const long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
-      const bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
-      S[k] = valid ? ckS[p] : 0.0;
-      Q[k] = valid ? ckQ[p] : 0.0;
+    for (int k = 0; k <= kHalfMax; ++k) {
+      const long p = p_lo + off(k);
+      S[k] = valid(k) ? ckS[p] : 0.0;
+      Q[k] = valid(k) ? ckQ[p] : 0.0;
     }
   }
 
+  const int g0 = lane & ~15;  // first lane of this leaf's group
   for (int c = 0; c < L; ++c, ++ci) {
     const int t = s + n_acc + c;
     const int n = n_acc + c + 1;
@@ -176,51 +187,56 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
     const double rn = __ddiv_rn(1.0, dn);
     const uint16_t* ct = acquire(ci);
     const bool pure = first_pure && t == 0;
-    double acc = 0.0, tail = 0.0;
+    double sd[kHalfMax + 1];
 #pragma unroll
-    for (int k = 0; k <= kMaxPerLane; ++k) {
-      const int o = (k < kMaxPerLane) ? lb + sub + 8 * k : lb + 8 * nmain + sub;
-      const bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
-      if (valid) {
-        double e = energy_of(ct[o], pure, A, B);
+    for (int k = 0; k <= kHalfMax; ++k) {
+      sd[k] = 0.0;
+      if (valid(k)) {
+        const double e = energy_of(ct[off(k)], pure, A, B);
         S[k] = __dadd_rn(S[k], e);
         Q[k] = __dadd_rn(Q[k], __dmul_rn(e, e));
-        double m = div_small(S[k], dn, rn);
-        double var = __dsub_rn(div_small(Q[k], dn, rn), __dmul_rn(m, m));
-        double sd = __dsqrt_rn(var >= 0.0 ? var : 0.0);
-        if (k < kMaxPerLane)
-          acc = (k == 0) ? sd : __dadd_rn(acc, sd);
-        else
-          tail = sd;
+        const double m = div_small(S[k], dn, rn);
+        const double var = __dsub_rn(div_small(Q[k], dn, rn), __dmul_rn(m, m));
+        sd[k] = __dsqrt_rn(var >= 0.0 ? var : 0.0);
       }
     }
     release(ci);
-    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)): IEEE addition commutes, so xor-shuffles give
-    // exactly numpy's bracketing.
+    // first half: r_j's leading part; second half continues the sequential sum
+    double acc = sd[0];
+#pragma unroll
+    for (int k = 1; k < kHalfMax; ++k)
+      if (h == 0 && k < cnt) acc = __dadd_rn(acc, sd[k]);
+    const double part = __shfl_sync(0xffffffffu, acc, g0 + j);
+    if (h == 1) {
+      acc = part;
+#pragma unroll
+      for (int k = 0; k < kHalfMax; ++k)
+        if (k < cnt) acc = __dadd_rn(acc, sd[k]);
+    }
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in the second half (xor within lanes 8..15)
     double x = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
     x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 2));
     x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 4));
-    const int g0 = lane & ~7;
+    if (nmain == 0) x = 0.0;  // n < 8: numpy's plain loop from 0
     for (int k = 0; k < 7; ++k) {  // tail elements in order (uniform trip count for shuffles)
-      double tv = __shfl_sync(0xffffffffu, tail, g0 + k);
+      const double tv = __shfl_sync(0xffffffffu, sd[kHalfMax], g0 + k);
       if (k < ntail) x = __dadd_rn(x, tv);
     }
-    if (active && sub == 0) leafsum[(size_t)c * nleaves + leaf] = x;
+    if (active && sub == 8) leafsum[(size_t)c * nleaves + leaf] = x;
   }
 
   // checkpoint S,Q after n_acc + L frames
 #pragma unroll
-  for (int k = 0; k <= kMaxPerLane; ++k) {
-    long p = (k < kMaxPerLane) ? base + sub + 8 * k : base + 8 * nmain + sub;
-    bool valid = active && ((k < kMaxPerLane) ? (k < nmain) : (sub < ntail));
-    if (valid) {
+  for (int k = 0; k <= kHalfMax; ++k) {
+    if (valid(k)) {
+      const long p = p_lo + off(k);
       ckS[p] = S[k];
       ckQ[p] = Q[k];
     }
   }
 }
 
-__global__ void __launch_bounds__(256) window_stats_kernel(const uint16_t* __restrict__ codes, long N,
+__global__ void __launch_bounds__(256, 3) window_stats_kernel(const uint16_t* __restrict__ codes, long N,
                                                            const int2* __restrict__ leaves, int nleaves,
                                                            int s, int n_acc, int L, int first_pure, int init,
                                                            double wm, double wg, double* __restrict__ ckS,
@@ -230,7 +246,7 @@ __global__ void __launch_bounds__(256) window_stats_kernel(const uint16_t* __res
 }
 
 // Scan variant: the window comes from the device-side scan state (no host round trip).
-__global__ void __launch_bounds__(256) window_stats_scan_kernel(const ScanState* __restrict__ S,
+__global__ void __launch_bounds__(256, 3) window_stats_scan_kernel(const ScanState* __restrict__ S,
                                                                 const int2* __restrict__ leaves, int nleaves) {
   const int L = S->L;
   if (L <= 0) return;
@@ -324,7 +340,7 @@ void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int 
                          double* leafsum, const PwVnode* vnodes, double* partial, double* asde_out,
                          cudaStream_t st) {
   int threads = 256;
-  int blocks = cdiv((long)nleaves * 8, threads);
+  int blocks = cdiv((long)nleaves * kLeafLanes, threads);
   stats_smem_attr();
   window_stats_kernel<<<blocks, threads, kStatSmem, st>>>(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init,
                                                           wm, wg, ckS, ckQ, leafsum);
@@ -437,7 +453,7 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   stats_smem_attr();
-  window_stats_scan_kernel<<<cdiv((long)nleaves * 8, 256), 256, kStatSmem, cs>>>(S, leaves, nleaves);
+  window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem, cs>>>(S, leaves, nleaves);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, cs>>>(nullptr, nleaves, vnodes, nullptr, S);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
@@ -463,7 +479,7 @@ void run_scan_host(ScanState* S, const int2* leaves, int nleaves, const PwVnode*
                               cudaMemcpyDeviceToHost, st));
     SCPL_CUDA(cudaStreamSynchronize(st));
     if (*h_L <= 0) break;
-    window_stats_scan_kernel<<<cdiv((long)nleaves * 8, 256), 256, kStatSmem, st>>>(S, leaves, nleaves);
+    window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem, st>>>(S, leaves, nleaves);
     SCPL_CHECK_LAUNCH();
     fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, st>>>(nullptr, nleaves, vnodes, nullptr, S);
     SCPL_CHECK_LAUNCH();
