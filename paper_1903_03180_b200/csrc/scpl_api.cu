@@ -599,18 +599,24 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   const size_t fbytes0 = (size_t)h * w * C;
   const bool host_in = frames_host != nullptr, host_out = out_host != nullptr;
   const bool buffered = P.mode == 2;
-  // the scan is the critical path (it releases the runs): codes and scan get the highest
-  // stream priority, the carve groups the lowest
+  // Priorities: the scan feeds everything (it releases the runs), so codes and scan get the
+  // highest; carve groups get higher priorities the later they start -- the last group is
+  // the critical path, the early ones have slack, and the carve passes compete for whole SMs.
+  // Levels: prio_hi (scan) .. prio_lo; carve groups use prio_hi+1 .. prio_lo (or all if the
+  // range is tiny), kStreamsPerLevel streams each.
   int prio_lo = 0, prio_hi = 0;
   SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_d2h})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
   for (cudaStream_t* x : {&ctx->s_codes, &ctx->s_scan})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithPriority(x, cudaStreamNonBlocking, prio_hi));
-  const int kCarveStreams = 16;
-  while ((int)ctx->s_carve.size() < kCarveStreams) {
+  const int carve_hi = prio_lo - prio_hi >= 2 ? prio_hi + 1 : prio_hi;
+  const int nlevels = prio_lo - carve_hi + 1;  // levels carve_hi .. prio_lo
+  const int kStreamsPerLevel = 4;
+  while ((int)ctx->s_carve.size() < nlevels * kStreamsPerLevel) {
+    const int level = (int)ctx->s_carve.size() / kStreamsPerLevel;  // 0 = lowest priority
     cudaStream_t x;
-    SCPL_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_lo));
+    SCPL_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_lo - level));
     ctx->s_carve.push_back(x);
   }
   std::vector<int> phases;  // 0 width, 1 height (pipeline.py:192-193, 246-277)
@@ -742,7 +748,11 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   auto dispatch = [&](int r0, int r1, cudaEvent_t ready) {
     if (r1 <= r0) return;
     Group& G = groups.emplace_back();
-    G.st = ctx->s_carve[next_stream++ % kCarveStreams];
+    {  // later groups (by first frame) on higher-priority streams
+      const int ta0 = runs[r0].first;
+      const int level = std::min(nlevels - 1, (int)((long)ta0 * nlevels / std::max(T, 1)));
+      G.st = ctx->s_carve[level * kStreamsPerLevel + (next_stream++ % kStreamsPerLevel)];
+    }
     cudaStream_t gs = G.st;
     SCPL_CUDA(cudaStreamWaitEvent(gs, ev_alloc, 0));
     SCPL_CUDA(cudaStreamWaitEvent(gs, ready, 0));
