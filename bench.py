@@ -133,6 +133,28 @@ def dist_setup():
     return world, rank, local
 
 
+def reduce_max(x: float, world: int, device: str) -> float:
+    """Max of a per-rank time over the job (the slowest rank bounds the step)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def rank_workload(name: str, rank: int, frames=None):
+    """Each rank retargets its own clip of the config's recipe (seed = rank): clips are
+    independent, so the data path has no collective (weak scaling)."""
+    if rank == 0 or name == "C4":
+        return config_clip(name, frames=frames, clip=rank)
+    from dataclasses import replace
+    from paper_1903_03180_b200.synth import generate_clip
+    spec, tw, th = CONFIGS[name]
+    return generate_clip(replace(spec, seed=spec.seed + 1000 * rank), frames=frames), tw, th
+
+
 # ------------------------------------------------------------------ CPU legs (oracle port)
 def _oracle_window(args):
     """Retarget one bounded window of the config clip with the oracle port (worker process)."""
@@ -211,7 +233,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     name = a.config
-    clip, tw, th = config_clip(name, frames=a.frames, clip=rank)
+    clip, tw, th = rank_workload(name, rank, a.frames)
     T, H, W, C = clip.shape
     tw = tw or W
     th = th or H
@@ -226,11 +248,7 @@ def main():
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(x, world, "cuda")
 
     for _ in range(a.warmup):
         out, m = P.retarget_video_tensor(dev, cfg)
