@@ -96,15 +96,16 @@ def _frame(spec: ClipSpec, t: int, rects, flick, out: np.ndarray) -> None:
 
 
 def generate_clip(spec: ClipSpec, frames: int | None = None, out: np.ndarray | None = None,
-                  threads: int | None = None) -> np.ndarray:
-    """(T, H, W, 3) uint8 clip; ``frames`` truncates to the first T frames."""
-    t_total = spec.frames if frames is None else min(frames, spec.frames)
+                  threads: int | None = None, start: int = 0) -> np.ndarray:
+    """(T, H, W, 3) uint8 clip; ``frames`` truncates to T frames, from frame ``start`` (every
+    frame is a function of its index alone, so any window is generated directly)."""
+    t_total = (spec.frames - start) if frames is None else min(frames, spec.frames - start)
     if out is None:
         out = np.empty((t_total, spec.height, spec.width, 3), dtype=np.uint8)
     rects, flick = _rects(spec)
     threads = threads or min(16, os.cpu_count() or 1)
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(lambda t: _frame(spec, t, rects, flick, out[t]), range(t_total)))
+        list(ex.map(lambda t: _frame(spec, start + t, rects, flick, out[t]), range(t_total)))
     return out
 
 
