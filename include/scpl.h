@@ -104,6 +104,7 @@ typedef struct {
   double w_motion, w_grad;
   const double* phi;  /* host, max_len+1 entries: threshold(n, policy) as the reference computes it */
   int spec_len;       /* window candidates evaluated per stats launch (0 = default) */
+  int reaverage;      /* RetargetConfig.reaverage_energy (pipeline.py:269-270, 280-296) */
 } scpl_video_params;
 
 typedef struct {

@@ -380,10 +380,29 @@ def _transpose(a):
     return np.ascontiguousarray(np.swapaxes(np.asarray(a), 0, 1))
 
 
-def _carve_frames(frames, tw, th, first_energy, height_first, kmax, literal_replay=False):
+def _carve_run_reaverage(frames, target_width, energy):
+    """pipeline.py:280-296: batch carve a whole run, re-averaging the gradient energy over
+    every carved frame (np.stack(...).mean(0)) before each pass after the first."""
+    cur = [np.asarray(f) for f in frames]
+    batches = []
+    emap = energy
+    while cur[0].shape[1] > target_width:
+        if emap is None:
+            emap = np.stack([default_energy(f) for f in cur]).mean(axis=0)
+        ce, back = cumulative_energy(emap)
+        labels = label_parents(back)
+        b = select_batch(ce, back, labels, k=cur[0].shape[1] - target_width)
+        cur = [remove_batch(f, b) for f in cur]
+        batches.append(b)
+        emap = None
+    return cur, batches
+
+
+def _carve_frames(frames, tw, th, first_energy, height_first, kmax, literal_replay=False, reaverage=False):
     """_process_run / _retarget_single (pipeline.py:196-226, 246-277): width then height,
     the first carved phase on `first_energy`, later phases on gradient energy; the carve
-    runs on frames[0] and is replayed on every frame of the group."""
+    runs on frames[0] and is replayed on every frame of the group (reaverage: on the mean
+    gradient of all the group's carved frames, pipeline.py:269-270)."""
     cur = list(frames)
     passes = 0
     emap = first_energy
@@ -395,6 +414,13 @@ def _carve_frames(frames, tw, th, first_energy, height_first, kmax, literal_repl
             continue
         work = [_transpose(f) for f in cur] if axis == "height" else cur
         pe = (_transpose(emap) if emap is not None else None) if axis == "height" else emap
+        if reaverage:
+            work, batches = _carve_run_reaverage(work, target, pe)
+            passes += len(batches)
+            per_phase.append(batches)
+            cur = [_transpose(f) for f in work] if axis == "height" else work
+            emap = None
+            continue
         _, batches = batch_carve(work[0], target, energy=pe, kmax=kmax)
         if literal_replay:   # the reference's batch-by-batch remove_batch loop (timing fidelity)
             work = replay_batches(work, batches)
@@ -420,8 +446,9 @@ def _resolve(size, target, axis):
 
 def retarget_video(frames, target_width=None, target_height=None, mode="buffered",
                    policy: BufferPolicy = BufferPolicy(), w_motion=0.6, w_grad=0.4,
-                   height_first=False, keep_batches=False, literal_replay=False) -> Result:
-    """pipeline.py:92-137 (buffered, scpl, raw branches; reaverage_energy=False)."""
+                   height_first=False, keep_batches=False, literal_replay=False,
+                   reaverage_energy=False) -> Result:
+    """pipeline.py:92-137 (buffered, scpl, raw branches; reaverage_energy for buffered/scpl)."""
     t0 = time.perf_counter()
     frames = [np.asarray(f) for f in frames]
     if not frames:
@@ -454,7 +481,7 @@ def retarget_video(frames, target_width=None, target_height=None, mode="buffered
             if mode == "scpl":
                 u = emaps[s]
             c, p, b = _carve_frames(frames[s:s + n], tw, th, u, height_first, kmax=None,
-                                    literal_replay=literal_replay)
+                                    literal_replay=literal_replay, reaverage=reaverage_energy)
             out += c
             passes += p
             all_batches.append(b if keep_batches else None)

@@ -25,7 +25,7 @@ class VideoParams(ctypes.Structure):
         ("target_width", ctypes.c_int), ("target_height", ctypes.c_int), ("mode", ctypes.c_int),
         ("height_first", ctypes.c_int), ("max_len", ctypes.c_int),
         ("w_motion", ctypes.c_double), ("w_grad", ctypes.c_double),
-        ("phi", ctypes.POINTER(ctypes.c_double)), ("spec_len", ctypes.c_int),
+        ("phi", ctypes.POINTER(ctypes.c_double)), ("spec_len", ctypes.c_int), ("reaverage", ctypes.c_int),
     ]
 
 

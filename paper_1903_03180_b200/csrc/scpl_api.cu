@@ -260,6 +260,9 @@ struct CarveSet {
   std::vector<CarveRun> runs;
   int rows = 0, cols = 0, pitch = 0, target = 0, cl = 1;
   size_t planes_bytes = 0;  // luma + gradient planes of every run, at the start of mem
+  int max_fr = 1;           // most frames carved together by one run (reaverage)
+  bool reaverage = false;
+  bool has_uniform = false;  // U holds a uniform map for the first pass (else the mean gradient)
   long long prof[4] = {0, 0, 0, 0};
   cudaGraphExec_t loop = nullptr;  // device-side iteration loop (alive until the work completes)
   CarveRun* h_runs = nullptr;      // pinned: run state after the carve (read once the stream is done)
@@ -272,8 +275,9 @@ struct CarveSet {
   }
 };
 
+// nfr (nullable): frames carved together per run (reaverage_energy), else one each
 void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
-                 int cl, cudaStream_t st) {
+                 int cl, cudaStream_t st, const int* nfr = nullptr, bool reaverage = false) {
   SCPL_ARG(cols <= 4096, "frames wider than 4096 columns (in the carve orientation) are not supported");
   const int pitch = (cols + 15) & ~15;
   const int nblk = std::max(1, (rows - 1 + kBlockRows - 1) / kBlockRows);
@@ -283,7 +287,16 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   // every run's luma and gradient plane first (compacted in place; one contiguous range for
   // the L2 persistence window), then each run's tables
   const size_t plane_al = align256(plane);
-  const size_t planes_bytes = (size_t)nruns * 2 * plane_al;
+  long total_fr = 0;
+  int max_fr = 1;
+  for (int r = 0; r < nruns; ++r) {
+    const int n = nfr ? std::max(1, nfr[r]) : 1;
+    total_fr += n;
+    max_fr = std::max(max_fr, n);
+  }
+  const size_t planes_bytes = (size_t)total_fr * 2 * plane_al;
+  const bool uniform_given = with_U;
+  if (reaverage) with_U = true;  // U = the mean gradient, recomputed every pass
   size_t per = align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
                align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
                align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(256) +
@@ -296,8 +309,12 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   S.pitch = pitch;
   S.target = target;
   S.cl = cl;
+  S.max_fr = max_fr;
+  S.reaverage = reaverage;
+  S.has_uniform = uniform_given;
   S.runs.assign(nruns, CarveRun{});
   uint8_t* base = S.mem.as<uint8_t>();
+  size_t plane_off = 0;
   const int stage = carve_stage_dtab(rows, pitch, cl) ? 1 : 0;
   for (int r = 0; r < nruns; ++r) {
     uint8_t* p = base + planes_bytes + per * r;
@@ -313,8 +330,12 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.target = target;
     R.kmax = kmax;
     R.stage_dtab = stage;
-    R.luma[0] = R.luma[1] = base + (size_t)(2 * r) * plane_al;
-    R.grad[0] = R.grad[1] = base + (size_t)(2 * r + 1) * plane_al;
+    R.nfr = nfr ? std::max(1, nfr[r]) : 1;
+    R.reaverage = reaverage ? 1 : 0;
+    R.fstride = (long long)plane_al;
+    R.luma[0] = R.luma[1] = base + plane_off;
+    R.grad[0] = R.grad[1] = base + plane_off + (size_t)R.nfr * plane_al;
+    plane_off += (size_t)R.nfr * 2 * plane_al;
     R.width = cols;
     R.idx = reinterpret_cast<int16_t*>(take(plane * 2));
     R.pw = reinterpret_cast<uint32_t*>(take((size_t)nblk * pitch * 4));
@@ -352,10 +373,14 @@ void carve_launch(CarveSet& S, CarveRun* h_runs, int* h_iters, cudaStream_t st) 
   launch_word_copy(S.runs_d.p, h_runs, sizeof(CarveRun) * nruns, st);  // from mapped pinned memory
   int* iters_d = reinterpret_cast<int*>(S.runs_d.as<uint8_t>() + sizeof(CarveRun) * nruns);
   SCPL_CUDA(cudaMemsetAsync(iters_d, 0, sizeof(int), st));
+  if (S.reaverage && !S.has_uniform)  // first pass on the mean gradient too (pipeline.py:289-290)
+    launch_carve_mean(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
   if (S.cols > S.target && host_loops()) {  // bursts of 8 iterations, host checks the widths
     int done_iters = 0;
     while (true) {
-      for (int k = 0; k < 8; ++k) launch_carve_iteration(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st);
+      for (int k = 0; k < 8; ++k)
+        launch_carve_iteration(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st, S.max_fr,
+                               S.reaverage);
       done_iters += 8;
       launch_word_copy(h_runs, S.runs_d.p, sizeof(CarveRun) * nruns, st);
       SCPL_CUDA(cudaStreamSynchronize(st));
@@ -365,7 +390,7 @@ void carve_launch(CarveSet& S, CarveRun* h_runs, int* h_iters, cudaStream_t st) 
     }
   } else if (S.cols > S.target) {
     S.loop = build_carve_loop(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1,
-                              iters_d);
+                              iters_d, S.max_fr, S.reaverage);
     SCPL_CUDA(cudaGraphLaunch(S.loop, st));
   }
   launch_carve_index(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
@@ -781,17 +806,25 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       const bool with_U = (ph == 0) && P.mode != 0;
       CarveSet& S = G.sets.emplace_back();
       hmark("group alloc");
+      const bool rea = P.reaverage != 0 && P.mode != 0;  // raw mode ignores it (pipeline.py:120-132)
+      std::vector<int> nfr;
+      if (rea)
+        for (int r = r0; r < r1; ++r) nfr.push_back(runs[r].second);
       carve_alloc(S, nr, rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
-                  carve_cluster_size(nr, cols, ctx->num_sms), gs);
+                  carve_cluster_size(nr, cols, ctx->num_sms), gs, rea ? nfr.data() : nullptr, rea);
       hmark("group setup");
       const size_t fbytes = (size_t)curH * curW * C;
       for (int r = r0; r < r1; ++r) {
         CarveRun& R = S.runs[r - r0];
         const int s0 = runs[r].first;
         // the first carved axis works on the original frames, whose energy codes carry the
-        // Sobel gradient of every frame (so the carve's gradient plane needs no recompute)
-        const uint16_t* fcodes = (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)s0 * h * w : nullptr;
-        launch_run_setup(cur + fbytes * (s0 - cur_t0), curH, curW, C, height ? 1 : 0, fcodes, R, gs);
+        // Sobel gradient of every frame (so the carve's gradient plane needs no recompute);
+        // reaverage carves every frame of the run, otherwise its first frame represents it
+        for (int f = 0; f < R.nfr; ++f) {
+          const uint16_t* fcodes =
+              (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)(s0 + f) * h * w : nullptr;
+          launch_run_setup(cur + fbytes * (s0 + f - cur_t0), curH, curW, C, height ? 1 : 0, fcodes, R, gs, f);
+        }
         if (with_U)
           launch_uniform(codes.as<uint16_t>(), h, w, s0, runs[r].second, 1, P.w_motion, P.w_grad, height ? 1 : 0,
                          const_cast<double*>(R.U), gs, R.pitch);

@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
 
   const int per = ((w + CL - 1) / CL + 15) & ~15;
   const int ndp = min(kMaxWarps, (per + kOwn - 1) / kOwn);
-  const bool fp64 = iters == 0 && R.U != nullptr;
+  const bool fp64 = R.U != nullptr && (iters == 0 || R.reaverage);  // reaverage: every pass on the mean
   if (tid == 0) {
     mbar_init(&s_xbar[0], 1);
     mbar_init(&s_xbar[1], 1);
@@ -973,6 +973,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) carve_compact_kernel(CarveRun*
   const CarveRun& R = runs[blockIdx.y];
   const int b = R.b;
   if (b == 0 || R.width <= R.target) return;  // nothing removed / no further pass reads the planes
+  if ((int)blockIdx.z >= R.nfr) return;       // frame of the run's plane stack (reaverage)
+  const long long fo = (long long)blockIdx.z * R.fstride;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int i = blockIdx.x * kRowWarps + wl;
   if (i >= R.rows) return;
@@ -983,8 +985,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) carve_compact_kernel(CarveRun*
   uint8_t* sG = base + pitch;
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + 2 * (size_t)pitch);
   uint64_t* bar = reinterpret_cast<uint64_t*>(hist + kMaxRowWords);
-  uint8_t* L = R.luma[0] + (long)i * pitch;
-  uint8_t* G = R.grad[0] + (long)i * pitch;
+  uint8_t* L = R.luma[0] + fo + (long)i * pitch;
+  uint8_t* G = R.grad[0] + fo + (long)i * pitch;
   const uint32_t rbytes = (uint32_t)(((w0 + 15) >> 4) << 4);
   if (lane == 0) {
     mbar_init(bar, 1);
@@ -1059,13 +1061,15 @@ __global__ void __launch_bounds__(kRowWarps * 32) carve_dirty_kernel(CarveRun* _
   const CarveRun& R = runs[blockIdx.y];
   const int b = R.b;
   if (b == 0 || R.width <= R.target) return;  // no further pass reads this gradient
+  if ((int)blockIdx.z >= R.nfr) return;
+  const long long fo = (long long)blockIdx.z * R.fstride;
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   const int rows = R.rows;
   if (i >= rows) return;
   const int wn = R.width, w0 = wn + b;
   const int dst = 0;  // planes are compacted in place
-  uint8_t* gr = R.grad[dst] + (long)i * R.pitch;
+  uint8_t* gr = R.grad[dst] + fo + (long)i * R.pitch;
   if (rows < 3 || wn < 3) {
     for (int y = lane; y < wn; y += 32) gr[y] = 0;
     return;
@@ -1075,9 +1079,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) carve_dirty_kernel(CarveRun* _
   const int16_t* l3[3] = {R.rem + (long)ia * R.rem_cap + off, R.rem + (long)i * R.rem_cap + off,
                           R.rem + (long)ib * R.rem_cap + off};
   const int16_t* ri = l3[1];
-  const uint8_t* la = R.luma[dst] + (long)ia * R.pitch;
-  const uint8_t* lb = R.luma[dst] + (long)i * R.pitch;
-  const uint8_t* lc = R.luma[dst] + (long)ib * R.pitch;
+  const uint8_t* la = R.luma[dst] + fo + (long)ia * R.pitch;
+  const uint8_t* lb = R.luma[dst] + fo + (long)i * R.pitch;
+  const uint8_t* lc = R.luma[dst] + fo + (long)ib * R.pitch;
   for (int q = lane; q < 9 * b; q += 32) {
     const int rsel = q / (3 * b), rem = q - rsel * 3 * b;
     const int s = rem / 3, offc = rem - s * 3 - 1;
@@ -1176,7 +1180,7 @@ __global__ void run_setup_kernel(const uint8_t* __restrict__ frame, int H, int W
       if (!transposed) {
         luma[(long)i * pitch + j] = v;
         grad[(long)i * pitch + j] = gv;
-        idx[(long)i * pitch + j] = (int16_t)j;
+        if (idx) idx[(long)i * pitch + j] = (int16_t)j;
       }
     }
     tl[r][threadIdx.x] = v;
@@ -1189,7 +1193,7 @@ __global__ void run_setup_kernel(const uint8_t* __restrict__ frame, int H, int W
     if (i < H && j < W) {
       luma[(long)j * pitch + i] = tl[threadIdx.x][r];
       grad[(long)j * pitch + i] = tg[threadIdx.x][r];
-      idx[(long)j * pitch + i] = (int16_t)i;
+      if (idx) idx[(long)j * pitch + i] = (int16_t)i;
     }
   }
 }
@@ -1216,16 +1220,41 @@ __global__ void plane_sobel_kernel(const uint8_t* __restrict__ luma, int rows, i
 }
 
 void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes,
-                      const CarveRun& R, cudaStream_t st) {
+                      const CarveRun& R, cudaStream_t st, int f) {
   dim3 grid(cdiv(W, 32), cdiv(H, 32));
-  run_setup_kernel<<<grid, dim3(32, 8), 0, st>>>(frame, H, W, C, transposed, codes, R.pitch, R.luma[0],
-                                                 R.grad[0], R.idx);
+  uint8_t* L = R.luma[0] + (long long)f * R.fstride;
+  uint8_t* G = R.grad[0] + (long long)f * R.fstride;
+  // the index map is the run's (one per run); frame f > 0 of a reaverage stack only needs planes
+  run_setup_kernel<<<grid, dim3(32, 8), 0, st>>>(frame, H, W, C, transposed, codes, R.pitch, L, G,
+                                                 f == 0 ? R.idx : nullptr);
   SCPL_CHECK_LAUNCH();
   if (!codes) {
-    plane_sobel_kernel<<<dim3(cdiv(R.width0, 256), R.rows), 256, 0, st>>>(R.luma[0], R.rows, R.width0,
-                                                                         R.pitch, R.grad[0]);
+    plane_sobel_kernel<<<dim3(cdiv(R.width0, 256), R.rows), 256, 0, st>>>(L, R.rows, R.width0, R.pitch, G);
     SCPL_CHECK_LAUNCH();
   }
+}
+
+// reaverage_energy (pipeline.py:289-290): U = np.stack(default_energy of every carved frame)
+// .mean(0).  The gradients are integers, so the per-pixel sum over the stack is exact in any
+// order and the mean is one correctly rounded division, as numpy's.
+__global__ void carve_mean_kernel(CarveRun* __restrict__ runs) {
+  const CarveRun& R = runs[blockIdx.y];
+  if (!R.reaverage || R.width <= R.target) return;
+  const int i = blockIdx.x;
+  if (i >= R.rows) return;
+  const double dn = (double)R.nfr;
+  double* u = const_cast<double*>(R.U) + (long)i * R.pitch;
+  for (int j = threadIdx.x; j < R.width; j += blockDim.x) {
+    uint32_t sum = 0;
+    const uint8_t* g = R.grad[0] + (long)i * R.pitch + j;
+    for (int f = 0; f < R.nfr; ++f) sum += g[(long long)f * R.fstride];
+    u[j] = __ddiv_rn((double)sum, dn);
+  }
+}
+
+void launch_carve_mean(CarveRun* runs_d, int nruns, int rows, cudaStream_t st) {
+  carve_mean_kernel<<<dim3(rows, nruns), 256, 0, st>>>(runs_d);
+  SCPL_CHECK_LAUNCH();
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)
@@ -1299,7 +1328,8 @@ bool carve_stage_dtab(int rows, int pitch, int cl) {
   return carve_smem_bytes(rows, pitch, true, 0, carve_dp_warps(pitch, cl)) <= kSmemBudget;
 }
 
-void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st) {
+void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
+                            int max_fr, bool reaverage) {
   if (nruns == 0) return;
   const int dpw = carve_dp_warps(width, cl);
   SCPL_ARG(dpw <= kMaxWarps, "carve width too large for the cluster size");
@@ -1321,13 +1351,14 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   cfg.numAttrs = 1;
   SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl));
   SCPL_CHECK_LAUNCH();
-  dim3 rgrid(cdiv(rows, kRowWarps), nruns);
+  dim3 rgrid(cdiv(rows, kRowWarps), nruns, max_fr);
   const size_t csmem = carve_compact_smem(pitch);
   smem_optin(reinterpret_cast<const void*>(carve_compact_kernel));
   carve_compact_kernel<<<rgrid, kRowWarps * 32, csmem, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();
   carve_dirty_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();
+  if (reaverage) launch_carve_mean(runs_d, nruns, rows, st);
 }
 
 // Word copy by the SMs.  Small control transfers between device memory and mapped pinned
@@ -1365,7 +1396,7 @@ __global__ void carve_check_kernel(const CarveRun* __restrict__ runs, int nruns,
 // carve every run to its target in ONE graph launch: while (any run above target)
 // { pass; compact; gradient } -- no host round trip per iteration.
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
-                                 int* iters_d) {
+                                 int* iters_d, int max_fr, bool reaverage) {
   cudaGraph_t g;
   SCPL_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -1382,7 +1413,7 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
   SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   const long before = g_launches.load();
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs);
+  launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage);
   carve_check_kernel<<<1, 256, 0, cs>>>(runs_d, nruns, max_iters, iters_d, h);
   SCPL_CUDA(cudaGetLastError());
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));

@@ -63,10 +63,13 @@ struct alignas(64) CarveRun {
   CUtensorMap tm_U;
   int rows, pitch, width0, target;
   int kmax;             // 0 = SCPL batch (k = remaining), 1 = raw (one min seam per pass)
+  int nfr;              // frames carved together (reaverage_energy: the run's frames; else 1)
+  int reaverage;        // every pass on U = mean gradient of the nfr carved frames (fp64 DP)
+  long long fstride;    // bytes between consecutive frames' luma (and gradient) planes
   int stage_dtab;       // stage the landing-delta table in shared memory (set by the launcher)
   const double* U;      // fp64 energy of the first pass, or nullptr (gradient from the start)
-  uint8_t* luma[2];     // ping-pong: pass k reads plane k & 1, the row kernels write the other
-  uint8_t* grad[2];     // gradient of the compacted luma (incrementally maintained)
+  uint8_t* luma[2];     // luma plane(s) of the carved frame(s), compacted in place ([1] == [0])
+  uint8_t* grad[2];     // their gradients (incrementally maintained; [1] == [0])
   int16_t* idx;         // output: original column of each kept column (rows x pitch)
   uint32_t* alive;      // rows x alive_pitch bitmask of surviving original columns
   int alive_pitch;
@@ -86,17 +89,20 @@ struct alignas(64) CarveRun {
   int removed;          // seams removed so far (offset of the next batch in the log)
   int b;                // size of the batch selected by the latest pass (0: none)
 };
+// planes of frame f of the run's stack (f > 0 only with reaverage_energy)
 void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes,
-                      const CarveRun& R, cudaStream_t st);
+                      const CarveRun& R, cudaStream_t st, int f = 0);
+void launch_carve_mean(CarveRun* runs_d, int nruns, int rows, cudaStream_t st);
 int carve_cluster_size(int nruns, int width, int num_sms);
 void encode_carve_tensor_maps(CarveRun& R);
-void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st);
+void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
+                            int max_fr = 1, bool reaverage = false);
 void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st);
 // dst/src: device or mapped pinned host memory; bytes rounded up to whole words (4-aligned)
 void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // 4 kernels per executed iteration (pass, compact, gradient, check); iters_d counts them
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
-                                 int* iters_d);
+                                 int* iters_d, int max_fr = 1, bool reaverage = false);
 bool carve_stage_dtab(int rows, int pitch, int cl);
 int carve_warps(int width, int cl);
 

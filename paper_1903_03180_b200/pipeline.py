@@ -101,8 +101,6 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
     clip and out should be pinned for the copies to run asynchronously.
     """
     torch = _lib.torch_cuda()
-    if config.reaverage_energy:
-        raise NotImplementedError("reaverage_energy=True is not implemented on the GPU path yet")
     T, H, W = clip.shape[:3]
     C = clip.shape[3] if clip.dim() == 4 else 1
     host = not clip.is_cuda
@@ -116,7 +114,7 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
     phi = _phi_table(config.policy)
     params = _lib.VideoParams(tw, th, _MODE_ID[config.mode], int(config.height_first), config.policy.max_len,
                               float(config.w_motion), float(config.w_grad),
-                              ctypes.cast(phi, ctypes.POINTER(ctypes.c_double)), 0)
+                              ctypes.cast(phi, ctypes.POINTER(ctypes.c_double)), 0, int(config.reaverage_energy))
     starts = (ctypes.c_int * max(T, 1))()
     lens = (ctypes.c_int * max(T, 1))()
     res = _lib.VideoResult(0, 0, ctypes.cast(starts, ctypes.POINTER(ctypes.c_int)),

@@ -126,4 +126,12 @@ CLIP_CASES = {
     "raw_w": (dict(seed=14, t=4), dict(target_width=26, mode="raw")),
     "raw_h": (dict(seed=15, t=3), dict(target_height=20, mode="raw")),
     "buf_single": (dict(seed=16, t=1), dict(target_width=20, mode="buffered")),
+    # reaverage_energy (pipeline.py:269-270, 280-296): every pass after a run's first on the
+    # mean gradient of all the run's carved frames
+    "rea_w": (dict(seed=17), dict(target_width=24, mode="buffered", reaverage_energy=True)),
+    "rea_wh": (dict(seed=18), dict(target_width=25, target_height=19, mode="buffered", reaverage_energy=True)),
+    "rea_hf": (dict(seed=19), dict(target_width=26, target_height=18, mode="buffered", height_first=True,
+                                   reaverage_energy=True)),
+    "rea_scpl": (dict(seed=20, t=5), dict(target_width=24, mode="scpl", reaverage_energy=True)),
+    "rea_gray": (dict(seed=21, gray=True), dict(target_width=21, mode="buffered", reaverage_energy=True)),
 }

@@ -316,3 +316,18 @@ def test_run_grouping_does_not_change_results(P, group_min, host, monkeypatch):
     assert [list(r) for r in m.runs] == g["runs"] and m.dp_passes == g["dp_passes"]
     bad = [i for i in range(host_out.shape[0]) if sha(host_out[i]) != g["frames_sha"][i]]
     assert not bad, f"{len(bad)} frames differ"
+
+
+def test_reaverage_small_clips_golden(P, small):
+    """reaverage_energy (pipeline.py:269-270, 280-296): runs carved on the mean gradient of
+    all their carved frames, vs the reference's outputs."""
+    names = [n for n in cases.CLIP_CASES if n.startswith("rea")]
+    assert names
+    for name in names:
+        ck, cfg = cases.CLIP_CASES[name]
+        frames = cases.small_clip(**ck)
+        out, m = P.retarget_video(frames, _cfg(P, cfg))
+        g = small["clips"][name]
+        assert m.dp_passes == g["dp_passes"], name
+        assert [list(f.shape) for f in out] == g["shapes"], name
+        assert [sha(f) for f in out] == g["frames"], name
