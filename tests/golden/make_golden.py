@@ -118,7 +118,7 @@ def small():
         json.dump(out, f, indent=0, sort_keys=True)
 
 
-def config(name: str, frames: int | None, clip: int):
+def config(name: str, frames: int | None, clip: int, reaverage: bool = False):
     from paper_1903_03180_b200.synth import config_clip
     arr, tw, th = config_clip(name, frames=frames, clip=clip)
     runs, batches = [], []
@@ -137,7 +137,8 @@ def config(name: str, frames: int | None, clip: int):
     vp.batch_carve, vp._process_run = rec_carve, rec_process
     try:
         t0 = time.time()
-        out, m = vp.retarget_video(list(arr), vp.RetargetConfig(target_width=tw, target_height=th, mode="buffered"))
+        out, m = vp.retarget_video(list(arr), vp.RetargetConfig(target_width=tw, target_height=th, mode="buffered",
+                                                                reaverage_energy=reaverage))
         wall = time.time() - t0
     finally:
         vp.batch_carve, vp._process_run = orig_carve, orig_process
@@ -148,10 +149,11 @@ def config(name: str, frames: int | None, clip: int):
         "runs": [[int(s), int(n)] for s, n in zip(starts, runs)],
         "dp_passes": m.dp_passes, "batches": batches,
         "frames_sha": [sha(f) for f in out], "out_shape": list(out[0].shape),
-        "reference_wall_s": wall,
+        "reference_wall_s": wall, "reaverage": reaverage,
     }
     suffix = f"_clip{clip}" if name == "C4" else ""
     suffix += f"_f{frames}" if frames is not None else ""
+    suffix += "_rea" if reaverage else ""
     with open(os.path.join(HERE, f"{name}{suffix}.json"), "w") as f:
         json.dump(rec, f, indent=0)
     print(name, suffix, "runs", runs, "dp", m.dp_passes, f"{wall:.1f}s", flush=True)
@@ -162,9 +164,10 @@ if __name__ == "__main__":
     ap.add_argument("what", nargs="+")
     ap.add_argument("--frames", type=int, default=None)
     ap.add_argument("--clip", type=int, default=0)
+    ap.add_argument("--reaverage", action="store_true")
     a = ap.parse_args()
     for w in a.what:
         if w == "small":
             small()
         else:
-            config(w, a.frames, a.clip)
+            config(w, a.frames, a.clip, a.reaverage)

@@ -238,7 +238,8 @@ def test_config_clip_golden(P, path):
     g = json.load(open(path))
     clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
     dev = torch.from_numpy(clip).cuda()
-    out, m = P.retarget_video_tensor(dev, P.RetargetConfig(target_width=tw, target_height=th, mode="buffered"))
+    out, m = P.retarget_video_tensor(dev, P.RetargetConfig(target_width=tw, target_height=th, mode="buffered",
+                                                           reaverage_energy=g.get("reaverage", False)))
     assert [list(r) for r in m.runs] == g["runs"]
     assert m.dp_passes == g["dp_passes"]
     host = out.cpu().numpy()
@@ -256,7 +257,8 @@ def test_config_clip_golden_host_buffers(P, path):
     clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
     host_in = torch.from_numpy(clip).pin_memory()
     out = torch.full((clip.shape[0],) + tuple(g["out_shape"]), 7, dtype=torch.uint8).pin_memory()
-    res, m = P.retarget_video(host_in, P.RetargetConfig(target_width=tw, target_height=th, mode="buffered"), out=out)
+    res, m = P.retarget_video(host_in, P.RetargetConfig(target_width=tw, target_height=th, mode="buffered",
+                                                        reaverage_energy=g.get("reaverage", False)), out=out)
     assert res.data_ptr() == out.data_ptr() and not res.is_cuda
     assert [list(r) for r in m.runs] == g["runs"]
     assert m.dp_passes == g["dp_passes"]
