@@ -133,6 +133,11 @@ int scpl_retarget_video_host(scpl_ctx* ctx, const uint8_t* frames /*host*/, int 
                              const scpl_video_params* params, uint8_t* out /*host*/, scpl_video_result* result,
                              void* stream);
 
+/* bench.jitter (bench.py:39-57): sums[t] = sum over pixels of |luma(t+1) - luma(t)| for
+ * t < T-1 (exact integers; the caller divides by h*w and averages windows as the reference). */
+int scpl_jitter_sums(scpl_ctx* ctx, const uint8_t* frames /*dev*/, int T, int h, int w, int channels,
+                     unsigned long long* sums /*dev, T-1*/, void* stream);
+
 /* ---- lower-level reference functions (API completeness; not on the hot path) ---- */
 
 /* seams.cumulative_energy (seams.py:39-65): full float64 ce and int8 back tables. */

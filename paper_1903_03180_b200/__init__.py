@@ -15,13 +15,17 @@ _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from .batching import SeamBatch, batch_carve, default_energy, label_parents, remove_batch, select_batch
 from .buffering import BufferPolicy, FixedRun, SpatioTemporalBuffer, threshold
 from .energy import MAXVAL, gradient_energy, motion_energy, to_luma
+from .media import MediaFormatError, read_clip_pinned, read_frames, retarget_stream, write_clip, write_frames
 from .pipeline import (MODES, RetargetConfig, RunMetrics, replay_batches, retarget_image, retarget_video,
                        retarget_video_tensor)
+from .quality import JitterReport, jitter
 from .seams import DpTables, Seam, cumulative_energy, min_seam, remove_seam, trace_columns, transpose
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "JitterReport", "MediaFormatError", "jitter", "read_clip_pinned", "read_frames", "retarget_stream", "write_clip",
+    "write_frames",
     "MAXVAL", "MODES", "BufferPolicy", "DpTables", "FixedRun", "RetargetConfig", "RunMetrics", "Seam",
     "SeamBatch", "SpatioTemporalBuffer", "batch_carve", "cumulative_energy", "default_energy",
     "gradient_energy", "label_parents", "min_seam", "motion_energy", "remove_batch", "remove_seam",

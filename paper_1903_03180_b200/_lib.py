@@ -57,6 +57,7 @@ _SIGS = {
                          _vp, _c_int_p, _vp, _vp, _vp, _vp, _vp],
     "scpl_replay": [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int,
                     ctypes.c_int, ctypes.c_int, _vp, _vp],
+    "scpl_jitter_sums": [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp],
     "scpl_retarget_video": [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                             ctypes.POINTER(VideoParams), _vp, ctypes.POINTER(VideoResult), _vp],
     "scpl_retarget_video_host": [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,

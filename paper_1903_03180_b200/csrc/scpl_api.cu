@@ -927,6 +927,15 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
 
 extern "C" {
 
+int scpl_jitter_sums(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int w, int channels,
+                     unsigned long long* sums, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
+    SCPL_ARG(T >= 2, "need at least 2 frames");
+    launch_jitter_sums(frames, T, (long)h * w, channels, sums, (cudaStream_t)stream);
+  });
+}
+
 int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int w, int channels,
                         const scpl_video_params* params, uint8_t* out, scpl_video_result* result, void* stream) {
   return guarded(ctx, [&] {

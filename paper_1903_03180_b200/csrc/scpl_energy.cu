@@ -382,6 +382,41 @@ void launch_decode(const uint16_t* codes, long per_frame, int T, int first_pure,
   SCPL_CHECK_LAUNCH();
 }
 
+// jitter (bench.py:39-57): per consecutive frame pair, the exact integer sum over pixels of
+// |luma(t+1) - luma(t)| (the reference takes the float64 mean of these integers, which is
+// exact up to the one division done on the host)
+template <int C>
+__global__ void jitter_sums_kernel(const uint8_t* __restrict__ frames, long npx, unsigned long long* __restrict__ sums) {
+  const int t = blockIdx.y;
+  const uint8_t* a = frames + (size_t)t * npx * C;
+  const uint8_t* b = a + (size_t)npx * C;
+  unsigned long long acc = 0;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < npx; p += (long)gridDim.x * blockDim.x) {
+    int la, lb;
+    if (C == 3) {
+      la = (int)luma_of(a[3 * p], a[3 * p + 1], a[3 * p + 2]);
+      lb = (int)luma_of(b[3 * p], b[3 * p + 1], b[3 * p + 2]);
+    } else {
+      la = a[p];
+      lb = b[p];
+    }
+    acc += (unsigned long long)abs(lb - la);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&sums[t], acc);
+}
+
+void launch_jitter_sums(const uint8_t* frames, int T, long npx, int C, unsigned long long* sums, cudaStream_t st) {
+  if (T < 2) return;
+  SCPL_CUDA(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * (T - 1), st));
+  dim3 grid((unsigned)std::min<long>(cdiv(npx, 256), 256), T - 1);
+  if (C == 3)
+    jitter_sums_kernel<3><<<grid, 256, 0, st>>>(frames, npx, sums);
+  else
+    jitter_sums_kernel<1><<<grid, 256, 0, st>>>(frames, npx, sums);
+  SCPL_CHECK_LAUNCH();
+}
+
 // gradient_energy of a luma plane, as float64 (API) -- energy.py:40-59
 __global__ void sobel_f64_kernel(const uint8_t* __restrict__ luma, int H, int W, double* __restrict__ out) {
   long n = (long)H * W;

@@ -27,6 +27,7 @@ void launch_luma(const uint8_t* rgb, long npx, int C, uint8_t* out, cudaStream_t
 void launch_decode(const uint16_t* codes, long per_frame, int T, int first_pure, double wm, double wg,
                    double* out, cudaStream_t st);
 void launch_sobel_f64(const uint8_t* luma, int H, int W, double* out, cudaStream_t st);
+void launch_jitter_sums(const uint8_t* frames, int T, long npx, int C, unsigned long long* sums, cudaStream_t st);
 
 void launch_window_stats(const uint16_t* codes, long N, const int2* leaves, int nleaves, int s, int n_acc,
                          int L, int first_pure, int init, double wm, double wg, double* ckS, double* ckQ,

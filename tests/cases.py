@@ -135,3 +135,37 @@ CLIP_CASES = {
     "rea_scpl": (dict(seed=20, t=5), dict(target_width=24, mode="scpl", reaverage_energy=True)),
     "rea_gray": (dict(seed=21, gray=True), dict(target_width=21, mode="buffered", reaverage_energy=True)),
 }
+
+
+# ------------------------------------------------------------------ media / jitter
+def media_streams():
+    """(name, bytes) PNM streams exercising the byte grammar and its errors (media.py:139-223)."""
+    rng = np.random.default_rng(31)
+    rgb = rng.integers(0, 256, (5, 7, 3), dtype=np.uint8)
+    gray = rng.integers(0, 256, (4, 6), dtype=np.uint8)
+    rgb2 = rng.integers(0, 256, (5, 7, 3), dtype=np.uint8)
+    p6 = b"P6\n7 5\n255\n" + rgb.tobytes()
+    return [
+        ("p6_two", p6 + b"P6 7 5 255 " + rgb2.tobytes()),
+        ("p5_comment", b"P5 # a comment\n6\t4\r\n# more\n255\n" + gray.tobytes()),
+        ("empty", b""),
+        ("whitespace_only", b" \n\t "),
+        ("bad_magic", b"P3 7 5 255\n" + rgb.tobytes()),
+        ("bad_maxval", b"P6 7 5 65535\n" + rgb.tobytes()),
+        ("bad_dims", b"P6 0 5 255\n"),
+        ("bad_width", b"P6 x 5 255\n"),
+        ("truncated", p6[:-5]),
+        ("header_eof", b"P6 7"),
+        ("dim_change", p6 + b"P6 6 5 255\n" + rgb[:, :6].tobytes()),
+        ("mixed_gray_rgb", p6 + b"P5 7 5 255\n" + gray.ravel()[:1].tobytes() * 35),
+    ]
+
+
+JITTER_CASES = {  # name -> (small_clip kwargs, window)
+    "j_default": (dict(seed=40, t=9), 4),
+    "j_short": (dict(seed=41, t=3), 4),
+    "j_two": (dict(seed=42, t=2), 4),
+    "j_w2": (dict(seed=43, t=12), 2),
+    "j_gray": (dict(seed=44, t=7, gray=True), 3),
+    "j_long": (dict(seed=45, t=40, h=30, w=50), 5),
+}

@@ -114,6 +114,25 @@ def small():
         cl[name] = {"frames": [sha(f) for f in res], "shapes": [list(f.shape) for f in res],
                     "dp_passes": m.dp_passes}
     out["clips"] = cl
+
+    import io
+    from vidcarve import bench as vb, media as vm
+    md = {}
+    for name, data in cases.media_streams():
+        try:
+            fr = list(vm.read_frames(io.BytesIO(data)))
+            md[name] = {"frames": [sha(f) for f in fr], "shapes": [list(f.shape) for f in fr]}
+            buf = io.BytesIO()
+            vm.write_frames(buf, fr)
+            md[name]["written"] = sha(np.frombuffer(buf.getvalue(), np.uint8)) if fr else None
+        except Exception as e:  # noqa: BLE001 -- the reference's exception type and message are the fixture
+            md[name] = {"error": type(e).__name__, "message": str(e)}
+    out["media"] = md
+    jt = {}
+    for name, (ck, win) in cases.JITTER_CASES.items():
+        frames = cases.small_clip(**ck)
+        jt[name] = fhex(vb.jitter(frames, window=win).value)
+    out["jitter"] = jt
     with open(os.path.join(HERE, "small.json"), "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)
 

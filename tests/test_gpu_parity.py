@@ -333,3 +333,35 @@ def test_reaverage_small_clips_golden(P, small):
         assert m.dp_passes == g["dp_passes"], name
         assert [list(f.shape) for f in out] == g["shapes"], name
         assert [sha(f) for f in out] == g["frames"], name
+
+
+def test_jitter_golden(P, small):
+    """bench.jitter (bench.py:39-57) on the GPU: exact integer pair sums, the reference's float
+    means -- bit-equal values."""
+    for name, (ck, win) in cases.JITTER_CASES.items():
+        rep = P.jitter(cases.small_clip(**ck), window=win)
+        assert rep.window == win
+        assert float(rep.value).hex() == small["jitter"][name], name
+    with pytest.raises(ValueError, match="at least 2 frames"):
+        P.jitter([np.zeros((4, 4, 3), np.uint8)])
+
+
+def test_pnm_stream_retarget_roundtrip(P, small):
+    """The `vidcarve video - -` pipe on the GPU: PNM bytes -> pinned clip -> retarget ->
+    PNM bytes, frames equal to the reference's retarget_video outputs."""
+    import io
+    from paper_1903_03180_b200 import media
+    for name in ("buf_w", "buf_wh", "rea_w"):
+        ck, cfg = cases.CLIP_CASES[name]
+        frames = cases.small_clip(**ck)
+        src = io.BytesIO()
+        media.write_frames(src, frames)
+        src.seek(0)
+        clip = media.read_clip_pinned(src)
+        assert clip.is_pinned() and tuple(clip.shape) == (len(frames),) + frames[0].shape
+        src.seek(0)
+        dst = io.BytesIO()
+        media.retarget_stream(src, dst, _cfg(P, cfg))
+        dst.seek(0)
+        out = list(media.read_frames(dst))
+        assert [sha(f) for f in out] == small["clips"][name]["frames"], name
