@@ -18,13 +18,14 @@ from .energy import MAXVAL, gradient_energy, motion_energy, to_luma
 from .media import MediaFormatError, read_clip_pinned, read_frames, retarget_stream, write_clip, write_frames
 from .pipeline import (MODES, RetargetConfig, RunMetrics, replay_batches, retarget_image, retarget_video,
                        retarget_video_tensor)
-from .quality import JitterReport, jitter
+from .quality import SYNTHETIC_KINDS, JitterReport, SyntheticSpec, compare, format_metrics, generate, jitter
 from .seams import DpTables, Seam, cumulative_energy, min_seam, remove_seam, trace_columns, transpose
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "JitterReport", "MediaFormatError", "jitter", "read_clip_pinned", "read_frames", "retarget_stream", "write_clip",
+    "JitterReport", "MediaFormatError", "SYNTHETIC_KINDS", "SyntheticSpec", "compare", "format_metrics", "generate",
+    "jitter", "read_clip_pinned", "read_frames", "retarget_stream", "write_clip",
     "write_frames",
     "MAXVAL", "MODES", "BufferPolicy", "DpTables", "FixedRun", "RetargetConfig", "RunMetrics", "Seam",
     "SeamBatch", "SpatioTemporalBuffer", "batch_carve", "cumulative_energy", "default_energy",

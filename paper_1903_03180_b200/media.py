@@ -230,8 +230,10 @@ def read_clip_pinned(source: str | Path | BinaryIO, capacity: int = 64):
     read_frames and one copy per frame.
     """
     import torch
-    if source != "-" and not hasattr(source, "read") and Path(source).suffix.lower() not in (".ppm", ".pgm"):
-        frames = list(read_frames(source))
+    if (source != "-" and not hasattr(source, "read")
+            and (Path(source).is_dir() or Path(source).suffix.lower() not in (".ppm", ".pgm")
+                 or not Path(source).exists())):
+        frames = list(read_frames(source))  # directories, PNG, missing paths: read_frames' behaviour
         if not frames:
             return torch.empty((0,), dtype=torch.uint8)
         return torch.from_numpy(np.stack(frames)).pin_memory()

@@ -51,4 +51,79 @@ def jitter(frames, window: int = 4) -> JitterReport:
     return JitterReport(window=window, value=float(np.mean(values)))
 
 
-__all__ = ["JitterReport", "jitter"]
+# ------------------------------------------------------------------ corpora and comparison
+SYNTHETIC_KINDS = ("static", "moving-box", "brightness-ramp")
+
+
+@dataclass(frozen=True)
+class SyntheticSpec:
+    """Deterministic corpus recipe (bench.py:29-36)."""
+
+    kind: str
+    width: int = 320
+    height: int = 240
+    frames: int = 32
+    seed: int = 0
+
+
+def generate(spec: SyntheticSpec) -> list:
+    """The reference's three synthetic corpora, byte for byte (bench.py:60-97): a static noise
+    frame, a bright box sliding over a noise background, a wrapping brightness ramp."""
+    if spec.kind not in SYNTHETIC_KINDS:
+        raise ValueError(f"unknown corpus kind {spec.kind!r}, expected one of {SYNTHETIC_KINDS}")
+    if spec.width < 3 or spec.height < 3:
+        raise ValueError(f"corpus frames must be at least 3x3, got {spec.width}x{spec.height}")
+    if spec.frames < 1:
+        raise ValueError(f"frame count must be >= 1, got {spec.frames}")
+    rng = np.random.default_rng(spec.seed)
+    h, w, n = spec.height, spec.width, spec.frames
+    if spec.kind == "static":
+        still = rng.integers(112, 144, size=(h, w, 3), dtype=np.uint8)
+        return [still.copy() for _ in range(n)]
+    if spec.kind == "moving-box":
+        bg = rng.integers(0, 128, size=(h, w, 3), dtype=np.uint8)
+        bw, bh, top = max(4, w // 8), max(4, h // 8), h // 4
+        out = []
+        for t in range(n):
+            f = bg.copy()
+            left = t % (w - bw + 1)
+            f[top:top + bh, left:left + bw] = 250
+            out.append(f)
+        return out
+    ramp = rng.integers(0, 64, size=(h, w, 3), dtype=np.int64)
+    return [np.clip(ramp + (16 * t) % 192, 0, 255).astype(np.uint8) for t in range(n)]
+
+
+def compare(frames, variants: dict) -> dict:
+    """Every config variant over the corpus, metrics with jitter (bench.py:100-112)."""
+    from .pipeline import retarget_video
+    if not variants:
+        raise ValueError("need at least one config variant")
+    results = {}
+    for name, config in variants.items():
+        out, metrics = retarget_video(frames, config)
+        if len(out) >= 2:
+            metrics.jitter = jitter(out).value
+        results[name] = metrics
+    return results
+
+
+def format_metrics(results) -> str:
+    """Flat key=value report, variant-prefixed keys when comparing (bench.py:115-131)."""
+    lines = []
+
+    def emit(prefix, m):
+        lines.extend([f"{prefix}dp_passes={m.dp_passes}", f"{prefix}wall_time_s={m.wall_time:.6f}",
+                      f"{prefix}frames_out={m.frames_out}"])
+        if m.jitter is not None:
+            lines.append(f"{prefix}jitter={m.jitter:.6f}")
+
+    if isinstance(results, dict):
+        for name, m in results.items():
+            emit(f"{name}.", m)
+    else:
+        emit("", results)
+    return "\n".join(lines) + "\n"
+
+
+__all__ = ["JitterReport", "SYNTHETIC_KINDS", "SyntheticSpec", "compare", "format_metrics", "generate", "jitter"]

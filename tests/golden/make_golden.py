@@ -133,6 +133,13 @@ def small():
         frames = cases.small_clip(**ck)
         jt[name] = fhex(vb.jitter(frames, window=win).value)
     out["jitter"] = jt
+    cb = {}
+    for kind in vb.SYNTHETIC_KINDS:
+        frames = vb.generate(vb.SyntheticSpec(kind=kind, width=40, height=30, frames=9, seed=2))
+        res = vb.compare(frames, {m: vidcarve.RetargetConfig(target_width=30, mode=m) for m in vidcarve.MODES})
+        cb[kind] = {m: {"dp_passes": r.dp_passes, "frames_out": r.frames_out, "jitter": f"{r.jitter:.6f}"}
+                    for m, r in res.items()}
+    out["cli_bench"] = cb
     with open(os.path.join(HERE, "small.json"), "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)
 
