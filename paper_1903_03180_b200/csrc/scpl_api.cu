@@ -727,42 +727,42 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   cudaEvent_t ev_alloc = new_event(false);
   SCPL_CUDA(cudaEventRecord(ev_alloc, st));
 
-  // 1. frames in (host) and energy codes, chunk by chunk
+  // 1. frames in (host) and energy codes, chunk by chunk (the scan starts on the first chunk)
   std::vector<cudaEvent_t> ev_chunk_codes(nchunk, nullptr);
-  if (host_in) {
-    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
-    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ev_alloc, 0));
-    for (int c = 0; c < nchunk; ++c) {
-      const int t0 = c * chunk, n = std::min(chunk, T - t0);
+  if (host_in) SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
+  SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ev_alloc, 0));
+  for (int c = 0; c < nchunk; ++c) {
+    const int t0 = c * chunk, n = std::min(chunk, T - t0);
+    if (host_in) {
       SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
                                 fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
       mark("h2d " + std::to_string(c), ctx->s_h2d);
       cudaEvent_t e = new_event(false);
       SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
       SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, e, 0));
-      if (P.mode != 0)
-        launch_codes(frames, nullptr, t0, n, h, w, C, codes.as<uint16_t>(), ctx->num_sms, ctx->s_codes);
-      ev_chunk_codes[c] = new_event(false);
-      SCPL_CUDA(cudaEventRecord(ev_chunk_codes[c], ctx->s_codes));
     }
+    if (P.mode != 0)
+      launch_codes(frames, nullptr, t0, n, h, w, C, codes.as<uint16_t>(), ctx->num_sms, ctx->s_codes);
+    ev_chunk_codes[c] = new_event(false);
+    SCPL_CUDA(cudaEventRecord(ev_chunk_codes[c], ctx->s_codes));
   }
   cudaStream_t ss = ctx->s_scan;
   SCPL_CUDA(cudaStreamWaitEvent(ss, ev_alloc, 0));
-  if (!host_in && P.mode != 0) launch_codes(frames, nullptr, 0, T, h, w, C, codes.as<uint16_t>(), ctx->num_sms, ss);
-  SCPL_CUDA(cudaEventRecord(ev_codes, ss));
+  SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[0], 0));
+  SCPL_CUDA(cudaEventRecord(ev_codes, ss));  // (first chunk's codes)
 
   // 2. buffer scan, chunk by chunk (fixed one-frame runs for scpl / raw)
   std::vector<cudaEvent_t> ev_chunk(nchunk, nullptr);
   if (buffered) {
     for (int c = 0; c < nchunk; ++c) {
-      if (host_in) SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[c], 0));
+      SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[c], 0));
       scan_chunk(ctx, scan, c, std::min(T, (c + 1) * chunk), ss);
       mark("scan " + std::to_string(c), ss);
       ev_chunk[c] = new_event(false);
       SCPL_CUDA(cudaEventRecord(ev_chunk[c], ss));
     }
     scan_end(ctx, scan, ss);
-  } else if (host_in) {
+  } else {
     SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[nchunk - 1], 0));
   }
   SCPL_CUDA(cudaEventRecord(ev_scan, ss));
