@@ -403,7 +403,7 @@ void carve_finish(CarveSet& S) {
   const int nruns = (int)S.runs.size();
   if (nruns == 0) return;
   std::memcpy(S.runs.data(), S.h_runs, sizeof(CarveRun) * nruns);
-  g_launches.fetch_add(4L * *S.h_iters, std::memory_order_relaxed);
+  g_launches.fetch_add((long)carve_kernels_per_iteration(S.reaverage) * *S.h_iters, std::memory_order_relaxed);
   for (auto& R : S.runs)
     if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;

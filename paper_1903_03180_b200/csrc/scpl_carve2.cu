@@ -214,7 +214,7 @@ struct DpCfg<false> {
 };
 template <>
 struct DpCfg<true> {
-  static constexpr int kStageRows = 4, kStages = 6;   // fp64 rows are 8x larger: finer ring
+  static constexpr int kStageRows = 4, kStages = 3;   // fp64 rows are 8x larger: finer ring
 };
 template <bool F64>
 __host__ __device__ constexpr size_t dp_ring_bytes() {
@@ -681,6 +681,156 @@ __device__ __forceinline__ int alive_select(const uint32_t* wv, const int* pre, 
   return lo * 32 + (int)__fns(wv[lo], 0, c - pre[lo] + 1);
 }
 
+// ------------------------------------------------------------------ row kernels
+// Compact one row of luma and gradient in place (remove_batch, batching.py:76-107).  Output
+// byte y reads input byte y + s(y), s(y) = #{t : a_t <= y}, a_t = rem[t] - t.  The warp
+// stages the source row in shared memory (TMA bulk copy, so the in-place writes cannot race
+// the reads), counts a_t per output word in a packed histogram (low half: a_t <= 4q, high
+// half: a_t <= 4q + 3), prefix-sums it, and writes each output word as one funnel shift of
+// two source words -- or byte by byte when its shift changes inside the word.
+constexpr int kRowWarps = 8;
+constexpr int kMaxRowWords = 1024;  // widths up to 4096
+
+// The compaction CTA is small (kCompWarps warps, shared memory sized by the pitch) so that it
+// fits next to a resident pass CTA: the row kernels of one group then run on SMs that other
+// groups' (latency-bound) passes hold, instead of queueing for free SMs.
+constexpr int kCompWarps = 4;
+__host__ __device__ __forceinline__ size_t compact_warp_bytes(int pitch) {
+  return 2 * (size_t)pitch + 4 * (size_t)((pitch >> 2) + 4) + 16;  // rows, histogram (nwo + 1 words), barrier
+}
+size_t carve_compact_smem(int pitch) { return (size_t)kCompWarps * compact_warp_bytes(pitch); }
+
+// Stage one row of luma and gradient (lane 0; whole 16-byte chunks of the w0 columns).
+__device__ __forceinline__ void compact_issue(const uint8_t* L, const uint8_t* G, int w0, uint8_t* sL, uint8_t* sG,
+                                              uint64_t* bar) {
+  const uint32_t rbytes = (uint32_t)(((w0 + 15) >> 4) << 4);
+  mbar_arrive_tx(bar, 2 * rbytes);
+  bulk_g2s(sL, L, rbytes, bar);
+  bulk_g2s(sG, G, rbytes, bar);
+}
+
+// One warp compacts one staged row in place: rg = the row's b removed columns (ascending, in
+// the w0 = wn + b column frame); the staging completes on bar (phase `parity`).
+__device__ __forceinline__ void compact_row(uint8_t* L, uint8_t* G, const int16_t* rg, int b, int wn,
+                                            const uint8_t* sL, const uint8_t* sG, uint32_t* hist, uint64_t* bar,
+                                            uint32_t parity) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = wn + b;
+  const int nwo = (wn + 3) >> 2;
+  for (int q = lane; q <= nwo; q += 32) hist[q] = 0u;
+  __syncwarp();
+  for (int t = lane; t < b; t += 32) {
+    const int at = rg[t] - t;  // >= 0
+    const int q1 = (at + 3) >> 2, q2 = at >> 2;  // a_t <= 4q  <=>  q >= q1;  a_t <= 4q+3  <=>  q >= q2
+    if (q1 <= nwo) atomicAdd(&hist[q1], 1u);
+    if (q2 <= nwo) atomicAdd(&hist[q2], 0x10000u);
+  }
+  __syncwarp();
+  // inclusive prefix over q = 0 .. nwo-1: lane owns a contiguous segment
+  const int per = (nwo + 31) >> 5;
+  const int q0 = min(nwo, lane * per), q1 = min(nwo, q0 + per);
+  uint32_t run = 0;
+  for (int q = q0; q < q1; ++q) run += hist[q];
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  run = incl - run;
+  for (int q = q0; q < q1; ++q) {
+    run += hist[q];
+    hist[q] = run;
+  }
+  mbar_wait(bar, parity);
+  __syncwarp();
+  const uint32_t* Lw = reinterpret_cast<const uint32_t*>(sL);
+  const uint32_t* Gw = reinterpret_cast<const uint32_t*>(sG);
+  const int nwi = (w0 + 3) >> 2;
+  for (int q = lane; q < nwo; q += 32) {
+    const uint32_t h = hist[q];
+    const int s0 = (int)(h & 0xffffu), s3 = (int)(h >> 16);
+    uint32_t lv, gv;
+    if (s0 == s3) {
+      const int x0 = 4 * q + s0, wq = x0 >> 2;
+      const uint32_t sh = (uint32_t)(x0 & 3) * 8u;
+      const bool nx = wq + 1 < nwi;
+      lv = __funnelshift_r(Lw[wq], nx ? Lw[wq + 1] : 0u, sh);
+      gv = __funnelshift_r(Gw[wq], nx ? Gw[wq + 1] : 0u, sh);
+    } else {  // s(4q + u) for u = 0..3 from the removed list
+      int t = s0;
+      lv = 0u;
+      gv = 0u;
+      for (int u = 0; u < 4; ++u) {
+        while (t < b && rg[t] - t <= 4 * q + u) ++t;
+        const int x = 4 * q + u + t;
+        if (x < w0) {
+          lv |= (uint32_t)sL[x] << (8 * u);
+          gv |= (uint32_t)sG[x] << (8 * u);
+        }
+      }
+    }
+    reinterpret_cast<uint32_t*>(L)[q] = lv;
+    reinterpret_cast<uint32_t*>(G)[q] = gv;
+  }
+  __syncwarp();  // hist and the staged row are free again
+}
+
+// default_energy (batching.py:110-115) of row i of the carved frame, incrementally: a pixel's
+// Sobel value changes only if a removed pixel of rows i-1..i+1 lay within one column of it.
+// `lum`/`gra` are the frame's planes, off = the batch's offset in the removed-column log.
+// The three rows' removed-column lists are staged in the warp's shared memory (`stage`, 3 x
+// kDirtyCap entries) when they fit, so the binary searches below do not chain global loads.
+constexpr int kDirtyCap = 256;
+__device__ __forceinline__ void dirty_row(const CarveRun& R, const uint8_t* lum, uint8_t* gra, int i, int b, int wn,
+                                          int off, int16_t* stage) {
+  const int lane = threadIdx.x & 31;
+  const int rows = R.rows;
+  const int w0 = wn + b;
+  uint8_t* gr = gra + (long)i * R.pitch;
+  if (rows < 3 || wn < 3) {
+    for (int y = lane; y < wn; y += 32) gr[y] = 0;
+    return;
+  }
+  const int ia = max(i - 1, 0), ib = min(i + 1, rows - 1);
+  const int16_t* ra = R.rem + (long)ia * R.rem_cap + off;
+  const int16_t* ri = R.rem + (long)i * R.rem_cap + off;
+  const int16_t* rc = R.rem + (long)ib * R.rem_cap + off;
+  if (b <= kDirtyCap) {
+    for (int t = lane; t < b; t += 32) {
+      const int16_t va = ra[t], vi = ri[t], vc = rc[t];
+      stage[t] = va;
+      stage[kDirtyCap + t] = vi;
+      stage[2 * kDirtyCap + t] = vc;
+    }
+    __syncwarp();
+    ra = stage;
+    ri = stage + kDirtyCap;
+    rc = stage + 2 * kDirtyCap;
+  }
+  const uint8_t* la = lum + (long)ia * R.pitch;
+  const uint8_t* lb = lum + (long)i * R.pitch;
+  const uint8_t* lc = lum + (long)ib * R.pitch;
+  for (int q = lane; q < 9 * b; q += 32) {
+    const int rsel = q / (3 * b), rem = q - rsel * 3 * b;
+    const int s = rem / 3, offc = rem - s * 3 - 1;
+    const int x = (rsel == 0 ? ra : rsel == 1 ? ri : rc)[s] + offc;
+    if (x < 0 || x >= w0) continue;
+    int lo = 0, hi = b;  // row-i removed columns < x
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (ri[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    if (lo < b && ri[lo] == x) continue;  // removed itself
+    const int y = x - lo;
+    const int ym = max(y - 1, 0), yp = min(y + 1, wn - 1);
+    const int gx = (la[yp] + 2 * lb[yp] + lc[yp]) - (la[ym] + 2 * lb[ym] + lc[ym]);
+    const int gy = (lc[ym] + 2 * lc[y] + lc[yp]) - (la[ym] + 2 * la[y] + la[yp]);
+    const int gv = abs(gx) + abs(gy);
+    gr[y] = (uint8_t)(gv > 255 ? 255 : gv);
+  }
+}
+
 // One DP pass + select + trace for every active run (one cluster per run).  Per-run state
 // (width, iters, removed) is read at entry and written back at exit.
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun* __restrict__ runs, int CL) {
@@ -956,19 +1106,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   }
 }
 
-// ------------------------------------------------------------------ row kernels
-// Compact one row of luma and gradient in place (remove_batch, batching.py:76-107).  Output
-// byte y reads input byte y + s(y), s(y) = #{t : a_t <= y}, a_t = rem[t] - t.  The warp
-// stages the source row in shared memory (TMA bulk copy, so the in-place writes cannot race
-// the reads), counts a_t per output word in a packed histogram (low half: a_t <= 4q, high
-// half: a_t <= 4q + 3), prefix-sums it, and writes each output word as one funnel shift of
-// two source words -- or byte by byte when its shift changes inside the word.
-constexpr int kRowWarps = 8;
-constexpr int kMaxRowWords = 1024;  // widths up to 4096
-
-size_t carve_compact_smem(int pitch) { return (size_t)kRowWarps * (2 * (size_t)pitch + 4 * kMaxRowWords + 16); }
-
-__global__ void __launch_bounds__(kRowWarps * 32) carve_compact_kernel(CarveRun* __restrict__ runs) {
+__global__ void __launch_bounds__(kCompWarps * 32) carve_compact_kernel(CarveRun* __restrict__ runs) {
   extern __shared__ __align__(16) uint8_t csm[];
   const CarveRun& R = runs[blockIdx.y];
   const int b = R.b;
@@ -976,130 +1114,34 @@ __global__ void __launch_bounds__(kRowWarps * 32) carve_compact_kernel(CarveRun*
   if ((int)blockIdx.z >= R.nfr) return;       // frame of the run's plane stack (reaverage)
   const long long fo = (long long)blockIdx.z * R.fstride;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int i = blockIdx.x * kRowWarps + wl;
+  const int i = blockIdx.x * kCompWarps + wl;
   if (i >= R.rows) return;
   const int pitch = R.pitch;
-  const int wn = R.width, w0 = wn + b;
-  uint8_t* base = csm + (size_t)wl * (2 * (size_t)pitch + 4 * kMaxRowWords + 16);
+  uint8_t* base = csm + (size_t)wl * compact_warp_bytes(pitch);
   uint8_t* sL = base;
   uint8_t* sG = base + pitch;
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + 2 * (size_t)pitch);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(hist + kMaxRowWords);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(hist + (pitch >> 2) + 4);
   uint8_t* L = R.luma[0] + fo + (long)i * pitch;
   uint8_t* G = R.grad[0] + fo + (long)i * pitch;
-  const uint32_t rbytes = (uint32_t)(((w0 + 15) >> 4) << 4);
   if (lane == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    mbar_arrive_tx(bar, 2 * rbytes);
-    bulk_g2s(sL, L, rbytes, bar);
-    bulk_g2s(sG, G, rbytes, bar);
+    compact_issue(L, G, R.width + b, sL, sG, bar);
   }
-  const int nwo = (wn + 3) >> 2;
-  for (int q = lane; q <= nwo; q += 32) hist[q] = 0u;
-  __syncwarp();
-  const int16_t* rg = R.rem + (long)i * R.rem_cap + (R.removed - b);
-  for (int t = lane; t < b; t += 32) {
-    const int at = rg[t] - t;  // >= 0
-    const int q1 = (at + 3) >> 2, q2 = at >> 2;  // a_t <= 4q  <=>  q >= q1;  a_t <= 4q+3  <=>  q >= q2
-    if (q1 <= nwo) atomicAdd(&hist[q1], 1u);
-    if (q2 <= nwo) atomicAdd(&hist[q2], 0x10000u);
-  }
-  __syncwarp();
-  // inclusive prefix over q = 0 .. nwo-1: lane owns a contiguous segment
-  const int per = (nwo + 31) >> 5;
-  const int q0 = min(nwo, lane * per), q1 = min(nwo, q0 + per);
-  uint32_t run = 0;
-  for (int q = q0; q < q1; ++q) run += hist[q];
-  uint32_t incl = run;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  run = incl - run;
-  for (int q = q0; q < q1; ++q) {
-    run += hist[q];
-    hist[q] = run;
-  }
-  mbar_wait(bar, 0);
-  __syncwarp();
-  const uint32_t* Lw = reinterpret_cast<const uint32_t*>(sL);
-  const uint32_t* Gw = reinterpret_cast<const uint32_t*>(sG);
-  const int nwi = (w0 + 3) >> 2;
-  for (int q = lane; q < nwo; q += 32) {
-    const uint32_t h = hist[q];
-    const int s0 = (int)(h & 0xffffu), s3 = (int)(h >> 16);
-    uint32_t lv, gv;
-    if (s0 == s3) {
-      const int x0 = 4 * q + s0, wq = x0 >> 2;
-      const uint32_t sh = (uint32_t)(x0 & 3) * 8u;
-      const bool nx = wq + 1 < nwi;
-      lv = __funnelshift_r(Lw[wq], nx ? Lw[wq + 1] : 0u, sh);
-      gv = __funnelshift_r(Gw[wq], nx ? Gw[wq + 1] : 0u, sh);
-    } else {  // s(4q + u) for u = 0..3 from the removed list
-      int t = s0;
-      lv = 0u;
-      gv = 0u;
-      for (int u = 0; u < 4; ++u) {
-        while (t < b && rg[t] - t <= 4 * q + u) ++t;
-        const int x = 4 * q + u + t;
-        if (x < w0) {
-          lv |= (uint32_t)sL[x] << (8 * u);
-          gv |= (uint32_t)sG[x] << (8 * u);
-        }
-      }
-    }
-    reinterpret_cast<uint32_t*>(L)[q] = lv;
-    reinterpret_cast<uint32_t*>(G)[q] = gv;
-  }
+  compact_row(L, G, R.rem + (long)i * R.rem_cap + (R.removed - b), b, R.width, sL, sG, hist, bar, 0);
 }
 
-// default_energy (batching.py:110-115) of the carved frame, incrementally: a pixel's Sobel
-// value changes only if a removed pixel of rows i-1..i+1 lay within one column of it.
 __global__ void __launch_bounds__(kRowWarps * 32) carve_dirty_kernel(CarveRun* __restrict__ runs) {
   const CarveRun& R = runs[blockIdx.y];
   const int b = R.b;
   if (b == 0 || R.width <= R.target) return;  // no further pass reads this gradient
   if ((int)blockIdx.z >= R.nfr) return;
   const long long fo = (long long)blockIdx.z * R.fstride;
-  const int lane = threadIdx.x & 31;
+  __shared__ int16_t s_lists[kRowWarps][3 * kDirtyCap];
   const int i = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
-  const int rows = R.rows;
-  if (i >= rows) return;
-  const int wn = R.width, w0 = wn + b;
-  const int dst = 0;  // planes are compacted in place
-  uint8_t* gr = R.grad[dst] + fo + (long)i * R.pitch;
-  if (rows < 3 || wn < 3) {
-    for (int y = lane; y < wn; y += 32) gr[y] = 0;
-    return;
-  }
-  const int off = R.removed - b;
-  const int ia = max(i - 1, 0), ib = min(i + 1, rows - 1);
-  const int16_t* l3[3] = {R.rem + (long)ia * R.rem_cap + off, R.rem + (long)i * R.rem_cap + off,
-                          R.rem + (long)ib * R.rem_cap + off};
-  const int16_t* ri = l3[1];
-  const uint8_t* la = R.luma[dst] + fo + (long)ia * R.pitch;
-  const uint8_t* lb = R.luma[dst] + fo + (long)i * R.pitch;
-  const uint8_t* lc = R.luma[dst] + fo + (long)ib * R.pitch;
-  for (int q = lane; q < 9 * b; q += 32) {
-    const int rsel = q / (3 * b), rem = q - rsel * 3 * b;
-    const int s = rem / 3, offc = rem - s * 3 - 1;
-    const int x = l3[rsel][s] + offc;
-    if (x < 0 || x >= w0) continue;
-    int lo = 0, hi = b;  // row-i removed columns < x
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (ri[mid] < x) lo = mid + 1; else hi = mid;
-    }
-    if (lo < b && ri[lo] == x) continue;  // removed itself
-    const int y = x - lo;
-    const int ym = max(y - 1, 0), yp = min(y + 1, wn - 1);
-    const int gx = (la[yp] + 2 * lb[yp] + lc[yp]) - (la[ym] + 2 * lb[ym] + lc[ym]);
-    const int gy = (lc[ym] + 2 * lc[y] + lc[yp]) - (la[ym] + 2 * la[y] + la[yp]);
-    const int gv = abs(gx) + abs(gy);
-    gr[y] = (uint8_t)(gv > 255 ? 255 : gv);
-  }
+  if (i >= R.rows) return;
+  dirty_row(R, R.luma[0] + fo, R.grad[0] + fo, i, b, R.width, R.removed - b, s_lists[threadIdx.x >> 5]);
 }
 
 // Final index map (original column of every kept column): replay each row's batches on an
@@ -1291,25 +1333,23 @@ void encode_carve_tensor_maps(CarveRun& R) {
                  DpCfg<true>::kStageRows);
 }
 
-int carve_cluster_size(int nruns, int width, int num_sms) {
-  // one DP warp per SM sub-partition: kDpWarps x 128 columns per CTA, at most 8 CTAs
-  int cl = (width + kOwn * kDpWarps - 1) / (kOwn * kDpWarps);
-  return cl < 1 ? 1 : (cl > 8 ? 8 : cl);
-}
-
 int carve_dp_warps(int width, int cl) {
   const int per = ((width + cl - 1) / cl + 15) & ~15;
   return (per + kOwn - 1) / kOwn;
 }
 
-constexpr size_t kSmemBudget = 220 * 1024;
-
-// warps that stage rows for the compaction / gradient phases (4 staged rows each)
-int carve_comp_warps(int pitch) {
-  const size_t RB = (((size_t)pitch + 15) & ~(size_t)15) + 16;
-  size_t n = kSmemBudget / (4 * RB + kWarpScratch);
-  return (int)(n > (size_t)kMaxWarps ? kMaxWarps : n);
+int carve_cluster_size(int nruns, int width, int num_sms) {
+  // one DP warp per SM sub-partition: kDpWarps x 128 columns per CTA, at most 8 CTAs
+  int cl = (width + kOwn * kDpWarps - 1) / (kOwn * kDpWarps);
+  if (const char* e = getenv("SCPL_CARVE_CL")) {  // experiments: fewer CTAs, more DP warps each
+    const int want = atoi(e);
+    if (want >= 1 && want <= 8 && carve_dp_warps(width, want) <= kMaxWarps) cl = want;
+  }
+  return cl < 1 ? 1 : (cl > 8 ? 8 : cl);
 }
+
+
+constexpr size_t kSmemBudget = 220 * 1024;
 
 size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps) {
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
@@ -1323,6 +1363,9 @@ size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps
 }
 
 int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
+
+// pass, compact, gradient, check (+ mean with reaverage_energy)
+int carve_kernels_per_iteration(bool reaverage) { return reaverage ? 5 : 4; }
 
 bool carve_stage_dtab(int rows, int pitch, int cl) {
   return carve_smem_bytes(rows, pitch, true, 0, carve_dp_warps(pitch, cl)) <= kSmemBudget;
@@ -1351,10 +1394,10 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   cfg.numAttrs = 1;
   SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl));
   SCPL_CHECK_LAUNCH();
-  dim3 rgrid(cdiv(rows, kRowWarps), nruns, max_fr);
   const size_t csmem = carve_compact_smem(pitch);
   smem_optin(reinterpret_cast<const void*>(carve_compact_kernel));
-  carve_compact_kernel<<<rgrid, kRowWarps * 32, csmem, st>>>(runs_d);
+  carve_compact_kernel<<<dim3(cdiv(rows, kCompWarps), nruns, max_fr), kCompWarps * 32, csmem, st>>>(runs_d);
+  dim3 rgrid(cdiv(rows, kRowWarps), nruns, max_fr);
   SCPL_CHECK_LAUNCH();
   carve_dirty_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
   SCPL_CHECK_LAUNCH();

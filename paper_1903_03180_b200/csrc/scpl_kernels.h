@@ -101,10 +101,11 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
 void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st);
 // dst/src: device or mapped pinned host memory; bytes rounded up to whole words (4-aligned)
 void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);
-// 4 kernels per executed iteration (pass, compact, gradient, check); iters_d counts them
+// carve_kernels_per_iteration() kernels per executed iteration; iters_d counts them
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
                                  int* iters_d, int max_fr = 1, bool reaverage = false);
 bool carve_stage_dtab(int rows, int pitch, int cl);
+int carve_kernels_per_iteration(bool reaverage);
 int carve_warps(int width, int cl);
 
 void launch_replay(const uint8_t* in, uint8_t* out, int T, int H, int W, int C, const int16_t* idx, int stride,
