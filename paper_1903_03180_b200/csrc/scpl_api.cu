@@ -18,6 +18,8 @@
 #include <cstddef>
 #include <cstring>
 #include <list>
+#include <array>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <set>
@@ -71,6 +73,16 @@ struct scpl_ctx {
   uint8_t* pin = nullptr;  // pinned scratch (pinned_scratch)
   size_t pin_cap = 0;
   std::vector<cudaStream_t> s_carve;  // concurrent run groups
+  // Instantiated carve loops kept for reuse (instantiating / destroying a conditional graph
+  // costs host time on every group): free entries by shape, each with its own run-state
+  // memory that the graph's kernels point at.
+  struct CarveLoop {
+    cudaGraphExec_t ex = nullptr;
+    void* mem = nullptr;  // nruns CarveRuns + the iteration counter
+  };
+  std::multimap<std::array<int, 8>, CarveLoop> loop_pool;
+  std::deque<std::array<int, 8>> loop_order;  // free entries, oldest first (eviction)
+  std::vector<cudaEvent_t> ev_pool[2];         // free events: [0] no timing, [1] timing
 };
 
 namespace {
@@ -256,7 +268,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Planes for `nruns` carves of rows x cols (carve orientation) in one stream-ordered slab.
 struct CarveSet {
-  DBuf mem, runs_d;
+  DBuf mem;
   std::vector<CarveRun> runs;
   int rows = 0, cols = 0, pitch = 0, target = 0, cl = 1;
   size_t planes_bytes = 0;  // luma + gradient planes of every run, at the start of mem
@@ -264,14 +276,28 @@ struct CarveSet {
   bool reaverage = false;
   bool has_uniform = false;  // U holds a uniform map for the first pass (else the mean gradient)
   long long prof[4] = {0, 0, 0, 0};
-  cudaGraphExec_t loop = nullptr;  // device-side iteration loop (alive until the work completes)
+  scpl_ctx* ctx = nullptr;
+  std::array<int, 8> loop_key{};
+  scpl_ctx::CarveLoop loop;        // device-side iteration loop + run states (back to the pool
+                                   // once the work is complete: sets outlive the final sync)
   CarveRun* h_runs = nullptr;      // pinned: run state after the carve (read once the stream is done)
   int* h_iters = nullptr;          // pinned: loop iterations executed
   CarveSet() = default;
   CarveSet(const CarveSet&) = delete;
   CarveSet& operator=(const CarveSet&) = delete;
   ~CarveSet() {
-    if (loop) cudaGraphExecDestroy(loop);
+    if (!loop.mem) return;
+    constexpr size_t kPoolCap = 64;
+    ctx->loop_pool.emplace(loop_key, loop);
+    ctx->loop_order.push_back(loop_key);
+    while (ctx->loop_order.size() > kPoolCap) {
+      auto it = ctx->loop_pool.find(ctx->loop_order.front());
+      ctx->loop_order.pop_front();
+      if (it == ctx->loop_pool.end()) continue;
+      if (it->second.ex) cudaGraphExecDestroy(it->second.ex);
+      cudaFree(it->second.mem);
+      ctx->loop_pool.erase(it);
+    }
   }
 };
 
@@ -347,6 +373,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.alive_pitch = alive_pitch;
     R.cend = reinterpret_cast<int16_t*>(take((size_t)nblk * pitch * 2));
     R.prof = reinterpret_cast<long long*>(take(256));
+    if (!getenv("SCPL_PROF")) R.prof = nullptr;
     R.U = with_U ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
     R.sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
     if (dbg) {
@@ -359,43 +386,61 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
 
 // Carve every run of a set to its target, asynchronously on st: one graph launch runs the
 // iteration loop on the device (pass, compaction, gradient until every run is done), then
-// the index kernel; the final run states land in pinned memory (h_runs / h_iters must hold
-// nruns CarveRuns and one int; they are read by carve_finish once the stream is done).
-void carve_launch(CarveSet& S, CarveRun* h_runs, int* h_iters, cudaStream_t st) {
+// the index kernel; the final run states and the iteration count land in pinned memory
+// (h_state: nruns CarveRuns + 16 bytes; read by carve_finish once the stream is done).
+void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   const int nruns = (int)S.runs.size();
+  CarveRun* h_runs = reinterpret_cast<CarveRun*>(h_state);
   S.h_runs = h_runs;
-  S.h_iters = h_iters;
-  *h_iters = 0;
+  S.h_iters = reinterpret_cast<int*>(h_runs + nruns);
+  *S.h_iters = 0;
   if (nruns == 0) return;
-  for (auto& R : S.runs) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, 256, st));
+  for (auto& R : S.runs) {
+    R.cyc_dp = R.cyc_sel = 0;
+    if (R.prof) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, 256, st));
+  }
+  const bool graph = S.cols > S.target && !host_loops();
+  S.ctx = ctx;
+  S.loop_key = {nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr, (int)S.reaverage + 2 * graph};
+  auto it = ctx->loop_pool.find(S.loop_key);
+  if (it != ctx->loop_pool.end()) {
+    S.loop = it->second;
+    ctx->loop_pool.erase(it);
+    for (auto o = ctx->loop_order.begin(); o != ctx->loop_order.end(); ++o)
+      if (*o == S.loop_key) {
+        ctx->loop_order.erase(o);
+        break;
+      }
+  } else {
+    SCPL_CUDA(cudaMalloc(&S.loop.mem, sizeof(CarveRun) * nruns + 16));
+  }
+  CarveRun* runs_d = reinterpret_cast<CarveRun*>(S.loop.mem);
+  int* iters_d = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(S.loop.mem) + sizeof(CarveRun) * nruns);
   std::memcpy(h_runs, S.runs.data(), sizeof(CarveRun) * nruns);
-  S.runs_d = DBuf(sizeof(CarveRun) * nruns + 16, st);
-  launch_word_copy(S.runs_d.p, h_runs, sizeof(CarveRun) * nruns, st);  // from mapped pinned memory
-  int* iters_d = reinterpret_cast<int*>(S.runs_d.as<uint8_t>() + sizeof(CarveRun) * nruns);
-  SCPL_CUDA(cudaMemsetAsync(iters_d, 0, sizeof(int), st));
+  // run states and the zeroed counter from mapped pinned memory
+  launch_word_copy(runs_d, h_runs, sizeof(CarveRun) * nruns + sizeof(int), st);
   if (S.reaverage && !S.has_uniform)  // first pass on the mean gradient too (pipeline.py:289-290)
-    launch_carve_mean(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
+    launch_carve_mean(runs_d, nruns, S.rows, st);
   if (S.cols > S.target && host_loops()) {  // bursts of 8 iterations, host checks the widths
     int done_iters = 0;
     while (true) {
       for (int k = 0; k < 8; ++k)
-        launch_carve_iteration(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, st, S.max_fr,
-                               S.reaverage);
+        launch_carve_iteration(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, st, S.max_fr, S.reaverage);
       done_iters += 8;
-      launch_word_copy(h_runs, S.runs_d.p, sizeof(CarveRun) * nruns, st);
+      launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns, st);
       SCPL_CUDA(cudaStreamSynchronize(st));
       bool all = true;
       for (int r = 0; r < nruns; ++r) all &= h_runs[r].width <= h_runs[r].target;
       if (all || done_iters > S.cols) break;
     }
-  } else if (S.cols > S.target) {
-    S.loop = build_carve_loop(S.runs_d.as<CarveRun>(), nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1,
-                              iters_d, S.max_fr, S.reaverage);
-    SCPL_CUDA(cudaGraphLaunch(S.loop, st));
+  } else if (graph) {
+    if (!S.loop.ex)
+      S.loop.ex = build_carve_loop(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d,
+                                   S.max_fr, S.reaverage);
+    SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
-  launch_carve_index(S.runs_d.as<CarveRun>(), nruns, S.rows, st);
-  launch_word_copy(h_runs, S.runs_d.p, sizeof(CarveRun) * nruns, st);
-  launch_word_copy(h_iters, iters_d, sizeof(int), st);
+  launch_carve_index(runs_d, nruns, S.rows, st);
+  launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns + sizeof(int), st);  // states + counter
 }
 
 // after the stream is done: run states back into S.runs, launch accounting, profile
@@ -408,20 +453,23 @@ void carve_finish(CarveSet& S) {
     if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;
   for (auto& R : S.runs) {
-    long long c[17];
-    SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
-    if (getenv("SCPL_PROF"))
+    long long c[17] = {};
+    if (R.prof) {
+      SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
+      c[0] = R.cyc_dp;
+      c[1] = R.cyc_sel;
       fprintf(stderr,
               "carve prof: iters %d rows %d | dp %lld sel %lld | xwait %lld ringwait %lld rows %lld publish %lld"
               " [bar1 %lld stores %lld bar2 %lld] store_pw %lld | sel: labels %lld min %lld cand %lld trunc %lld"
               " trace %lld (x CTAs)\n",
               R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11], c[12], c[13], c[14],
               c[15], c[16]);
-    long long tot = c[0] + c[1];
+    }
+    long long tot = R.cyc_dp + R.cyc_sel;
     if (tot > best) {
       best = tot;
-      S.prof[0] = c[0];
-      S.prof[1] = c[1];
+      S.prof[0] = R.cyc_dp;
+      S.prof[1] = R.cyc_sel;
       S.prof[2] = R.iters;  // passes of that run
       S.prof[3] = 0;
     }
@@ -431,7 +479,7 @@ void carve_finish(CarveSet& S) {
 void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
   const int nruns = (int)S.runs.size();
   uint8_t* pin = pinned_scratch(ctx, sizeof(CarveRun) * (size_t)std::max(nruns, 1) + 64);
-  carve_launch(S, reinterpret_cast<CarveRun*>(pin + 64), reinterpret_cast<int*>(pin), st);
+  carve_launch(ctx, S, pin, st);
   SCPL_CUDA(cudaStreamSynchronize(st));
   carve_finish(S);
 }
@@ -475,6 +523,12 @@ void scpl_destroy(scpl_ctx* ctx) {
   if (ctx->pin) cudaFreeHost(ctx->pin);
   for (cudaStream_t x : ctx->s_carve) cudaStreamDestroy(x);
   for (auto& kv : ctx->scan_graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : ctx->loop_pool) {
+    if (kv.second.ex) cudaGraphExecDestroy(kv.second.ex);
+    cudaFree(kv.second.mem);
+  }
+  for (auto& pool : ctx->ev_pool)
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
   if (ctx->scan) cudaFree(ctx->scan);
   if (ctx->phi_d) cudaFree(ctx->phi_d);
   for (cudaStream_t x : {ctx->s_h2d, ctx->s_codes, ctx->s_d2h, ctx->s_scan})
@@ -606,6 +660,14 @@ struct Group {
 void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* frames_host, int T, int h, int w,
                    int channels, const scpl_video_params& P, uint8_t* out_dev, uint8_t* out_host,
                    scpl_video_result* result, cudaStream_t st) {
+  const bool timeline = getenv("SCPL_TIMELINE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;  // (label, timing event)
+  const auto t_host0 = std::chrono::steady_clock::now();
+  auto hmark = [&](const std::string& label) {
+    if (!timeline) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    fprintf(stderr, "host %8.3f ms  %s\n", ms, label.c_str());
+  };
   SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
   SCPL_ARG(h >= 3 && w >= 3, "frame too small to carve");
   SCPL_ARG(P.target_width >= 1 && P.target_width <= w, "target width out of range");
@@ -664,22 +726,32 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     return q;
   };
 
-  std::vector<cudaEvent_t> events;
+  // events come from (and go back to) the context's pools: every use is complete once the
+  // call returns (final synchronize, or the drain guard on the error path)
+  std::vector<std::pair<cudaEvent_t, bool>> events;
   struct EvGuard {
-    std::vector<cudaEvent_t>& e;
+    scpl_ctx* ctx;
+    std::vector<std::pair<cudaEvent_t, bool>>& e;
     ~EvGuard() {
-      for (auto x : e) cudaEventDestroy(x);
+      for (auto& x : e) ctx->ev_pool[x.second].push_back(x.first);
     }
-  } evg{events};
+  } evg{ctx, events};
   auto new_event = [&](bool timing) {
     cudaEvent_t e;
-    SCPL_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
-    events.push_back(e);
+    auto& pool = ctx->ev_pool[timing];
+    if (!pool.empty()) {
+      e = pool.back();
+      pool.pop_back();
+    } else {
+      SCPL_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    }
+    events.push_back({e, timing});
     return e;
   };
   cudaEvent_t ev_start = new_event(true), ev_codes = new_event(true), ev_scan = new_event(true),
               ev_end = new_event(true);
   SCPL_CUDA(cudaEventRecord(ev_start, st));
+  hmark("start recorded");
 
   // buffers (stream-ordered on st; every other stream waits for ev_alloc)
   DBuf frames_buf, codes, out_buf;
@@ -703,14 +775,6 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     scan_start(ctx, scan, codes.as<uint16_t>(), T, h, w, P, st);
   }
   std::list<Group> groups;
-  const bool timeline = getenv("SCPL_TIMELINE") != nullptr;
-  std::vector<std::pair<std::string, cudaEvent_t>> marks;  // (label, timing event)
-  const auto t_host0 = std::chrono::steady_clock::now();
-  auto hmark = [&](const std::string& label) {
-    if (!timeline) return;
-    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
-    fprintf(stderr, "host %8.3f ms  %s\n", ms, label.c_str());
-  };
   auto mark = [&](const std::string& label, cudaStream_t sm) {
     if (!timeline) return;
     cudaEvent_t e = new_event(true);
@@ -831,8 +895,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       }
       mark("group " + std::to_string(groups.size() - 1) + " setup done", gs);
       hmark("group carve_launch");
-      carve_launch(S, reinterpret_cast<CarveRun*>(pin_take(sizeof(CarveRun) * nr)),
-                   reinterpret_cast<int*>(pin_take(sizeof(int))), gs);
+      carve_launch(ctx, S, pin_take(sizeof(CarveRun) * nr + 16), gs);
       hmark("group replay");
       mark("group " + std::to_string(groups.size() - 1) + " carve done", gs);
       const int nH = height ? th : curH, nW = height ? curW : tw;
@@ -892,8 +955,10 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     SCPL_CUDA(cudaStreamWaitEvent(st, e, 0));
   }
   SCPL_CUDA(cudaEventRecord(ev_end, st));
+  hmark("all queued");
   SCPL_CUDA(cudaStreamSynchronize(st));
   drain.armed = false;
+  hmark("synchronized");
 
   // 4. results
   if (buffered) scan_finish(scan, nchunk);
@@ -921,6 +986,12 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[0], ev_start, ev_codes));
   SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[1], ev_codes, ev_scan));
   SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[2], ev_scan, ev_end));
+  if (timeline) {
+    float ms = 0.f;
+    SCPL_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_end));
+    fprintf(stderr, "timeline %8.3f ms  end\n", ms);
+  }
+  hmark("results");
 }
 
 }  // namespace
@@ -940,7 +1011,11 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
                         const scpl_video_params* params, uint8_t* out, scpl_video_result* result, void* stream) {
   return guarded(ctx, [&] {
     SCPL_ARG(params != nullptr && result != nullptr, "params/result is NULL");
+    const auto t0 = std::chrono::steady_clock::now();
     retarget_core(ctx, frames, nullptr, T, h, w, channels, *params, out, nullptr, result, (cudaStream_t)stream);
+    if (getenv("SCPL_TIMELINE"))
+      fprintf(stderr, "host %8.3f ms  returned (after cleanup)\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   });
 }
 

@@ -1098,11 +1098,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     Rg.width = w - b;
     Rg.iters = iters + 1;
     Rg.removed = removed + b;
-    if (R.prof) {
-      R.prof[0] += t_dp;
-      R.prof[1] += clock64() - tp;
+    Rg.cyc_dp += t_dp;
+    Rg.cyc_sel += clock64() - tp;
+    if (R.prof)
       for (int k = 0; k < 8; ++k) R.prof[4 + k] += dprof[k];
-    }
   }
 }
 

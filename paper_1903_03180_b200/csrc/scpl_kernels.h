@@ -75,7 +75,7 @@ struct alignas(64) CarveRun {
   uint32_t* alive;      // rows x alive_pitch bitmask of surviving original columns
   int alive_pitch;
   int16_t* cend;        // nblk x pitch scratch: block-end columns of the selected seams
-  long long* prof;      // optional: SM cycles in dp / select / compact / gradient
+  long long* prof;      // optional (SCPL_PROF): detailed phase cycles
   uint32_t* pw;         // nblk x pitch path words at block-end rows
   int8_t* delta;        // nblk x pitch landing deltas
   double* lastce;       // pitch
@@ -89,6 +89,7 @@ struct alignas(64) CarveRun {
   int iters;            // DP passes done
   int removed;          // seams removed so far (offset of the next batch in the log)
   int b;                // size of the batch selected by the latest pass (0: none)
+  long long cyc_dp, cyc_sel;  // SM cycles of the DP and select/trace phases, summed over passes
 };
 // planes of frame f of the run's stack (f > 0 only with reaverage_energy)
 void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes,
