@@ -137,6 +137,30 @@ CLIP_CASES = {
 }
 
 
+# Wider / taller clips than the reference finishes quickly, checked against the oracle: every
+# carve cluster size (1..8 CTAs: widths up to the 4096-column limit), the staged and unstaged
+# landing-delta table (tall planes), height carving of tall frames, raw / scpl / reaverage.
+# (h, w, t, config)
+SIZE_CASES = [
+    (150, 600, 5, dict(target_width=430)),
+    (120, 1100, 4, dict(target_width=800)),
+    (100, 2100, 4, dict(target_width=1500)),
+    (80, 3300, 3, dict(target_width=2700)),
+    (64, 4096, 3, dict(target_width=3000)),
+    (1500, 40, 3, dict(target_width=29)),
+    (700, 24, 4, dict(target_height=520)),
+    (90, 2600, 4, dict(target_width=2000, target_height=70)),
+    (100, 1100, 4, dict(target_width=1000, mode="raw")),
+    (100, 1100, 4, dict(target_width=900, mode="scpl")),
+    (96, 1300, 6, dict(target_width=1000, reaverage_energy=True)),
+]
+
+
+def size_clip(i: int):
+    h, w, t, cfg = SIZE_CASES[i]
+    return small_clip(seed=100 + i, t=t, h=h, w=w, rects=6), dict(mode="buffered", **cfg) if "mode" not in cfg else cfg
+
+
 # ------------------------------------------------------------------ media / jitter
 def media_streams():
     """(name, bytes) PNM streams exercising the byte grammar and its errors (media.py:139-223)."""

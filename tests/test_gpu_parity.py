@@ -207,6 +207,26 @@ def test_pipeline_small_clips_golden(P, small):
         assert [sha(f) for f in out] == g["frames"], name
 
 
+@pytest.mark.parametrize("i", range(len(cases.SIZE_CASES)))
+def test_size_cases_vs_oracle(P, i):
+    """Every carve cluster size and plane shape class against the oracle (host frames and a CUDA clip)."""
+    import torch
+    from oracle import scpl_oracle as O
+    frames, cfg = cases.size_clip(i)
+    ref = O.retarget_video(frames, **cfg)
+    out, m = P.retarget_video(frames, P.RetargetConfig(**cfg))
+    assert m.dp_passes == ref.dp_passes
+    if cfg["mode"] == "buffered":
+        assert [tuple(r) for r in m.runs] == [tuple(r) for r in ref.runs]
+    assert len(out) == len(ref.frames)
+    for a, b in zip(out, ref.frames):
+        assert np.array_equal(a, b)
+    clip = torch.from_numpy(np.stack(frames)).cuda()
+    dev, m2 = P.retarget_video_tensor(clip, P.RetargetConfig(**cfg))
+    assert m2.dp_passes == ref.dp_passes
+    assert np.array_equal(dev.cpu().numpy(), np.stack(ref.frames))
+
+
 def test_pipeline_errors(P):
     with pytest.raises(ValueError, match="exceeds"):
         P.retarget_image(np.zeros((8, 8), np.uint8), P.RetargetConfig(target_width=9))
