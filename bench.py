@@ -8,9 +8,11 @@ width -25% workload.  Prints ONE JSON line on rank 0.
   value     frames/s with the clip resident in HBM (device-timed, CUDA events, max over ranks)
   e2e       frames/s through the public API with pinned HOST buffers: H2D of the clip, the
             carve, D2H of the output, every step
-  roofline  algorithmic HBM bytes per frame B = 6*H*W + 3*H'*W' (the input is
-            read by the energy/statistics pass and by the replay, the output written once)
-            times frames per step / step time, against the measured copy bandwidth
+  roofline  the dominant kernel (carve_pass_kernel): algorithmic bytes per launch / mean launch
+            duration, against the measured copy bandwidth (see pass_roofline)
+  step_roofline  the whole step: algorithmic HBM bytes per frame B = 6*H*W + 3*H'*W' (SURVEY.md
+            §8d: the input is read by the energy/statistics pass and by the replay, the output
+            written once) times frames per step / step time
   cpu_baseline  the CPU oracle port (numpy restatement of the reference) on a bounded sample
 
 Multi-GPU (torchrun): each rank retargets its own clip (C2 recipe, seed = rank) -- clips are
@@ -60,74 +62,141 @@ def alg_bytes_per_frame(h, w, th, tw, c=3):
     return 2 * c * h * w + c * th * tw
 
 
-def dominant_kernel(ph, m, H, W, tw, th):
-    """carve_pass_kernel (the DP + select + trace pass, ~70% of kernel time in the committed
-    launch list): average launch duration from the slowest run's device-clock counters, and
-    its algorithmic bytes -- per run and pass the gradient plane read once (rows x width B),
+def pass_roofline(ph, H, W, tw, peak, peak_src):
+    """Roofline of the dominant kernel, carve_pass_kernel (DP + select + trace of every run of a
+    group, one cluster per run; ~70% of kernel time in the committed launch list).
+
+    Per run and pass the algorithmic bytes are the gradient plane read once (rows x width B) and
     the 16-row path words + landing deltas written and read back (2 x 5 B per column per 16
-    rows).  The kernel is bound by the DP's row-to-row dependency, not by HBM."""
+    rows); a launch carries dp_passes / launches runs.  The launch duration is the slowest
+    cluster's SM-clock cycles (clock64 in the kernel) -- the passes run inside conditional
+    graphs on the library's own streams, where events cannot bracket a single kernel.
+    traffic: DRAM bytes per launch from the committed ncu --set full capture, scaled to the
+    same runs per launch."""
+    launches = ph.get("pass_launches") or 0
+    launch_ms = ph.get("pass_launch_ms") or 0.0
+    if not launches or not launch_ms:
+        return None
+    runs_per_launch = ph["dp_passes"] / launches
+    cols = 0.5 * (W + tw)  # mean width over the passes
+    per_run = H * cols * (1.0 + 2 * 5 / 16)
+    alg = per_run * runs_per_launch
+    achieved = alg / (launch_ms / 1e3) / 1e9
+    traffic = None
     try:
+        k = json.load(open(os.path.join(ROOT, "profiles", "kernel_shares.json")))
+        d = k.get("_carve_pass_dram_bytes_per_launch") or {}
+        if d.get("read") is not None:
+            traffic = (d["read"] + d.get("write", 0)) / d["runs_per_launch"] * runs_per_launch
+        share = k.get("carve_pass_kernel")
+    except Exception:
         share = None
-        sp = os.path.join(ROOT, "profiles", "kernel_shares.json")
-        if os.path.exists(sp):
-            share = json.load(open(sp)).get("carve_pass_kernel")
-        iters = max(1, max(m.dp_passes // max(1, len(m.runs)), 1))
-        cyc = (ph.get("carve_dp_Mcyc", 0.0) + ph.get("carve_select_Mcyc", 0.0)) * 1e6
-        # slowest run: iterations ~ dp_passes of that run; approximate with the max over runs
-        # via its own counters (cycles / SM clock of 1965 MHz)
-        n_iter = ph.get("slowest_run_iters") or iters
-        avg_us = cyc / max(n_iter, 1) / 1965.0
-        rows, cols = H, 0.5 * (W + tw)  # mean width over the passes
-        per_run = rows * cols * (1.0 + 2 * 5 / 16)
-        return {"name": "carve_pass_kernel", "avg_launch_us_device_clock": avg_us,
-                "alg_bytes_per_run_pass": per_run, "share_of_kernel_time": share,
-                "bound": "latency: one dependent DP row after another (min-plus recurrence)"}
-    except Exception as e:  # pragma: no cover
-        return {"name": "carve_pass_kernel", "error": str(e)}
+    return {"kernel": "carve_pass_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "alg_bytes_per_launch": alg, "runs_per_launch": runs_per_launch, "avg_launch_us": launch_ms * 1e3,
+            "launches_per_step": launches, "share_of_kernel_time": share,
+            "timing": "in-kernel SM clock (clock64), slowest cluster per launch, over the timed steps",
+            "limit": "latency: one dependent DP row after another (min-plus recurrence), not HBM"}
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled every 10 ms during the timed region (NVML; the
+    nvidia-smi CLI polled at 100 ms as a fallback)."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.sm, self.mx, self.reasons = gpu, [], [], set()
+        self.proc, self.stop, self.thread, self.nv = None, threading.Event(), None, None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+
+        try:  # the NVML device behind this CUDA ordinal (CUDA_VISIBLE_DEVICES may reorder)
+            import torch
+            p = torch.cuda.get_device_properties(self.gpu)
+            want = (int(p.pci_domain_id), int(p.pci_bus_id), int(p.pci_device_id))
+            for k in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(k)
+                q = pynvml.nvmlDeviceGetPciInfo(h)
+                if (int(q.domain), int(q.bus), int(q.device)) == want:
+                    return pynvml, h
+        except Exception:
+            pass
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
 
     def __enter__(self):
+        try:
+            if os.environ.get("SCPL_BENCH_CLOCKS") == "off":
+                return self
+            if os.environ.get("SCPL_BENCH_CLOCKS") == "smi":
+                raise RuntimeError("nvidia-smi sampler requested")
+            self.nv, h = self._handle()
+            self.mx.append(float(self.nv.nvmlDeviceGetMaxClockInfo(h, self.nv.NVML_CLOCK_SM)))
+            self.thread = threading.Thread(target=self._poll_nvml, args=(h,), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
+            self.thread = threading.Thread(target=self._read_smi, daemon=True)
+            self.thread.start()
         except FileNotFoundError:
             self.proc = None
         return self
 
-    def _read(self):
+    def _poll_nvml(self, h):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, const in self.REASONS:
+                    if r & getattr(nv, const):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self.stop.wait(0.01)
+
+    def _read_smi(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                if parts[1].replace(".", "").isdigit():
+                    self.sm.append(float(parts[1]))
+                if parts[2].replace(".", "").isdigit():
+                    self.mx.append(float(parts[2]))
+                for (name, _), v in zip(self.REASONS, parts[4:8]):
+                    if v.lower() == "active":
+                        self.reasons.add(name)
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
             self.proc.wait()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
-        loaded = [s for s in sm if s > 0.5 * max(mx or [1])] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        top = max(self.mx) if self.mx else max(self.sm)
+        loaded = [s for s in self.sm if s > 0.5 * top] or self.sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": top, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml" if self.nv else "nvidia-smi"}
 
 
 def dist_setup():
@@ -183,6 +252,13 @@ def cpu_sample(name: str, workers: int, frames_per_worker: int, pool=None):
     return max(pool.map(_oracle_window, jobs))
 
 
+def workload(name: str) -> str:
+    """The config's workload name, identical on both arms."""
+    spec, tw, th = CONFIGS[name]
+    return (f"{name}: {spec.frames}x{spec.height}x{spec.width}x3 -> {th or spec.height}x{tw or spec.width}, "
+            f"buffered SCPL, alpha 0.2, max_len 64, wm/wg 0.6/0.4")
+
+
 def run_reference(a, world, rank):
     """--impl reference: the oracle port on the host cores, rank 0 only."""
     if rank != 0:
@@ -205,7 +281,8 @@ def run_reference(a, world, rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8/f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{a.config} sample", "frames_per_step": workers * fpw},
+        "config": {"workload": workload(a.config), "frames_per_step": workers * fpw,
+                   "sample": f"{workers} windows x {fpw} frames of the clip per step"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -325,16 +402,17 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8/f64", "data": "synthetic",
-        "config": {"workload": f"{name}: {T}x{H}x{W}x{C} -> {th}x{tw}, buffered SCPL, alpha 0.2, max_len 64, "
-                               f"wm/wg 0.6/0.4", "frames_per_step": T, "runs": len(m.runs),
+        "config": {"workload": workload(name) if a.frames is None else f"{name} (first {T} frames)",
+                   "frames_per_step": T, "runs": len(m.runs),
                    "dp_passes": m.dp_passes, "l2": "inputs (1.87 GB/clip) larger than L2",
                    "parallelism": f"clip-per-GPU x{world}"},
         "e2e": e2e,
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "scope": "whole step (all kernels); B = 6HW + 3H'W' bytes per frame",
-                     "peak_source": peak_src, "frac_of_nominal_8TBs": achieved / 8000.0},
-        "dominant_kernel": dominant_kernel(ph, m, H, W, tw, th),
+        "roofline": pass_roofline(dict(ph, dp_passes=m.dp_passes), H, W, tw, peak, peak_src),
+        "step_roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                          "frac": achieved / peak, "traffic": traffic,
+                          "scope": "whole step (all kernels); B = 6HW + 3H'W' bytes per frame",
+                          "peak_source": peak_src},
         "phases_ms": ph,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,

@@ -113,9 +113,11 @@ typedef struct {
   int* run_start;      /* host, capacity T (nullable) */
   int* run_len;        /* host, capacity T (nullable) */
   float phase_ms[4];   /* device ms: start -> codes done, -> scan done, scan done -> all carved and
-                          replayed (groups overlap the scan), unused */
-  long long carve_cycles[4]; /* slowest run (SCPL_PROF builds fill the cycle counters): dp cycles,
-                                select cycles, its pass count, unused */
+                          replayed (groups overlap the scan), mean carve-pass launch duration (SM
+                          clock cycles of the slowest cluster / base clock rate) */
+  long long carve_cycles[4]; /* slowest run: dp cycles, select cycles, its pass count; then the
+                                number of carve-pass kernel launches (dp_passes / launches = runs
+                                per launch) */
   int carve_cluster;   /* CTAs per run cluster used by the carve */
 } scpl_video_result;
 

@@ -61,6 +61,9 @@ struct PwPlan {
 struct scpl_ctx {
   int device = 0;
   int num_sms = 148;
+  int clock_khz = 0;  // base SM clock (queried once: the query costs milliseconds of host time)
+  int prio_lo = 0, prio_hi = 0;
+  bool prio_known = false;
   cudaStream_t s_h2d = nullptr, s_codes = nullptr, s_d2h = nullptr, s_scan = nullptr;  // pipeline streams
   double* h_asde = nullptr;  // pinned
   int h_asde_cap = 0;
@@ -503,6 +506,7 @@ int scpl_create(int device, scpl_ctx** out) {
     auto* c = new scpl_ctx();
     c->device = device;
     SCPL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    SCPL_CUDA(cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, device));
     // keep freed workspace in the stream-ordered pool (no unmap/remap of GBs per clip)
     cudaMemPool_t pool;
     SCPL_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -691,8 +695,11 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   // the critical path, the early ones have slack, and the carve passes compete for whole SMs.
   // Levels: prio_hi (scan) .. prio_lo; carve groups use prio_hi+1 .. prio_lo (or all if the
   // range is tiny), kStreamsPerLevel streams each.
-  int prio_lo = 0, prio_hi = 0;
-  SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  if (!ctx->prio_known) {
+    SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&ctx->prio_lo, &ctx->prio_hi));
+    ctx->prio_known = true;
+  }
+  const int prio_lo = ctx->prio_lo, prio_hi = ctx->prio_hi;
   for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_d2h})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
   for (cudaStream_t* x : {&ctx->s_codes, &ctx->s_scan})
@@ -968,16 +975,27 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       result->run_start[r] = runs[r].first;
       result->run_len[r] = runs[r].second;
     }
-  long dp = 0;
+  long dp = 0, pass_launches = 0;
+  long long pass_cyc = 0;
   for (Group& G : groups)
     for (CarveSet& S : G.sets) {
       carve_finish(S);
-      for (auto& R : S.runs) dp += R.iters;
+      long long slow = 0;
+      int launches = 0;
+      for (auto& R : S.runs) {
+        dp += R.iters;
+        slow = std::max(slow, R.cyc_dp + R.cyc_sel);
+        launches = std::max(launches, R.iters);
+      }
+      pass_cyc += slow;  // a launch lasts as long as its slowest cluster
+      pass_launches += launches;
       if (S.prof[0] + S.prof[1] > result->carve_cycles[0] + result->carve_cycles[1])
-        for (int k = 0; k < 4; ++k) result->carve_cycles[k] = S.prof[k];
+        for (int k = 0; k < 3; ++k) result->carve_cycles[k] = S.prof[k];
       result->carve_cluster = S.cl;
     }
   result->dp_passes = dp;
+  result->carve_cycles[3] = pass_launches;
+  if (pass_launches > 0) result->phase_ms[3] = (float)((double)pass_cyc / pass_launches / std::max(ctx->clock_khz, 1));
   for (auto& m : marks) {
     float ms = 0.f;
     SCPL_CUDA(cudaEventElapsedTime(&ms, ev_start, m.second));

@@ -132,6 +132,8 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
     last_phase_ms.update({f"carve_{k}_Mcyc": c / 1e6 for k, c in zip(("dp", "select"), res.carve_cycles[:2])})
     last_phase_ms["slowest_run_iters"] = int(res.carve_cycles[2])
     last_phase_ms["carve_cluster"] = res.carve_cluster
+    last_phase_ms["pass_launches"] = int(res.carve_cycles[3])
+    last_phase_ms["pass_launch_ms"] = float(res.phase_ms[3])
     return out, int(res.dp_passes), runs
 
 
