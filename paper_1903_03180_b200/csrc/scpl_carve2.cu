@@ -168,6 +168,9 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -192,6 +195,10 @@ struct Val<true> {
   static __device__ __forceinline__ T add(T a, T b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ double to_d(T v) { return v; }
 };
+
+// A DP warp's block-end staging (choice / path words, dir sums, then a 4-word header holding
+// the block index and row count), double buffered when a helper warp stores it.
+constexpr int kPwStageWords = 2 * kWin + 4;
 
 struct Geo {  // per-pass column ownership
   int w;          // current width
@@ -356,10 +363,47 @@ __device__ __forceinline__ uint32_t halo_bytes_for(int w, int CL, uint32_t rank,
   return bytes;
 }
 
+// Global stores of one staged block end (the lane-contiguous words transposed through the
+// staging row so the stores coalesce): owned columns' words and landing deltas.
+template <bool F64>
+__device__ __forceinline__ void store_block_end(const CarveRun& R, const Geo& g, const uint32_t* stg, int pbi,
+                                                int nrb) {
+  const int lane = threadIdx.x & 31;
+  uint32_t* gpw = R.pw + (long)pbi * R.pitch + g.win_lo;
+  int8_t* gdl = R.delta + (long)pbi * R.pitch + g.win_lo;
+#pragma unroll
+  for (int k = 0; k < kC; ++k) {
+    const int c = lane + 32 * k;
+    const int j = g.win_lo + c;
+    if (j >= g.own_lo && j < g.own_hi) {  // (transposed column: not this lane's own[])
+      const uint32_t word = stg[c];
+      gpw[c] = word;
+      const int sumdir = F64 ? __popc(word & 0x55555555u) + 2 * __popc(word & 0xAAAAAAAAu) : (int)stg[kWin + c];
+      gdl[c] = (int8_t)(sumdir - nrb);
+    }
+  }
+}
+
+// Helper warp of one DP warp: performs its block-end global stores (the DP warp only fills a
+// staging buffer and moves on).  hbar: full[2] (32 DP-lane arrivals), empty[2] (32 helper-
+// lane arrivals); a header of ~0 ends the pass.
+template <bool F64>
+__device__ void pw_helper(const CarveRun& R, const Geo& g, const uint32_t* stage, uint64_t* hbar) {
+  for (uint32_t n = 0;; ++n) {
+    mbar_wait(&hbar[n & 1], (n >> 1) & 1);
+    const uint32_t* stg = stage + (n & 1) * kPwStageWords;
+    const uint32_t hdr = stg[2 * kWin];
+    if (hdr == 0xffffffffu) break;
+    store_block_end<F64>(R, g, stg, (int)hdr, (int)stg[2 * kWin + 1]);
+    mbar_arrive(&hbar[2 + (n & 1)]);
+  }
+}
+
 template <bool F64, bool EDGE>
 __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
                         uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
-                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage) {
+                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage,
+                        uint64_t* hbar) {
   using V = Val<F64>;
   using T = typename V::T;
   constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
@@ -367,8 +411,6 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   static_assert(kXRows % RS == 0 && kBlockRows % RS == 0 || RS == kXRows, "stage layout");
   const int lane = threadIdx.x & 31;
   const int rows = R.rows, w = g.w, pitch = R.pitch;
-  uint32_t* const pw_g = R.pw;
-  int8_t* const delta_g = R.delta;
   const bool active = g.own_lo < g.own_hi;
   const int j0 = g.win_lo + lane * kC;
   const bool nb_mode = per_cta >= kXRows;
@@ -416,28 +458,32 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   // are transposed through this warp's staging row so the global stores coalesce
   // block-end path words and landing deltas of the owned columns: the lane-contiguous words
   // are transposed through this warp's staging row so the global stores coalesce
+  uint32_t hu = 0;  // staged block ends handed to the helper warp
+  auto next_stage = [&]() -> uint32_t* {  // helper mode: a free staging buffer
+    uint32_t* stg = pw_stage + (hu & 1) * kPwStageWords;
+    if (hu >= 2) mbar_wait(&hbar[2 + (hu & 1)], ((hu >> 1) - 1) & 1);
+    return stg;
+  };
   auto store_pw = [&](int pbi, int nrb) {
     [[maybe_unused]] long long t7 = DP_CLOCK();
+    uint32_t* stg = hbar ? next_stage() : pw_stage;
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < kC; k += 2) {
-      *reinterpret_cast<uint2*>(&pw_stage[lane * kC + k]) = make_uint2(pw[k], pw[k + 1]);
+      *reinterpret_cast<uint2*>(&stg[lane * kC + k]) = make_uint2(pw[k], pw[k + 1]);
       if constexpr (!F64)
-        *reinterpret_cast<int2*>(&pw_stage[kWin + lane * kC + k]) = make_int2(ce[k] & 63, ce[k + 1] & 63);
+        *reinterpret_cast<int2*>(&stg[kWin + lane * kC + k]) = make_int2(ce[k] & 63, ce[k + 1] & 63);
     }
-    __syncwarp();
-    uint32_t* gpw = pw_g + (long)pbi * pitch + g.win_lo;
-    int8_t* gdl = delta_g + (long)pbi * pitch + g.win_lo;
-#pragma unroll
-    for (int k = 0; k < kC; ++k) {
-      const int c = lane + 32 * k;
-      const int j = g.win_lo + c;
-      if (j >= g.own_lo && j < g.own_hi) {  // (transposed column: not this lane's own[])
-        const uint32_t word = pw_stage[c];
-        gpw[c] = word;
-        const int sumdir = F64 ? __popc(word & 0x55555555u) + 2 * __popc(word & 0xAAAAAAAAu) : (int)pw_stage[kWin + c];
-        gdl[c] = (int8_t)(sumdir - nrb);
+    if (hbar) {
+      if (lane == 0) {
+        stg[2 * kWin] = (uint32_t)pbi;
+        stg[2 * kWin + 1] = (uint32_t)nrb;
       }
+      mbar_arrive(&hbar[hu & 1]);
+      ++hu;
+    } else {
+      __syncwarp();
+      store_block_end<F64>(R, g, stg, pbi, nrb);
     }
     DP_PROF(7, DP_CLOCK() - t7);
   };
@@ -567,6 +613,11 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
     ++xc;
     if (nb_mode) ++xm;
   }
+  if (hbar) {  // end of the pass for the helper warp
+    uint32_t* stg = next_stage();
+    if (lane == 0) stg[2 * kWin] = 0xffffffffu;
+    mbar_arrive(&hbar[hu & 1]);
+  }
   if (nb_mode && nx > 0) {  // the last exchange must be complete before the smem is reused
     const uint32_t e = xm - 1;
     mbar_wait(&xbar[e & 1], (e >> 1) & 1);
@@ -589,14 +640,15 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
 template <bool F64>
 __device__ void dp_pass(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
                         uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
-                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage) {
+                        uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage,
+                        uint64_t* hbar) {
   // windows lie inside [0, w) unless the plane is narrower than one window
   if (g.w < kWin)
     dp_rows<F64, true>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
-                       pw_stage);
+                       pw_stage, hbar);
   else
     dp_rows<F64, false>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
-                        pw_stage);
+                        pw_stage, hbar);
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -839,6 +891,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   __shared__ __align__(8) uint64_t s_xbar[2];
   __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
   __shared__ __align__(8) uint64_t s_dbar;  // delta-table staging (select phase)
+  __shared__ __align__(8) uint64_t s_hbar[kMaxWarps * 4];  // DP warp -> helper warp staging
   const uint32_t rank = cluster_rank();
   CarveRun& Rg = runs[blockIdx.x / CL];
   const CarveRun& R = Rg;  // fields read in place; the state fields are copied below
@@ -865,33 +918,50 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     if (rows > 1 && per >= kXRows)  // the pass's first exchange, announced before it can start
       mbar_arrive_tx(&s_xbar[0], halo_bytes_for(w, CL, rank, fp64 ? 8 : 4));
   }
-  if (lane == 0)
+  if (lane == 0) {
     for (int k = 0; k < 6; ++k) mbar_init(&s_rbar[wid * 6 + k], 1);
-  if (lane == 0) fence_mbar_init();
+    for (int k = 0; k < 4; ++k) mbar_init(&s_hbar[wid * 4 + k], 32);
+    fence_mbar_init();
+  }
   uint32_t xc = 0, xm = 0, rph = 0;
   cluster_sync();
 
   // ---------------- 1. DP
   {
-    Geo g;
-    g.w = w;
-    g.cta_lo = min(w, (int)rank * per);
-    g.cta_hi = min(w, g.cta_lo + per);
-    g.own_lo = g.cta_lo + wid * kOwn;
-    g.own_hi = min(g.cta_hi, g.own_lo + kOwn);
-    // window: owned +- 32, shifted inside [0, w) when the plane is wide enough, so that a
-    // window edge is either an image border (exact +inf) or a decaying halo -- no masks
-    g.win_lo = w >= kWin ? min(max(g.own_lo - kXRows, 0), w - kWin) : g.own_lo - kXRows;
+    auto geo = [&](int dw) {
+      Geo g;
+      g.w = w;
+      g.cta_lo = min(w, (int)rank * per);
+      g.cta_hi = min(w, g.cta_lo + per);
+      g.own_lo = g.cta_lo + dw * kOwn;
+      g.own_hi = min(g.cta_hi, g.own_lo + kOwn);
+      // window: owned +- 32, shifted inside [0, w) when the plane is wide enough, so that a
+      // window edge is either an image border (exact +inf) or a decaying halo -- no masks
+      g.win_lo = w >= kWin ? min(max(g.own_lo - kXRows, 0), w - kWin) : g.own_lo - kXRows;
+      return g;
+    };
     const bool in_dp = wid < ndp || per < kXRows;
+    // helper warps: the block-end global stores of DP warp (wid - ndp), off its critical path
+    const bool helpers = per >= kXRows && 2 * ndp <= kMaxWarps;
+    uint8_t* ring = smem + 2 * sizeof(double) * (size_t)pitch;
+    uint32_t* pw_stage0 = reinterpret_cast<uint32_t*>(ring + (size_t)ndp * dp_ring_bytes<true>());
     if (in_dp) {
-      uint8_t* ring = smem + 2 * sizeof(double) * (size_t)pitch;
-      uint32_t* pw_stage = reinterpret_cast<uint32_t*>(ring + (size_t)ndp * dp_ring_bytes<true>()) + wid * 2 * kWin;
+      const Geo g = geo(wid);
+      uint32_t* pw_stage = pw_stage0 + wid * 2 * kPwStageWords;
+      uint64_t* hb = helpers ? &s_hbar[wid * 4] : nullptr;
       if (fp64)
         dp_pass<true>(R, Rg, g, plane, reinterpret_cast<double*>(smem), CL, rank, per, s_xbar, xc, xm,
-                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage);
+                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
       else
         dp_pass<false>(R, Rg, g, plane, reinterpret_cast<int*>(smem), CL, rank, per, s_xbar, xc, xm,
-                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage);
+                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
+    } else if (helpers && wid < 2 * ndp) {
+      const int dw = wid - ndp;
+      const uint32_t* stage = pw_stage0 + dw * 2 * kPwStageWords;
+      if (fp64)
+        pw_helper<true>(R, geo(dw), stage, &s_hbar[dw * 4]);
+      else
+        pw_helper<false>(R, geo(dw), stage, &s_hbar[dw * 4]);
     }
   }
   cluster_sync();  // lastce / pw / delta of all CTAs visible
@@ -1352,7 +1422,7 @@ constexpr size_t kSmemBudget = 220 * 1024;
 
 size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps) {
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
-  size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * (dp_ring_bytes<true>() + 8 * kWin);
+  size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * (dp_ring_bytes<true>() + 8 * kPwStageWords);
   size_t sel = (size_t)pitch * (8 + 8 + 4 * 4) + 16;
   if (stage) sel += (size_t)(nblk + 3) * pitch;  // delta table, later this CTA's choice-word rows
   const size_t RB = (((size_t)pitch + 15) & ~(size_t)15) + 16;
