@@ -308,6 +308,8 @@ struct CarveSet {
 void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
                  int cl, cudaStream_t st, const int* nfr = nullptr, bool reaverage = false) {
   SCPL_ARG(cols <= 4096, "frames wider than 4096 columns (in the carve orientation) are not supported");
+  // int-pass keys hold the path cost (<= 255 per row) above 9 bits of direction data
+  SCPL_ARG(rows <= 8192, "frames taller than 8192 rows (in the carve orientation) are not supported");
   const int pitch = (cols + 15) & ~15;
   const int nblk = std::max(1, (rows - 1 + kBlockRows - 1) / kBlockRows);
   const int rem_cap = std::max(1, cols - target);
@@ -326,7 +328,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   const size_t planes_bytes = (size_t)total_fr * 2 * plane_al;
   const bool uniform_given = with_U;
   if (reaverage) with_U = true;  // U = the mean gradient, recomputed every pass
-  size_t per = align256(plane * 2) + align256((size_t)nblk * pitch * 4) +
+  size_t per = align256(plane * 2) + align256((size_t)nblk * pitch * 8) +
                align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
                align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(256) +
                (with_U ? align256(plane * 8) : 0) + align256((size_t)cols * 4) +
@@ -367,7 +369,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     plane_off += (size_t)R.nfr * 2 * plane_al;
     R.width = cols;
     R.idx = reinterpret_cast<int16_t*>(take(plane * 2));
-    R.pw = reinterpret_cast<uint32_t*>(take((size_t)nblk * pitch * 4));
+    R.pw = reinterpret_cast<uint64_t*>(take((size_t)nblk * pitch * 8));
     R.delta = reinterpret_cast<int8_t*>(take((size_t)nblk * pitch));
     R.lastce = reinterpret_cast<double*>(take((size_t)pitch * 8));
     R.rem = reinterpret_cast<int16_t*>(take((size_t)rows * rem_cap * 2));

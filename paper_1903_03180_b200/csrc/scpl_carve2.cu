@@ -104,6 +104,11 @@ __device__ __forceinline__ uint32_t lds32_u(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint64_t lds64_u(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ int lds_s8(uint32_t a) {
   int v;
   asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -198,7 +203,11 @@ struct Val<true> {
 
 // A DP warp's block-end staging (choice / path words, dir sums, then a 4-word header holding
 // the block index and row count), double buffered when a helper warp stores it.
-constexpr int kPwStageWords = 2 * kWin + 4;
+constexpr int kPwStageWords = 3 * kWin + 4;  // 64-bit words, dir sums, header
+// Int-pass keys: K = ce << kKeyShift | dir << kDirShift | sumdir (the dir sum of the path within
+// the current 32-row block, <= 64: 7 bits).
+constexpr int kKeyShift = 9, kDirShift = 7, kSumMask = (1 << kDirShift) - 1;
+constexpr int kSubRows = 16;  // int passes: rows per 32-bit choice word (two per block)
 
 struct Geo {  // per-pass column ownership
   int w;          // current width
@@ -249,7 +258,7 @@ __device__ __forceinline__ void dp_issue_stage(const CarveRun& Rg, int plane, in
 // float64 pass (first pass of a buffered run): ce values with path words pw carried along
 // (2 bits per row of the seam ending in the column).
 template <bool F64, bool EDGE>
-__device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t (&pw)[kC],
+__device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint64_t (&pw)[kC],
                                        const uint8_t* erow, const bool (&in)[kC], int lane) {
   using V = Val<F64>;
   using T = typename V::T;
@@ -265,23 +274,23 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t 
   }
   T left = __shfl_up_sync(0xffffffffu, ce[kC - 1], 1);
   T right = __shfl_down_sync(0xffffffffu, ce[0], 1);
-  uint32_t pleft = __shfl_up_sync(0xffffffffu, pw[kC - 1], 1);
-  uint32_t pright = __shfl_down_sync(0xffffffffu, pw[0], 1);
+  uint64_t pleft = __shfl_up_sync(0xffffffffu, pw[kC - 1], 1);
+  uint64_t pright = __shfl_down_sync(0xffffffffu, pw[0], 1);
   if (lane == 0) left = V::inf();
   if (lane == 31) right = V::inf();
   T nce[kC];
-  uint32_t npw[kC];
+  uint64_t npw[kC];
 #pragma unroll
   for (int k = 0; k < kC; ++k) {
     T l = k > 0 ? ce[k - 1] : left;
     T c = ce[k];
     T r = k + 1 < kC ? ce[k + 1] : right;
-    uint32_t pl = k > 0 ? pw[k - 1] : pleft;
-    uint32_t pc = pw[k];
-    uint32_t pr = k + 1 < kC ? pw[k + 1] : pright;
+    uint64_t pl = k > 0 ? pw[k - 1] : pleft;
+    uint64_t pc = pw[k];
+    uint64_t pr = k + 1 < kC ? pw[k + 1] : pright;
     bool p1 = c < l;
     T m = p1 ? c : l;
-    uint32_t ps = p1 ? pc : pl;
+    uint64_t ps = p1 ? pc : pl;
     uint32_t code = p1 ? 1u : 0u;
     bool p2 = r < m;
     m = p2 ? r : m;
@@ -289,7 +298,7 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t 
     code = p2 ? 2u : code;
     T v = V::add(e[k], m);
     nce[k] = (!EDGE || in[k]) ? v : V::inf();
-    npw[k] = (ps << 2) | code;
+    npw[k] = (ps << 2) | (uint64_t)code;
   }
 #pragma unroll
   for (int k = 0; k < kC; ++k) {
@@ -298,11 +307,11 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint32_t 
   }
 }
 
-// int32 passes: one packed key per column, K = ce << 8 | dir << 6 | sumdir.  The three
-// candidates of a cell are K[j-1] (dir 0), K[j] + 64 (dir 1) and K[j+1] + 128 (dir 2); their
+// int32 passes: one packed key per column, K = ce << 9 | dir << 7 | sumdir.  The three
+// candidates of a cell are K[j-1] (dir 0), K[j] + 128 (dir 1) and K[j+1] + 256 (dir 2); their
 // minimum is the minimum cost with ties going to the lower dir -- exactly the reference's
 // strict '<' in the order -1, 0, +1 (seams.py:54-64) -- and carries the predecessor's sum of
-// dirs within the current 16-row block, so the block's landing delta (sumdir - rows) needs
+// dirs within the current 32-row block, so the block's landing delta (sumdir - rows) needs
 // no path word.  cw collects this column's own dir per row (the choice word, latest row in
 // the low bits); the trace walks the choice words of the columns a seam visits.
 template <bool EDGE>
@@ -320,11 +329,11 @@ __device__ __forceinline__ void dp_row_key(int (&K)[kC], uint32_t (&cw)[kC], con
 #pragma unroll
   for (int k = 0; k < kC; ++k) {
     const int l = k > 0 ? K[k - 1] : left;
-    const int c = K[k] + 64;
-    const int r = (k + 1 < kC ? K[k + 1] : right) + 128;
+    const int c = K[k] + (1 << kDirShift);
+    const int r = (k + 1 < kC ? K[k + 1] : right) + (2 << kDirShift);
     const int m = min(min(l, c), r);
-    const int dir = (m >> 6) & 3;
-    const int v = m - 63 * dir + (e[k] << 8);
+    const int dir = (m >> kDirShift) & 3;
+    const int v = m - kSumMask * dir + (e[k] << kKeyShift);
     n[k] = (!EDGE || in[k]) ? v : kIntInf;
     cw[k] = (cw[k] << 2) | (uint32_t)dir;
   }
@@ -333,8 +342,8 @@ __device__ __forceinline__ void dp_row_key(int (&K)[kC], uint32_t (&cw)[kC], con
 }
 
 // one row of either pass
-template <bool F64, bool EDGE>
-__device__ __forceinline__ void dp_step(typename Val<F64>::T (&ce)[kC], uint32_t (&pw)[kC], const uint8_t* erow,
+template <bool F64, bool EDGE, class PW>
+__device__ __forceinline__ void dp_step(typename Val<F64>::T (&ce)[kC], PW (&pw)[kC], const uint8_t* erow,
                                         const bool (&in)[kC], int lane) {
   if constexpr (F64)
     dp_row<true, EDGE>(ce, pw, erow, in, lane);
@@ -365,20 +374,24 @@ __device__ __forceinline__ uint32_t halo_bytes_for(int w, int CL, uint32_t rank,
 
 // Global stores of one staged block end (the lane-contiguous words transposed through the
 // staging row so the stores coalesce): owned columns' words and landing deltas.
+// stg: 64-bit words of the window's columns (2 bits per row, the block's last row in the low
+// bits), then their dir sums (int passes), then the header.
 template <bool F64>
 __device__ __forceinline__ void store_block_end(const CarveRun& R, const Geo& g, const uint32_t* stg, int pbi,
                                                 int nrb) {
   const int lane = threadIdx.x & 31;
-  uint32_t* gpw = R.pw + (long)pbi * R.pitch + g.win_lo;
+  const uint64_t* w64 = reinterpret_cast<const uint64_t*>(stg);
+  uint64_t* gpw = R.pw + (long)pbi * R.pitch + g.win_lo;
   int8_t* gdl = R.delta + (long)pbi * R.pitch + g.win_lo;
 #pragma unroll
   for (int k = 0; k < kC; ++k) {
     const int c = lane + 32 * k;
     const int j = g.win_lo + c;
     if (j >= g.own_lo && j < g.own_hi) {  // (transposed column: not this lane's own[])
-      const uint32_t word = stg[c];
+      const uint64_t word = w64[c];
       gpw[c] = word;
-      const int sumdir = F64 ? __popc(word & 0x55555555u) + 2 * __popc(word & 0xAAAAAAAAu) : (int)stg[kWin + c];
+      const int sumdir = F64 ? __popcll(word & 0x5555555555555555ull) + 2 * __popcll(word & 0xAAAAAAAAAAAAAAAAull)
+                             : (int)stg[2 * kWin + c];
       gdl[c] = (int8_t)(sumdir - nrb);
     }
   }
@@ -392,9 +405,9 @@ __device__ void pw_helper(const CarveRun& R, const Geo& g, const uint32_t* stage
   for (uint32_t n = 0;; ++n) {
     mbar_wait(&hbar[n & 1], (n >> 1) & 1);
     const uint32_t* stg = stage + (n & 1) * kPwStageWords;
-    const uint32_t hdr = stg[2 * kWin];
+    const uint32_t hdr = stg[3 * kWin];
     if (hdr == 0xffffffffu) break;
-    store_block_end<F64>(R, g, stg, (int)hdr, (int)stg[2 * kWin + 1]);
+    store_block_end<F64>(R, g, stg, (int)hdr, (int)stg[3 * kWin + 1]);
     mbar_arrive(&hbar[2 + (n & 1)]);
   }
 }
@@ -409,13 +422,16 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
   constexpr int sz = F64 ? 8 : 1;
   static_assert(kXRows % RS == 0 && kBlockRows % RS == 0 || RS == kXRows, "stage layout");
+  static_assert(kBlockRows == kXRows && kBlockRows == 2 * kSubRows, "one block per exchange, two choice words");
   const int lane = threadIdx.x & 31;
   const int rows = R.rows, w = g.w, pitch = R.pitch;
   const bool active = g.own_lo < g.own_hi;
   const int j0 = g.win_lo + lane * kC;
   const bool nb_mode = per_cta >= kXRows;
   T ce[kC];
-  uint32_t pw[kC];
+  using PW = std::conditional_t<F64, uint64_t, uint32_t>;
+  PW pw[kC];          // F64: path words of the block; int: choice words of the 16-row sub-block
+  uint32_t cwh[kC];   // int: choice words of the block's first sub-block
   bool in[kC];
 #pragma unroll
   for (int k = 0; k < kC; ++k) in[k] = (j0 + k >= 0) && (j0 + k < w);
@@ -432,7 +448,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       if constexpr (F64)
         v = in[k] ? R.U[j0 + k] : 0.0;
       else
-        v = in[k] ? (int)R.grad[plane][j0 + k] << 8 : 0;  // key of row 0
+        v = in[k] ? (int)R.grad[plane][j0 + k] << kKeyShift : 0;  // key of row 0
       ce[k] = in[k] ? v : V::inf();
     }
     if (lane == 0)
@@ -467,17 +483,28 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   auto store_pw = [&](int pbi, int nrb) {
     [[maybe_unused]] long long t7 = DP_CLOCK();
     uint32_t* stg = hbar ? next_stage() : pw_stage;
+    uint64_t* s64 = reinterpret_cast<uint64_t*>(stg);
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < kC; k += 2) {
-      *reinterpret_cast<uint2*>(&stg[lane * kC + k]) = make_uint2(pw[k], pw[k + 1]);
-      if constexpr (!F64)
-        *reinterpret_cast<int2*>(&stg[kWin + lane * kC + k]) = make_int2(ce[k] & 63, ce[k + 1] & 63);
+    for (int k = 0; k < kC; ++k) {
+      uint64_t word;
+      if constexpr (F64) {
+        word = pw[k];
+      } else {  // rows of the second sub-block in the low bits, contiguous with the first's
+        const int n2 = nrb - kSubRows;
+        word = n2 > 0 ? ((uint64_t)cwh[k] << (2 * n2)) | pw[k] : (uint64_t)pw[k];
+      }
+      s64[lane * kC + k] = word;
+    }
+    if constexpr (!F64) {
+#pragma unroll
+      for (int k = 0; k < kC; k += 2)
+        *reinterpret_cast<int2*>(&stg[2 * kWin + lane * kC + k]) = make_int2(ce[k] & kSumMask, ce[k + 1] & kSumMask);
     }
     if (hbar) {
       if (lane == 0) {
-        stg[2 * kWin] = (uint32_t)pbi;
-        stg[2 * kWin + 1] = (uint32_t)nrb;
+        stg[3 * kWin] = (uint32_t)pbi;
+        stg[3 * kWin + 1] = (uint32_t)nrb;
       }
       mbar_arrive(&hbar[hu & 1]);
       ++hu;
@@ -507,26 +534,38 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       }
       const uint8_t* stage = nullptr;
       if constexpr (RS == kXRows) stage = stage_rows(xb);
-#pragma unroll 1
-      for (int pb = 0; pb < kXRows / kBlockRows; ++pb) {
-        const int i0 = 1 + xb * kXRows + pb * kBlockRows;
-        const int nr = min(kBlockRows, rows - i0);
-        if (nr <= 0) break;
+      // one 32-row block per exchange block: path words / dir sums restart here; int passes
+      // fill a 32-bit choice word per 16-row sub-block
+      const int i0 = 1 + xb * kXRows;
+      const int nrb = min(kBlockRows, rows - i0);
 #pragma unroll
-        for (int k = 0; k < kC; ++k) {  // path / choice words and dir sums restart every 16 rows
-          pw[k] = 0u;
-          if constexpr (!F64) ce[k] &= ~63;
+      for (int k = 0; k < kC; ++k) {
+        pw[k] = 0;
+        if constexpr (!F64) ce[k] &= ~kSumMask;
+      }
+#pragma unroll 1
+      for (int sb = 0; sb * kSubRows < nrb; ++sb) {
+        const int s0 = i0 + sb * kSubRows;
+        const int nr = min(kSubRows, rows - s0);
+        if constexpr (!F64) {
+          if (sb == 1) {
+#pragma unroll
+            for (int k = 0; k < kC; ++k) {
+              cwh[k] = pw[k];
+              pw[k] = 0u;
+            }
+          }
         }
-        if (nr == kBlockRows) {
+        if (nr == kSubRows) {
           // 4 rows unrolled per step: short enough for the instruction cache
 #pragma unroll 1
-          for (int r4 = 0; r4 < kBlockRows; r4 += 4) {
+          for (int r4 = 0; r4 < kSubRows; r4 += 4) {
             const uint8_t* ebase;
             if constexpr (RS == kXRows) {
-              ebase = stage + (size_t)(pb * kBlockRows + r4) * kRingW * sz;
+              ebase = stage + (size_t)(sb * kSubRows + r4) * kRingW * sz;
             } else {
               static_assert(RS == 4, "fp64 stages hold 4 rows");
-              ebase = stage_rows((i0 - 1 + r4) / RS);
+              ebase = stage_rows((s0 - 1 + r4) / RS);
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r) dp_step<F64, EDGE>(ce, pw, ebase + (size_t)r * kRingW * sz, in, lane);
@@ -534,10 +573,10 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         } else {
 #pragma unroll 1
           for (int r = 0; r < nr; ++r) {
-            const int i = i0 + r;
+            const int i = s0 + r;
             const uint8_t* erow;
             if constexpr (RS == kXRows) {
-              erow = stage + (size_t)(pb * kBlockRows + r) * kRingW * sz;
+              erow = stage + (size_t)(sb * kSubRows + r) * kRingW * sz;
             } else {
               if ((i - 1) % RS == 0) stage = stage_rows((i - 1) / RS);
               erow = stage + (size_t)((i - 1) % RS) * kRingW * sz;
@@ -545,12 +584,17 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
             dp_step<F64, EDGE>(ce, pw, erow, in, lane);
           }
         }
-        // path-word block end: owned words and landing deltas (read after the pass); the
-        // exchange block's last one is stored after the exchange below
-        last_pbi = (i0 - 1) / kBlockRows;
-        last_nr = nr;
-        if (pb + 1 < kXRows / kBlockRows && i0 + nr < rows) store_pw(last_pbi, last_nr);
       }
+      if constexpr (!F64) {
+        if (nrb <= kSubRows) {  // a single sub-block: its words are the block's
+#pragma unroll
+          for (int k = 0; k < kC; ++k) cwh[k] = 0u;
+        }
+      }
+      // block end: owned words and landing deltas (read after the pass), stored after the
+      // exchange below
+      last_pbi = xb;
+      last_nr = nrb;
       DP_PROF(2, DP_CLOCK() - tx);
       tx = DP_CLOCK();
     }
@@ -615,7 +659,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   }
   if (hbar) {  // end of the pass for the helper warp
     uint32_t* stg = next_stage();
-    if (lane == 0) stg[2 * kWin] = 0xffffffffu;
+    if (lane == 0) stg[3 * kWin] = 0xffffffffu;
     mbar_arrive(&hbar[hu & 1]);
   }
   if (nb_mode && nx > 0) {  // the last exchange must be complete before the smem is reused
@@ -631,7 +675,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
         if constexpr (F64)
           R.lastce[j] = ce[k];
         else
-          R.lastce[j] = (double)(ce[k] >> 8);
+          R.lastce[j] = (double)(ce[k] >> kKeyShift);
       }
     }
   }
@@ -1122,9 +1166,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     if (stage_cw) {
       if (tid == 0) {
         fence_proxy_async_global();
-        mbar_arrive_tx(&s_dbar, (uint32_t)(myblk * pitch * 4));
+        mbar_arrive_tx(&s_dbar, (uint32_t)(myblk * pitch * 8));
         for (int m = 0; m < myblk; ++m)
-          bulk_g2s(S.dtab + (size_t)m * pitch * 4, R.pw + (long)((int)rank + m * CL) * pitch, (uint32_t)pitch * 4u,
+          bulk_g2s(S.dtab + (size_t)m * pitch * 8, R.pw + (long)((int)rank + m * CL) * pitch, (uint32_t)pitch * 8u,
                    &s_dbar);
       }
       mbar_wait(&s_dbar, 1);
@@ -1132,12 +1176,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     for (int q = tid; q < b * myblk; q += blockDim.x) {
       int s = q / myblk, bl = (int)rank + (q - s * myblk) * CL;
       int c = R.cend[(long)bl * pitch + s];
-      const uint32_t* pwb = R.pw + (long)bl * pitch;
-      const uint32_t cws = smem_u32(S.dtab) + (uint32_t)((q - s * myblk) * pitch) * 4u;
+      const uint64_t* pwb = R.pw + (long)bl * pitch;
+      const uint32_t cws = smem_u32(S.dtab) + (uint32_t)((q - s * myblk) * pitch) * 8u;
       int i_start = 1 + bl * kBlockRows;
       int i_end = min(i_start + kBlockRows, rows) - 1;
       if (fp64) {  // path word of the seam's end column
-        uint32_t word = pwb[c];
+        uint64_t word = pwb[c];
         for (int i = i_end; i >= i_start; --i) {
           log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
           c += (int)(word & 3u) - 1;
@@ -1146,7 +1190,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
       } else if (stage_cw) {  // choice words of the visited columns (shared memory)
         for (int i = i_end, q = 0; i >= i_start; --i, ++q) {
           log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
-          c += (int)((lds32_u(cws + 4u * (uint32_t)c) >> (2 * q)) & 3u) - 1;
+          c += (int)((lds64_u(cws + 8u * (uint32_t)c) >> (2 * q)) & 3u) - 1;
         }
       } else {
         for (int i = i_end, q = 0; i >= i_start; --i, ++q) {
@@ -1420,15 +1464,16 @@ int carve_cluster_size(int nruns, int width, int num_sms) {
 
 constexpr size_t kSmemBudget = 220 * 1024;
 
-size_t carve_smem_bytes(int rows, int pitch, bool stage, int warps, int dp_warps) {
+size_t carve_smem_bytes(int rows, int pitch, bool stage, int cl, int dp_warps) {
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
   size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * (dp_ring_bytes<true>() + 8 * kPwStageWords);
   size_t sel = (size_t)pitch * (8 + 8 + 4 * 4) + 16;
-  if (stage) sel += (size_t)(nblk + 3) * pitch;  // delta table, later this CTA's choice-word rows
-  const size_t RB = (((size_t)pitch + 15) & ~(size_t)15) + 16;
-  size_t comp = (size_t)warps * (4 * RB + kWarpScratch);
-  size_t m = dp > sel ? dp : sel;
-  return m > comp ? m : comp;
+  if (stage) {  // delta table, later (clusters of >= 4) this CTA's blocks of 64-bit choice words
+    const size_t dtab = (size_t)(nblk + 3) * pitch;
+    const size_t cw = cl >= 4 ? (size_t)((nblk + cl - 1) / cl) * pitch * 8 : 0;
+    sel += dtab > cw ? dtab : cw;
+  }
+  return dp > sel ? dp : sel;
 }
 
 int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
@@ -1437,7 +1482,7 @@ int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
 int carve_kernels_per_iteration(bool reaverage) { return reaverage ? 5 : 4; }
 
 bool carve_stage_dtab(int rows, int pitch, int cl) {
-  return carve_smem_bytes(rows, pitch, true, 0, carve_dp_warps(pitch, cl)) <= kSmemBudget;
+  return carve_smem_bytes(rows, pitch, true, cl, carve_dp_warps(pitch, cl)) <= kSmemBudget;
 }
 
 void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
@@ -1446,7 +1491,7 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   const int dpw = carve_dp_warps(width, cl);
   SCPL_ARG(dpw <= kMaxWarps, "carve width too large for the cluster size");
   const bool stage = carve_stage_dtab(rows, pitch, cl);
-  size_t smem = carve_smem_bytes(rows, pitch, stage, 0, dpw);
+  size_t smem = carve_smem_bytes(rows, pitch, stage, cl, dpw);
   SCPL_ARG(smem <= 227 * 1024, "carve plane too large for shared memory");
   smem_optin(reinterpret_cast<const void*>(carve_pass_kernel));
   cudaLaunchConfig_t cfg = {};

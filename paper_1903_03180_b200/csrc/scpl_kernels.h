@@ -10,7 +10,7 @@ namespace scpl {
 
 constexpr int kPwDepth = 14;   // virtual complete tree depth for the pairwise fold
 constexpr int kPwFoldCtas = 16;  // CTAs per candidate folding one depth-10 subtree each
-constexpr int kBlockRows = 16; // DP rows per 32-bit path word (2 bits per row)
+constexpr int kBlockRows = 32; // DP rows per 64-bit path / choice word (2 bits per row)
 
 struct PwVnode {
   int first_leaf;
@@ -76,7 +76,7 @@ struct alignas(64) CarveRun {
   int alive_pitch;
   int16_t* cend;        // nblk x pitch scratch: block-end columns of the selected seams
   long long* prof;      // optional (SCPL_PROF): detailed phase cycles
-  uint32_t* pw;         // nblk x pitch path words at block-end rows
+  uint64_t* pw;         // nblk x pitch path / choice words of each block (2 bits per row)
   int8_t* delta;        // nblk x pitch landing deltas
   double* lastce;       // pitch
   int16_t* rem;         // rows x rem_cap: removed columns of every batch, in that batch's coordinates
