@@ -119,6 +119,8 @@ typedef struct {
                                 number of carve-pass kernel launches (dp_passes / launches = runs
                                 per launch) */
   int carve_cluster;   /* CTAs per run cluster used by the carve */
+  int scan_windows;    /* buffered: windows the buffer scan evaluated (screened or exact) */
+  int scan_fallbacks;  /* buffered: screened windows re-run exactly (bound inconclusive) */
 } scpl_video_result;
 
 /* vidcarve.pipeline.retarget_video (pipeline.py:92-137), buffered / scpl / raw modes,

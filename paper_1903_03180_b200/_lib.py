@@ -34,6 +34,7 @@ class VideoResult(ctypes.Structure):
         ("dp_passes", ctypes.c_long), ("n_runs", ctypes.c_int),
         ("run_start", _c_int_p), ("run_len", _c_int_p), ("phase_ms", ctypes.c_float * 4),
         ("carve_cycles", ctypes.c_longlong * 4), ("carve_cluster", ctypes.c_int),
+        ("scan_windows", ctypes.c_int), ("scan_fallbacks", ctypes.c_int),
     ]
 
 

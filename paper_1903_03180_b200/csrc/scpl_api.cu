@@ -219,7 +219,7 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int 
   S.plan = &plan;
   S.spec = spec;
   S.T = T;
-  S.ck = DBuf(sizeof(double) * 2 * N, st);
+  S.ck = DBuf(sizeof(double) * 4 * N, st);
   S.leafsum = DBuf(sizeof(double) * spec * plan.nleaves, st);
   S.partial = DBuf(sizeof(double) * spec * kPwFoldCtas, st);
   S.runs_d = DBuf(sizeof(int) * 2 * T, st);
@@ -228,6 +228,13 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int 
   init.N = N;
   init.ckS = S.ck.as<double>();
   init.ckQ = S.ck.as<double>() + N;
+  init.ckS2 = S.ck.as<double>() + 2 * N;
+  init.ckQ2 = S.ck.as<double>() + 3 * N;
+  // screened windows (exact re-run only when the bound cannot settle a threshold test);
+  // SCPL_SCAN_EXACT=1 evaluates every window exactly, SCPL_SCAN_FORCE_FALLBACK=1 screens
+  // every window and then re-runs it exactly (tests of both paths)
+  init.approx = getenv("SCPL_SCAN_EXACT") ? 0 : 1;
+  init.force_fallback = getenv("SCPL_SCAN_FORCE_FALLBACK") ? 1 : 0;
   init.leafsum = S.leafsum.as<double>();
   init.partial = S.partial.as<double>();
   init.phi = ctx->phi_d;
@@ -260,10 +267,12 @@ void scan_end(scpl_ctx* ctx, ScanStream& S, cudaStream_t st) {
 }
 
 // after the stream is done
-void scan_finish(ScanStream& S, int chunks) {
+void scan_finish(ScanStream& S, int chunks, scpl_video_result* result) {
   const ScanState& R = *S.h_state;
   if (!(R.done == 1 && R.nruns >= 1 && R.nruns <= S.T)) throw Error{2, "buffer scan did not finish"};
   g_launches.fetch_add((long)chunks + 3L * R.steps, std::memory_order_relaxed);
+  result->scan_windows = R.steps;
+  result->scan_fallbacks = R.fallbacks;
 }
 
 // ------------------------------------------------------------------ carve driver
@@ -686,6 +695,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   for (float& x : result->phase_ms) x = 0.f;
   for (long long& x : result->carve_cycles) x = 0;
   result->carve_cluster = 0;
+  result->scan_windows = result->scan_fallbacks = 0;
   if (T <= 0) return;
   const int C = channels;
   const int tw = P.target_width, th = P.target_height;
@@ -970,7 +980,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   hmark("synchronized");
 
   // 4. results
-  if (buffered) scan_finish(scan, nchunk);
+  if (buffered) scan_finish(scan, nchunk, result);
   result->n_runs = (int)runs.size();
   if (result->run_start && result->run_len)
     for (size_t r = 0; r < runs.size(); ++r) {

@@ -68,8 +68,7 @@ __device__ __forceinline__ double div_small(double x, double n, double rn) {
 __device__ __forceinline__ double energy_of(uint32_t code, bool pure, const double* A, const double* B) {
   uint32_t g = code & 255u;
   if (pure) return (double)g;
-  double e = __dadd_rn(A[code >> 8], B[g]);
-  return e <= 255.0 ? e : 255.0;
+  return fmin(__dadd_rn(A[code >> 8], B[g]), 255.0);  // e is never NaN: fmin == the clamp
 }
 
 // ---------------------------------------------------------------- async copy helpers (TMA bulk)

@@ -38,16 +38,27 @@ void launch_pairwise_fold(const double* leafsum, int nleaves, const PwVnode* vno
                           double* partial, double* out, cudaStream_t st);
 
 // Device-side buffer scan state (scpl_stats.cu).  runs holds (start, len) pairs.
+constexpr int kScanMaxL = 64;  // candidates per window (spec_len <= 64)
 struct ScanState {
   const uint16_t* codes;
   long N;
-  double *ckS, *ckQ, *leafsum, *partial;
+  double *ckS, *ckQ;    // S, Q after the accepted frames (read by a window that continues a run)
+  double *ckS2, *ckQ2;  // written by every window; swapped with ckS/ckQ when all its candidates pass
+  double *leafsum, *partial;
   const double* phi;  // threshold(n), n = 0..max_len
   int* runs;
   double wm, wg;
   int T, max_len, spec, avail;
   int s, n_acc, init, L, done, nruns;
-  int steps;  // loop-body executions (3 kernels each)
+  int steps;      // loop-body executions (3 kernels each)
+  // Screened windows: a window is first evaluated by the cheap bounded kernel (approximate
+  // ASDE + a rigorous bound on its distance to the reference's value); only a window with a
+  // candidate whose threshold test the bound cannot settle is re-run exactly.
+  int approx;     // screening enabled
+  int exact;      // the current window runs the exact kernel (screening was inconclusive)
+  int force_fallback;  // testing: treat every screened window as inconclusive
+  int fallbacks;  // windows re-run exactly
+  double asum[kScanMaxL], bsum[kScanMaxL];  // per candidate: sum of approximate std, of bounds
 };
 cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec);
 void launch_scan_reset(ScanState* S, const ScanState& init, cudaStream_t st);

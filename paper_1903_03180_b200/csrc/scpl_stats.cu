@@ -71,6 +71,17 @@ void build_pairwise_plan(long N, std::vector<int2>& leaves, std::vector<PwVnode>
 // stream into an 8-stage shared-memory ring by 1-D TMA bulk copies issued up front, so the
 // fp64 work never waits on a global load; lanes then read their strided elements from
 // shared memory.  Rows of N not divisible by 8 fall back to cooperative plain copies.
+// Screening bound (APPROX).  With u = 2^-53, X = Q/n <= 255^2 (every e <= 255) and
+// M = S/n, the screened variance fma(-m, m, RN(Q*rn)) (m = RN(S*rn), rn = RN(1/n)) and the
+// reference's RN(RN(Q/n) - RN(RN(S/n)^2)) differ by at most 5.03uX + 9.12uM^2 <= 14.2uX
+// (+ O(u^2)) <= 1.03e-10; kScanDelta doubles that.  For x, y >= 0, |sqrt(x) - sqrt(y)| <=
+// min(sqrt|x-y|, |x-y| / sqrt(x)), and max(., 0) does not increase the distance, so per pixel
+// |std~ - std| <= min(sqrt(delta), delta / std~) plus relative roundings (f32 conversion,
+// rsqrt.approx (budgeted at 2^-20), the <= 9-term per-lane f32 sum: < 1.6e-6 of std~), which
+// the decision adds separately with a 5x margin.
+constexpr float kScanDelta = 2.0e-10f;
+constexpr float kScanSqrtDelta = 1.4143e-5f;  // > sqrt(kScanDelta)
+
 constexpr int kLeafLanes = 16;     // lanes per leaf: accumulator j = lanes j (first half) and j + 8
 constexpr int kHalfMax = 8;        // elements per lane and accumulator half (a leaf has <= 16 per accumulator)
 constexpr int kStatStages = 8;
@@ -83,11 +94,20 @@ constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatSt
 // (m0 = ceil(nmain/2)): the first half sums its part, hands the partial to the second half,
 // which continues the same sequential sum -- the bracketing is numpy's exactly, with half the
 // registers per lane (so twice the resident warps hide the fp64 latency).
+//
+// APPROX (screening, scan only): per candidate the CTA adds sum(std~) and sum(bound) into
+// asum/bsum, where std~ = sqrt_f32(f32(fma(-m, m, Q*rn))), m = S*rn, rn = RN(1/n), and bound
+// is a per-pixel bound on |std~ - std| (std = the reference's fl(sqrt(max(var, 0))), see
+// kScanDelta) -- see scan_step_kernel for how the decision uses them.  S, Q themselves are
+// accumulated exactly as in the exact kernel, so the checkpoint is the reference's.
+// The checkpoint is read from ckS/ckQ (runs continued from an earlier window) and written to
+// ckSo/ckQo (the same arrays for an in-place update).
+template <bool APPROX>
 __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ codes, long N,
                                                   const int2* __restrict__ leaves, int nleaves, int s, int n_acc,
                                                   int L, int first_pure, int init, double wm, double wg,
-                                                  double* __restrict__ ckS, double* __restrict__ ckQ,
-                                                  double* __restrict__ leafsum) {
+                                                  const double* ckS, const double* ckQ, double* ckSo, double* ckQo,
+                                                  double* __restrict__ leafsum, double* asum, double* bsum) {
   extern __shared__ __align__(128) uint8_t st_ring[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(st_ring + kStatStages * kStatStageBytes);
   __shared__ double A[256], B[256];
@@ -180,6 +200,7 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
   }
 
   const int g0 = lane & ~15;  // first lane of this leaf's group
+  __shared__ double red[APPROX ? kScanMaxL * 16 : 1];  // per candidate and warp: (sum std~, sum bound)
   for (int c = 0; c < L; ++c, ++ci) {
     const int t = s + n_acc + c;
     const int n = n_acc + c + 1;
@@ -187,6 +208,38 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
     const double rn = __ddiv_rn(1.0, dn);
     const uint16_t* ct = acquire(ci);
     const bool pure = first_pure && t == 0;
+    if constexpr (APPROX) {
+      float as = 0.f, ab = 0.f;
+#pragma unroll
+      for (int k = 0; k <= kHalfMax; ++k) {
+        if (valid(k)) {
+          const double e = energy_of(ct[off(k)], pure, A, B);
+          S[k] = __dadd_rn(S[k], e);
+          Q[k] = __dadd_rn(Q[k], __dmul_rn(e, e));
+          const double m = __dmul_rn(S[k], rn);
+          const double var = __fma_rn(-m, m, __dmul_rn(Q[k], rn));
+          // std~ = v * rsqrt(v) (MUFU; v > 0 so no 0 * inf); a variance <= 0 gives std~ ~ 1e-15
+          // and the bound sqrt(delta), which covers the reference's std <= sqrt(delta) there
+          const float v = fmaxf(__double2float_rn(var), 1e-30f);
+          float rs;
+          asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(v));
+          as += v * rs;
+          ab += fminf(kScanSqrtDelta, kScanDelta * rs);
+        }
+      }
+      release(ci);
+      double ds = (double)as, db = (double)ab;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ds += __shfl_xor_sync(0xffffffffu, ds, o);
+        db += __shfl_xor_sync(0xffffffffu, db, o);
+      }
+      if (lane == 0) {
+        red[(c * 8 + (threadIdx.x >> 5)) * 2] = ds;
+        red[(c * 8 + (threadIdx.x >> 5)) * 2 + 1] = db;
+      }
+      continue;
+    }
     double sd[kHalfMax + 1];
 #pragma unroll
     for (int k = 0; k <= kHalfMax; ++k) {
@@ -225,13 +278,25 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
     if (active && sub == 8) leafsum[(size_t)c * nleaves + leaf] = x;
   }
 
+  if constexpr (APPROX) {  // this CTA's per-candidate sums (release() synchronised the warps)
+    __syncthreads();
+    for (int c = threadIdx.x; c < L; c += blockDim.x) {
+      double ds = 0.0, db = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        ds += red[(c * 8 + w) * 2];
+        db += red[(c * 8 + w) * 2 + 1];
+      }
+      atomicAdd(&asum[c], ds);
+      atomicAdd(&bsum[c], db);
+    }
+  }
   // checkpoint S,Q after n_acc + L frames
 #pragma unroll
   for (int k = 0; k <= kHalfMax; ++k) {
     if (valid(k)) {
       const long p = p_lo + off(k);
-      ckS[p] = S[k];
-      ckQ[p] = Q[k];
+      ckSo[p] = S[k];
+      ckQo[p] = Q[k];
     }
   }
 }
@@ -242,16 +307,21 @@ __global__ void __launch_bounds__(256, 3) window_stats_kernel(const uint16_t* __
                                                            double wm, double wg, double* __restrict__ ckS,
                                                            double* __restrict__ ckQ,
                                                            double* __restrict__ leafsum) {
-  window_stats_body(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init, wm, wg, ckS, ckQ, leafsum);
+  window_stats_body<false>(codes, N, leaves, nleaves, s, n_acc, L, first_pure, init, wm, wg, ckS, ckQ, ckS, ckQ,
+                           leafsum, nullptr, nullptr);
 }
 
 // Scan variant: the window comes from the device-side scan state (no host round trip).
-__global__ void __launch_bounds__(256, 3) window_stats_scan_kernel(const ScanState* __restrict__ S,
+__global__ void __launch_bounds__(256, 4) window_stats_scan_kernel(ScanState* S,
                                                                 const int2* __restrict__ leaves, int nleaves) {
   const int L = S->L;
   if (L <= 0) return;
-  window_stats_body(S->codes, S->N, leaves, nleaves, S->s, S->n_acc, L, 1, S->init, S->wm, S->wg, S->ckS,
-                    S->ckQ, S->leafsum);
+  if (!S->approx || S->exact)
+    window_stats_body<false>(S->codes, S->N, leaves, nleaves, S->s, S->n_acc, L, 1, S->init, S->wm, S->wg, S->ckS,
+                             S->ckQ, S->ckS2, S->ckQ2, S->leafsum, nullptr, nullptr);
+  else
+    window_stats_body<true>(S->codes, S->N, leaves, nleaves, S->s, S->n_acc, L, 1, S->init, S->wm, S->wg, S->ckS,
+                            S->ckQ, S->ckS2, S->ckQ2, nullptr, S->asum, S->bsum);
 }
 
 static void stats_smem_attr() {
@@ -286,7 +356,7 @@ __global__ void __launch_bounds__(256) fold_partial_kernel(const double* leafsum
   __shared__ double v[kPwSub];
   const int c = blockIdx.y;
   if (Sp != nullptr) {
-    if (c >= Sp->L) return;
+    if (c >= Sp->L || (Sp->approx && !Sp->exact)) return;  // a screened window needs no fold
     leafsum = Sp->leafsum;
     partial = Sp->partial;
   }
@@ -382,6 +452,7 @@ __device__ void scan_plan(ScanState* S) {
     L = min(L, S->avail - (S->s + S->n_acc));
     if (L <= 0) break;  // wait for more frames
     S->L = L;
+    for (int c = 0; c < L; ++c) S->asum[c] = S->bsum[c] = 0.0;
     return;
   }
   S->L = 0;
@@ -389,24 +460,59 @@ __device__ void scan_plan(ScanState* S) {
 
 // One thread per candidate folds its root; thread 0 then decides and plans the next window.
 __global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, int decide, int in_graph) {
-  __shared__ double asde[64];
+  __shared__ double asde[kScanMaxL];
   const int L = S->L;
-  if (decide && L > 0) {
+  const bool exact = !S->approx || S->exact;
+  if (decide && L > 0 && exact) {
     for (int c = threadIdx.x; c < L; c += blockDim.x) asde[c] = fold_root(S->partial, c, S->N);
     __syncthreads();
   }
   if (threadIdx.x != 0) return;
   if (decide && L > 0) {
     int breach = -1;
-    for (int c = 0; c < L; ++c) {
-      if (!(asde[c] <= S->phi[S->n_acc + c + 1])) {
-        breach = c;
-        break;
+    if (exact) {
+      for (int c = 0; c < L; ++c) {
+        if (!(asde[c] <= S->phi[S->n_acc + c + 1])) {
+          breach = c;
+          break;
+        }
+      }
+    } else {
+      // screened window: the reference accepts candidate c iff asde(c) <= phi; with
+      // |asde~ - asde| <= marg (kScanDelta's per-pixel bounds, the relative f32 roundings of
+      // std~ with a 5x margin, and the reference's own fp64 rounding) the test is settled
+      // when asde~ + marg < phi or asde~ - marg > phi.  Otherwise re-run the window exactly.
+      const double invN = 1.0 / (double)S->N;
+      bool unsure = S->force_fallback != 0;
+      for (int c = 0; c < L && !unsure; ++c) {
+        const double a = S->asum[c] * invN;
+        const double marg = 2.0 * S->bsum[c] * invN + 8e-6 * a + 1e-9;
+        const double phi = S->phi[S->n_acc + c + 1];
+        if (a + marg < phi) continue;
+        if (a - marg > phi) {
+          breach = c;
+          break;
+        }
+        unsure = true;
+      }
+      if (unsure) {  // same window again, exact kernel (the checkpoint read is untouched)
+        S->exact = 1;
+        S->fallbacks++;
+        S->steps++;
+        if (in_graph) cudaGraphSetConditional(loop, 1u);
+        return;
       }
     }
-    if (breach < 0) {
+    S->exact = 0;
+    if (breach < 0) {  // every candidate accepted: the written checkpoint becomes current
       S->n_acc += L;
       S->init = 0;
+      double* t = S->ckS;
+      S->ckS = S->ckS2;
+      S->ckS2 = t;
+      t = S->ckQ;
+      S->ckQ = S->ckQ2;
+      S->ckQ2 = t;
     } else {
       S->runs[2 * S->nruns] = S->s;
       S->runs[2 * S->nruns + 1] = S->n_acc + breach;

@@ -134,6 +134,8 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
     last_phase_ms["carve_cluster"] = res.carve_cluster
     last_phase_ms["pass_launches"] = int(res.carve_cycles[3])
     last_phase_ms["pass_launch_ms"] = float(res.phase_ms[3])
+    last_phase_ms["scan_windows"] = int(res.scan_windows)
+    last_phase_ms["scan_fallbacks"] = int(res.scan_fallbacks)
     return out, int(res.dp_passes), runs
 
 

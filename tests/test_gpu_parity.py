@@ -385,3 +385,32 @@ def test_pnm_stream_retarget_roundtrip(P, small):
         dst.seek(0)
         out = list(media.read_frames(dst))
         assert [sha(f) for f in out] == small["clips"][name]["frames"], name
+
+
+@pytest.mark.parametrize("mode", [None, "SCPL_SCAN_EXACT", "SCPL_SCAN_FORCE_FALLBACK"])
+def test_scan_screening_modes_match(P, mode, monkeypatch):
+    """The buffer scan screens each window with a cheap bounded ASDE (buffering.py:119 decided
+    from |asde~ - asde| <= bound) and re-runs it exactly only when the bound cannot settle a
+    threshold test.  Screened (default), all-exact and screened-then-always-re-run scans give
+    the reference's run boundaries (and so its passes) on the config clips."""
+    from paper_1903_03180_b200 import pipeline
+    from paper_1903_03180_b200.synth import config_clip
+    import torch
+    if mode:
+        monkeypatch.setenv(mode, "1")
+    for path in _config_golden("C2") + _config_golden("C4_clip0") + _config_golden("C5"):
+        g = json.load(open(path))
+        if g.get("reaverage"):
+            continue
+        clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
+        out, m = P.retarget_video_tensor(torch.from_numpy(clip).cuda(),
+                                         P.RetargetConfig(target_width=tw, target_height=th, mode="buffered"))
+        assert [list(r) for r in m.runs] == g["runs"], path
+        assert m.dp_passes == g["dp_passes"], path
+        ph = pipeline.last_phase_ms
+        if mode == "SCPL_SCAN_FORCE_FALLBACK":
+            assert ph["scan_fallbacks"] > 0
+        elif mode is None:  # screening settles (almost) every window
+            assert ph["scan_fallbacks"] * 10 <= ph["scan_windows"], ph
+        else:
+            assert ph["scan_fallbacks"] == 0
