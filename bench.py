@@ -67,8 +67,8 @@ def pass_roofline(ph, H, W, tw, peak, peak_src):
     group, one cluster per run; ~70% of kernel time in the committed launch list).
 
     Per run and pass the algorithmic bytes are the gradient plane read once (rows x width B) and
-    the 16-row path words + landing deltas written and read back (2 x 5 B per column per 16
-    rows); a launch carries dp_passes / launches runs.  The launch duration is the slowest
+    the 32-row choice words + landing deltas written and read back (2 x (8 + 1) B per column per
+    32 rows); a launch carries dp_passes / launches runs.  The launch duration is the slowest
     cluster's SM-clock cycles (clock64 in the kernel) -- the passes run inside conditional
     graphs on the library's own streams, where events cannot bracket a single kernel.
     traffic: DRAM bytes per launch from the committed ncu --set full capture, scaled to the
@@ -79,7 +79,7 @@ def pass_roofline(ph, H, W, tw, peak, peak_src):
         return None
     runs_per_launch = ph["dp_passes"] / launches
     cols = 0.5 * (W + tw)  # mean width over the passes
-    per_run = H * cols * (1.0 + 2 * 5 / 16)
+    per_run = H * cols * (1.0 + 2 * 9 / 32)
     alg = per_run * runs_per_launch
     achieved = alg / (launch_ms / 1e3) / 1e9
     traffic = None

@@ -308,7 +308,7 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint64_t 
 }
 
 // int32 passes: one packed key per column, K = ce << 9 | dir << 7 | sumdir.  The three
-// candidates of a cell are K[j-1] (dir 0), K[j] + 128 (dir 1) and K[j+1] + 256 (dir 2); their
+// candidates of a cell are K[j-1] (dir 0), K[j] + 129 (dir 1) and K[j+1] + 258 (dir 2); their
 // minimum is the minimum cost with ties going to the lower dir -- exactly the reference's
 // strict '<' in the order -1, 0, +1 (seams.py:54-64) -- and carries the predecessor's sum of
 // dirs within the current 32-row block, so the block's landing delta (sumdir - rows) needs
@@ -328,14 +328,19 @@ __device__ __forceinline__ void dp_row_key(int (&K)[kC], uint32_t (&cw)[kC], con
   int n[kC];
 #pragma unroll
   for (int k = 0; k < kC; ++k) {
+    // the candidates' biases add dir to the dir field and to the dir sum at once (sumdir + dir
+    // <= 64 + 2 never carries into the dir field, so ties still go to the lower dir); the new
+    // key is the minimum with its dir field cleared plus the energy
     const int l = k > 0 ? K[k - 1] : left;
-    const int c = K[k] + (1 << kDirShift);
-    const int r = (k + 1 < kC ? K[k + 1] : right) + (2 << kDirShift);
+    const int c = K[k] + ((1 << kDirShift) + 1);
+    const int r = (k + 1 < kC ? K[k + 1] : right) + ((2 << kDirShift) + 2);
     const int m = min(min(l, c), r);
-    const int dir = (m >> kDirShift) & 3;
-    const int v = m - kSumMask * dir + (e[k] << kKeyShift);
+    const int d = m & (3 << kDirShift);
+    int v;  // m - d + e * 512 as two multiply-adds (FMA pipe; the ALU pipe is the DP's bottleneck)
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(v) : "r"(e[k]), "r"(1 << kKeyShift), "r"(m));
+    asm("mad.lo.s32 %0, %1, -1, %2;" : "=r"(v) : "r"(d), "r"(v));
     n[k] = (!EDGE || in[k]) ? v : kIntInf;
-    cw[k] = (cw[k] << 2) | (uint32_t)dir;
+    cw[k] = cw[k] * 4u + __umulhi((uint32_t)d, 1u << (32 - kDirShift));  // d >> kDirShift
   }
 #pragma unroll
   for (int k = 0; k < kC; ++k) K[k] = n[k];
