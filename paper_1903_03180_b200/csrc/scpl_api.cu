@@ -279,6 +279,8 @@ void scan_finish(ScanStream& S, int chunks, scpl_video_result* result) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Planes for `nruns` carves of rows x cols (carve orientation) in one stream-ordered slab.
+constexpr size_t kProfBytes = 8192;  // SCPL_PROF: 32 counters + (entry, exit) timestamps per pass
+
 struct CarveSet {
   DBuf mem;
   std::vector<CarveRun> runs;
@@ -339,7 +341,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   if (reaverage) with_U = true;  // U = the mean gradient, recomputed every pass
   size_t per = align256(plane * 2) + align256((size_t)nblk * pitch * 8) +
                align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
-               align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(256) +
+               align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(kProfBytes) +
                (with_U ? align256(plane * 8) : 0) + align256((size_t)cols * 4) +
                (dbg ? align256((size_t)cols * 2) + align256((size_t)cols * 8) : 0);
   S.mem = DBuf(planes_bytes + per * nruns, st);
@@ -386,7 +388,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.alive = reinterpret_cast<uint32_t*>(take((size_t)rows * alive_pitch * 4));
     R.alive_pitch = alive_pitch;
     R.cend = reinterpret_cast<int16_t*>(take((size_t)nblk * pitch * 2));
-    R.prof = reinterpret_cast<long long*>(take(256));
+    R.prof = reinterpret_cast<long long*>(take(kProfBytes));
     if (!getenv("SCPL_PROF")) R.prof = nullptr;
     R.U = with_U ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
     R.sizes = reinterpret_cast<int*>(take((size_t)cols * 4));
@@ -411,7 +413,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   if (nruns == 0) return;
   for (auto& R : S.runs) {
     R.cyc_dp = R.cyc_sel = 0;
-    if (R.prof) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, 256, st));
+    if (R.prof) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, kProfBytes, st));
   }
   const bool graph = S.cols > S.target && !host_loops();
   S.ctx = ctx;
@@ -478,6 +480,19 @@ void carve_finish(CarveSet& S) {
               " trace %lld (x CTAs)\n",
               R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11], c[12], c[13], c[14],
               c[15], c[16]);
+      // pass timestamps (globaltimer ns at entry / exit of each pass): time inside passes vs gaps
+      const int n = std::min(R.iters, (int)(kProfBytes / 16) - 16);
+      std::vector<long long> ts(2 * (size_t)n);
+      if (n > 0) {
+        SCPL_CUDA(cudaMemcpy(ts.data(), R.prof + 32, sizeof(long long) * 2 * n, cudaMemcpyDeviceToHost));
+        long long in = 0, gap = 0;
+        for (int k = 0; k < n; ++k) {
+          in += ts[2 * k + 1] - ts[2 * k];
+          if (k > 0) gap += ts[2 * k] - ts[2 * k - 1];
+        }
+        fprintf(stderr, "carve ts: iters %d span %.3f ms in-pass %.3f ms gaps %.3f ms (first start %.3f ms)\n", n,
+                (ts[2 * n - 1] - ts[0]) * 1e-6, in * 1e-6, gap * 1e-6, (ts[0] % 1000000000LL) * 1e-6);
+      }
     }
     long long tot = R.cyc_dp + R.cyc_sel;
     if (tot > best) {

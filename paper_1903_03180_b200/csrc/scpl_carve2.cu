@@ -72,6 +72,11 @@ constexpr int kMaxWarps = 12;                    // 384 threads: up to 168 regis
 #define SEL_PROF(k) ((void)0)
 #endif
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -796,8 +801,10 @@ constexpr int kMaxRowWords = 1024;  // widths up to 4096
 // fits next to a resident pass CTA: the row kernels of one group then run on SMs that other
 // groups' (latency-bound) passes hold, instead of queueing for free SMs.
 constexpr int kCompWarps = 4;
+constexpr int kRowListCap = 256;  // removed-column list staged in shared memory (rows of batches up to this)
 __host__ __device__ __forceinline__ size_t compact_warp_bytes(int pitch) {
-  return 2 * (size_t)pitch + 4 * (size_t)((pitch >> 2) + 4) + 16;  // rows, histogram (nwo + 1 words), barrier
+  // rows, histogram (nwo + 1 words), barrier, removed-column list
+  return 2 * (size_t)pitch + 4 * (size_t)((pitch >> 2) + 4) + 16 + 2 * kRowListCap;
 }
 size_t carve_compact_smem(int pitch) { return (size_t)kCompWarps * compact_warp_bytes(pitch); }
 
@@ -812,19 +819,36 @@ __device__ __forceinline__ void compact_issue(const uint8_t* L, const uint8_t* G
 
 // One warp compacts one staged row in place: rg = the row's b removed columns (ascending, in
 // the w0 = wn + b column frame); the staging completes on bar (phase `parity`).
+// (bar == nullptr: the row is already staged; G / sG == nullptr: luma only; L2: a second luma
+// destination; rs: kRowListCap int16 of shared memory where a global list is staged for the
+// words whose shift changes inside them -- else a chain of dependent global loads per word)
 __device__ __forceinline__ void compact_row(uint8_t* L, uint8_t* G, const int16_t* rg, int b, int wn,
                                             const uint8_t* sL, const uint8_t* sG, uint32_t* hist, uint64_t* bar,
-                                            uint32_t parity) {
+                                            uint32_t parity, uint8_t* L2 = nullptr, int16_t* rs = nullptr) {
   const int lane = threadIdx.x & 31;
   const int w0 = wn + b;
   const int nwo = (wn + 3) >> 2;
   for (int q = lane; q <= nwo; q += 32) hist[q] = 0u;
   __syncwarp();
+  const bool stage_list = rs != nullptr && b <= kRowListCap;
+  // b <= 255: four 8-bit fields, field u counting a_t <= 4q + u, so every output byte's shift is
+  // known (no search when a removed column falls inside a word); else two 16-bit fields (u = 0, 3)
+  const bool f4 = b <= 255;
   for (int t = lane; t < b; t += 32) {
-    const int at = rg[t] - t;  // >= 0
-    const int q1 = (at + 3) >> 2, q2 = at >> 2;  // a_t <= 4q  <=>  q >= q1;  a_t <= 4q+3  <=>  q >= q2
-    if (q1 <= nwo) atomicAdd(&hist[q1], 1u);
-    if (q2 <= nwo) atomicAdd(&hist[q2], 0x10000u);
+    const int16_t rv = rg[t];
+    if (stage_list) rs[t] = rv;
+    const int at = rv - t;  // >= 0
+    if (f4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // a_t <= 4q + u  <=>  q >= (a_t - u + 3) >> 2
+        const int qu = (at - u + 3) >> 2;
+        if (qu <= nwo) atomicAdd(&hist[qu], 1u << (8 * u));
+      }
+    } else {
+      const int q1 = (at + 3) >> 2, q2 = at >> 2;  // a_t <= 4q  <=>  q >= q1;  a_t <= 4q+3  <=>  q >= q2
+      if (q1 <= nwo) atomicAdd(&hist[q1], 1u);
+      if (q2 <= nwo) atomicAdd(&hist[q2], 0x10000u);
+    }
   }
   __syncwarp();
   // inclusive prefix over q = 0 .. nwo-1: lane owns a contiguous segment
@@ -843,21 +867,33 @@ __device__ __forceinline__ void compact_row(uint8_t* L, uint8_t* G, const int16_
     run += hist[q];
     hist[q] = run;
   }
-  mbar_wait(bar, parity);
+  if (bar) mbar_wait(bar, parity);
   __syncwarp();
+  if (stage_list) rg = rs;  // (staged before the histogram's __syncwarp)
   const uint32_t* Lw = reinterpret_cast<const uint32_t*>(sL);
   const uint32_t* Gw = reinterpret_cast<const uint32_t*>(sG);
   const int nwi = (w0 + 3) >> 2;
   for (int q = lane; q < nwo; q += 32) {
     const uint32_t h = hist[q];
-    const int s0 = (int)(h & 0xffffu), s3 = (int)(h >> 16);
+    const int s0 = f4 ? (int)(h & 255u) : (int)(h & 0xffffu), s3 = f4 ? (int)(h >> 24) : (int)(h >> 16);
     uint32_t lv, gv;
     if (s0 == s3) {
       const int x0 = 4 * q + s0, wq = x0 >> 2;
       const uint32_t sh = (uint32_t)(x0 & 3) * 8u;
       const bool nx = wq + 1 < nwi;
       lv = __funnelshift_r(Lw[wq], nx ? Lw[wq + 1] : 0u, sh);
-      gv = __funnelshift_r(Gw[wq], nx ? Gw[wq + 1] : 0u, sh);
+      gv = G ? __funnelshift_r(Gw[wq], nx ? Gw[wq + 1] : 0u, sh) : 0u;
+    } else if (f4) {  // byte u from 4q + u + s(4q + u)
+      lv = 0u;
+      gv = 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = 4 * q + u + (int)((h >> (8 * u)) & 255u);
+        if (x < w0) {
+          lv |= (uint32_t)sL[x] << (8 * u);
+          if (G) gv |= (uint32_t)sG[x] << (8 * u);
+        }
+      }
     } else {  // s(4q + u) for u = 0..3 from the removed list
       int t = s0;
       lv = 0u;
@@ -867,36 +903,29 @@ __device__ __forceinline__ void compact_row(uint8_t* L, uint8_t* G, const int16_
         const int x = 4 * q + u + t;
         if (x < w0) {
           lv |= (uint32_t)sL[x] << (8 * u);
-          gv |= (uint32_t)sG[x] << (8 * u);
+          if (G) gv |= (uint32_t)sG[x] << (8 * u);
         }
       }
     }
     reinterpret_cast<uint32_t*>(L)[q] = lv;
-    reinterpret_cast<uint32_t*>(G)[q] = gv;
+    if (L2) reinterpret_cast<uint32_t*>(L2)[q] = lv;
+    if (G) reinterpret_cast<uint32_t*>(G)[q] = gv;
   }
   __syncwarp();  // hist and the staged row are free again
 }
 
-// default_energy (batching.py:110-115) of row i of the carved frame, incrementally: a pixel's
-// Sobel value changes only if a removed pixel of rows i-1..i+1 lay within one column of it.
-// `lum`/`gra` are the frame's planes, off = the batch's offset in the removed-column log.
-// The three rows' removed-column lists are staged in the warp's shared memory (`stage`, 3 x
-// kDirtyCap entries) when they fit, so the binary searches below do not chain global loads.
 constexpr int kDirtyCap = 256;
-__device__ __forceinline__ void dirty_row(const CarveRun& R, const uint8_t* lum, uint8_t* gra, int i, int b, int wn,
-                                          int off, int16_t* stage) {
+// la / lb / lc: the compacted luma rows i-1, i, i+1 (clamped), gr: the gradient row i to patch;
+// ra / ri / rc: the batch's removed columns of those rows (b each, ascending, w0 frame).
+__device__ __forceinline__ void dirty_row_at(const uint8_t* la, const uint8_t* lb, const uint8_t* lc, uint8_t* gr,
+                                             const int16_t* ra, const int16_t* ri, const int16_t* rc, int b, int wn,
+                                             bool tiny, int16_t* stage) {
   const int lane = threadIdx.x & 31;
-  const int rows = R.rows;
   const int w0 = wn + b;
-  uint8_t* gr = gra + (long)i * R.pitch;
-  if (rows < 3 || wn < 3) {
+  if (tiny) {  // fewer than 3 rows or columns: zero energy (default_energy)
     for (int y = lane; y < wn; y += 32) gr[y] = 0;
     return;
   }
-  const int ia = max(i - 1, 0), ib = min(i + 1, rows - 1);
-  const int16_t* ra = R.rem + (long)ia * R.rem_cap + off;
-  const int16_t* ri = R.rem + (long)i * R.rem_cap + off;
-  const int16_t* rc = R.rem + (long)ib * R.rem_cap + off;
   if (b <= kDirtyCap) {
     for (int t = lane; t < b; t += 32) {
       const int16_t va = ra[t], vi = ri[t], vc = rc[t];
@@ -909,9 +938,6 @@ __device__ __forceinline__ void dirty_row(const CarveRun& R, const uint8_t* lum,
     ri = stage + kDirtyCap;
     rc = stage + 2 * kDirtyCap;
   }
-  const uint8_t* la = lum + (long)ia * R.pitch;
-  const uint8_t* lb = lum + (long)i * R.pitch;
-  const uint8_t* lc = lum + (long)ib * R.pitch;
   for (int q = lane; q < 9 * b; q += 32) {
     const int rsel = q / (3 * b), rem = q - rsel * 3 * b;
     const int s = rem / 3, offc = rem - s * 3 - 1;
@@ -930,6 +956,21 @@ __device__ __forceinline__ void dirty_row(const CarveRun& R, const uint8_t* lum,
     const int gv = abs(gx) + abs(gy);
     gr[y] = (uint8_t)(gv > 255 ? 255 : gv);
   }
+  __syncwarp();  // the staged lists are free again
+}
+
+// default_energy (batching.py:110-115) of row i of the carved frame, incrementally: a pixel's
+// Sobel value changes only if a removed pixel of rows i-1..i+1 lay within one column of it.
+// `lum`/`gra` are the frame's planes, off = the batch's offset in the removed-column log.
+// The three rows' removed-column lists are staged in the warp's shared memory (`stage`, 3 x
+// kDirtyCap entries) when they fit, so the binary searches do not chain global loads.
+__device__ __forceinline__ void dirty_row(const CarveRun& R, const uint8_t* lum, uint8_t* gra, int i, int b, int wn,
+                                          int off, int16_t* stage) {
+  const int rows = R.rows;
+  const int ia = max(i - 1, 0), ib = min(i + 1, rows - 1);
+  dirty_row_at(lum + (long)ia * R.pitch, lum + (long)i * R.pitch, lum + (long)ib * R.pitch, gra + (long)i * R.pitch,
+               R.rem + (long)ia * R.rem_cap + off, R.rem + (long)i * R.rem_cap + off,
+               R.rem + (long)ib * R.rem_cap + off, b, wn, rows < 3 || wn < 3, stage);
 }
 
 // One DP pass + select + trace for every active run (one cluster per run).  Per-run state
@@ -956,6 +997,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
   const int plane = 0;  // planes are compacted in place
   long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tp = clock64();
+  if (R.prof && rank == 0 && tid == 0 && iters < 500) R.prof[32 + 2 * iters] = (long long)globaltimer_ns();
 
   const int per = ((w + CL - 1) / CL + 15) & ~15;
   const int ndp = min(kMaxWarps, (per + kOwn - 1) / kOwn);
@@ -1219,8 +1261,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun*
     Rg.removed = removed + b;
     Rg.cyc_dp += t_dp;
     Rg.cyc_sel += clock64() - tp;
-    if (R.prof)
+    if (R.prof) {
       for (int k = 0; k < 8; ++k) R.prof[4 + k] += dprof[k];
+      if (iters < 500) R.prof[33 + 2 * iters] = (long long)globaltimer_ns();
+    }
   }
 }
 
@@ -1247,7 +1291,8 @@ __global__ void __launch_bounds__(kCompWarps * 32) carve_compact_kernel(CarveRun
     fence_mbar_init();
     compact_issue(L, G, R.width + b, sL, sG, bar);
   }
-  compact_row(L, G, R.rem + (long)i * R.rem_cap + (R.removed - b), b, R.width, sL, sG, hist, bar, 0);
+  int16_t* rs = reinterpret_cast<int16_t*>(base + compact_warp_bytes(pitch) - 2 * kRowListCap);
+  compact_row(L, G, R.rem + (long)i * R.rem_cap + (R.removed - b), b, R.width, sL, sG, hist, bar, 0, nullptr, rs);
 }
 
 __global__ void __launch_bounds__(kRowWarps * 32) carve_dirty_kernel(CarveRun* __restrict__ runs) {
