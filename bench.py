@@ -300,6 +300,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--split-runs", action="store_true",
+                    help="one clip across the GPUs (sharding.py: every rank scans, carves its runs, "
+                         "outputs exchanged by NCCL broadcasts); strong scaling")
     a = ap.parse_args()
     world, rank, local = dist_setup()
     if a.impl == "reference":
@@ -316,7 +319,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     name = a.config
-    clip, tw, th = rank_workload(name, rank, a.frames)
+    split = a.split_runs and world > 1
+    clip, tw, th = rank_workload(name, 0 if split else rank, a.frames)
     T, H, W, C = clip.shape
     tw = tw or W
     th = th or H
@@ -333,8 +337,15 @@ def main():
     def max_over_ranks(x: float) -> float:
         return reduce_max(x, world, "cuda")
 
+    from paper_1903_03180_b200 import sharding
+
+    def step(clip_dev):
+        if split:
+            return sharding.retarget_clip_sharded(clip_dev, cfg)
+        return P.retarget_video_tensor(clip_dev, cfg)
+
     for _ in range(a.warmup):
-        out, m = P.retarget_video_tensor(dev, cfg)
+        out, m = step(dev)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region
@@ -347,31 +358,44 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(a.steps):
-            out, m = P.retarget_video_tensor(dev, cfg)
+            out, m = step(dev)
             phases.append(dict(pipeline.last_phase_ms))
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         launches = (lib.scpl_kernel_launches() - launches0) / a.steps
     ms = max_over_ranks(e0.elapsed_time(e1) / a.steps)
-    value = world * T / (ms / 1e3)
+    value = (1 if split else world) * T / (ms / 1e3)
 
     # ---- end to end through the public API with host buffers
     e2e = None
     if not a.no_e2e:
         host_out = torch.empty((T, th, tw, C), dtype=torch.uint8, pin_memory=True)
+
+        def e2e_step():
+            if not split:
+                return P.retarget_video(host_in, cfg, out=host_out)
+            # one clip across the ranks: every rank copies it in, carves its runs; after the
+            # exchange rank 0 copies the whole output back
+            dev.copy_(host_in, non_blocking=True)
+            res, m_ = sharding.retarget_clip_sharded(dev, cfg)
+            if rank == 0:
+                host_out.copy_(res, non_blocking=True)
+            return host_out, m_
+
         for _ in range(1):
-            P.retarget_video(host_in, cfg, out=host_out)
+            e2e_step()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(a.steps):
-            host_out, _m = P.retarget_video(host_in, cfg, out=host_out)
+            host_out, _m = e2e_step()
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / a.steps)
         barrier()
-        e2e = {"value": world * T / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(host_in.numel()), "d2h_bytes_per_step": int(host_out.numel())}
+        e2e = {"value": (1 if split else world) * T / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(host_in.numel()),
+               "d2h_bytes_per_step": int(host_out.numel()) if (rank == 0 or not split) else 0}
 
     if rank != 0:
         if world > 1:
@@ -400,12 +424,13 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if split else "weak", "vs_baseline": None,
         "dtype": "u8/f64", "data": "synthetic",
         "config": {"workload": workload(name) if a.frames is None else f"{name} (first {T} frames)",
                    "frames_per_step": T, "runs": len(m.runs),
                    "dp_passes": m.dp_passes, "l2": "inputs (1.87 GB/clip) larger than L2",
-                   "parallelism": f"clip-per-GPU x{world}"},
+                   "parallelism": (f"one clip, runs split over {world} GPUs (every rank scans; outputs "
+                                   f"exchanged by NCCL broadcasts)" if split else f"clip-per-GPU x{world}")},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": pass_roofline(dict(ph, dp_passes=m.dp_passes), H, W, tw, peak, peak_src),

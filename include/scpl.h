@@ -105,6 +105,10 @@ typedef struct {
   const double* phi;  /* host, max_len+1 entries: threshold(n, policy) as the reference computes it */
   int spec_len;       /* window candidates evaluated per stats launch (0 = default) */
   int reaverage;      /* RetargetConfig.reaverage_energy (pipeline.py:269-270, 280-296) */
+  int shard_rank;     /* multi-GPU split of ONE clip: every rank computes the codes and */
+  int shard_count;    /* the whole buffer scan, then carves and replays only the runs r with
+                         r % shard_count == shard_rank (scpl/raw: a contiguous block of frames);
+                         other runs' output frames are left untouched.  0 or 1: all runs */
 } scpl_video_params;
 
 typedef struct {

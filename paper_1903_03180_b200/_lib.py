@@ -26,6 +26,7 @@ class VideoParams(ctypes.Structure):
         ("height_first", ctypes.c_int), ("max_len", ctypes.c_int),
         ("w_motion", ctypes.c_double), ("w_grad", ctypes.c_double),
         ("phi", ctypes.POINTER(ctypes.c_double)), ("spec_len", ctypes.c_int), ("reaverage", ctypes.c_int),
+        ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
     ]
 
 

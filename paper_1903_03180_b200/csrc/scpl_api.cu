@@ -705,6 +705,9 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   SCPL_ARG(P.mode >= 0 && P.mode <= 2, "unknown mode");
   SCPL_ARG(P.max_len >= 1, "max_len must be >= 1");
   SCPL_ARG(P.mode != 2 || P.phi != nullptr, "phi table required for buffered mode");
+  SCPL_ARG(P.shard_count <= 1 || (P.shard_rank >= 0 && P.shard_rank < P.shard_count),
+           "shard_rank must be in 0 .. shard_count-1");
+  const int shards = std::max(1, P.shard_count);
   result->dp_passes = 0;
   result->n_runs = 0;
   for (float& x : result->phase_ms) x = 0.f;
@@ -968,14 +971,19 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       SCPL_CUDA(cudaEventSynchronize(ev_chunk[c]));
       const int n = scan.h_n[c];
       for (int r = (int)runs.size(); r < n; ++r) runs.push_back({scan.h_runs[2 * r], scan.h_runs[2 * r + 1]});
-      if (n - done >= min_group || (c + 1 == nchunk && n > done)) {
+      if (shards > 1) {  // this rank's runs (round-robin by run index), each as it closes
+        for (int r = done; r < n; ++r)
+          if (r % shards == P.shard_rank) dispatch(r, r + 1, ev_chunk[c]);
+        done = n;
+      } else if (n - done >= min_group || (c + 1 == nchunk && n > done)) {
         dispatch(done, n, ev_chunk[c]);
         done = n;
       }
     }
   } else {
     for (int t = 0; t < T; ++t) runs.push_back({t, 1});
-    dispatch(0, T, ev_scan);
+    // sharded: a contiguous block of frames per rank
+    dispatch((int)((long)T * P.shard_rank / shards), (int)((long)T * (P.shard_rank + 1) / shards), ev_scan);
   }
   SCPL_CUDA(cudaStreamWaitEvent(st, ev_scan, 0));
   for (Group& G : groups) {

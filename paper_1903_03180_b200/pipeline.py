@@ -92,8 +92,10 @@ def _phi_table(policy: BufferPolicy):
     return (ctypes.c_double * len(vals))(*vals)
 
 
-def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
+def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None, shard=(0, 1)):
     """Call libscpl on a uint8 clip (T, H, W, C); returns (out, dp, runs).
+
+    shard = (rank, count): carve only this rank's runs (sharding.py); dp counts those runs.
 
     A CUDA clip goes through scpl_retarget_video (device in, device out).  A host clip goes
     through scpl_retarget_video_host, which streams it in chunks, overlaps the copies with the
@@ -114,7 +116,8 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
     phi = _phi_table(config.policy)
     params = _lib.VideoParams(tw, th, _MODE_ID[config.mode], int(config.height_first), config.policy.max_len,
                               float(config.w_motion), float(config.w_grad),
-                              ctypes.cast(phi, ctypes.POINTER(ctypes.c_double)), 0, int(config.reaverage_energy))
+                              ctypes.cast(phi, ctypes.POINTER(ctypes.c_double)), 0, int(config.reaverage_energy),
+                              int(shard[0]), int(shard[1]))
     starts = (ctypes.c_int * max(T, 1))()
     lens = (ctypes.c_int * max(T, 1))()
     res = _lib.VideoResult(0, 0, ctypes.cast(starts, ctypes.POINTER(ctypes.c_int)),
@@ -142,8 +145,11 @@ def _run_device(clip, config: RetargetConfig, tw: int, th: int, out=None):
 last_phase_ms: dict = {}   # device time per phase of the last clip (bench instrumentation)
 
 
-def retarget_video_tensor(clip, config: RetargetConfig, out=None):
-    """Device-resident variant: clip is a CUDA uint8 tensor (T,H,W[,C]); returns (tensor, RunMetrics)."""
+def retarget_video_tensor(clip, config: RetargetConfig, out=None, shard=None):
+    """Device-resident variant: clip is a CUDA uint8 tensor (T,H,W[,C]); returns (tensor, RunMetrics).
+
+    shard = (rank, count) (extension, sharding.py): the whole scan runs, but only this rank's runs
+    are carved and written; RunMetrics.dp_passes then counts those runs only."""
     start = time.perf_counter()
     if clip.dim() not in (3, 4):
         raise ValueError(f"expected a (T, H, W[, C]) clip, got shape {tuple(clip.shape)}")
@@ -155,7 +161,7 @@ def retarget_video_tensor(clip, config: RetargetConfig, out=None):
     H, W = clip.shape[1:3]
     tw = _resolve_target(W, config.target_width, "width")
     th = _resolve_target(H, config.target_height, "height")
-    out, dp, runs = _run_device(clip.contiguous(), config, tw, th, out=out)
+    out, dp, runs = _run_device(clip.contiguous(), config, tw, th, out=out, shard=shard or (0, 1))
     if clip.dim() == 3 and out.dim() == 4:
         out = out[..., 0]
     return out, RunMetrics(dp_passes=dp, wall_time=time.perf_counter() - start, frames_out=T, runs=runs)

@@ -414,3 +414,31 @@ def test_scan_screening_modes_match(P, mode, monkeypatch):
             assert ph["scan_fallbacks"] * 10 <= ph["scan_windows"], ph
         else:
             assert ph["scan_fallbacks"] == 0
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_clip_matches_reference(P, world):
+    """One clip split across `world` ranks (sharding.py): each rank scans the whole clip and
+    carves only its runs; the union of the ranks' outputs is the reference's clip and their
+    passes add up to its dp_passes.  (The ranks run one after another on one GPU here: they
+    never wait on each other, so this is exactly what each GPU of a multi-GPU job computes.)"""
+    from paper_1903_03180_b200 import sharding
+    from paper_1903_03180_b200.synth import config_clip
+    import torch
+    for name in ("C4_clip0", "C5"):
+        g = json.load(open(_config_golden(name)[0]))
+        clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
+        dev = torch.from_numpy(clip).cuda()
+        cfg = P.RetargetConfig(target_width=tw, target_height=th, mode="buffered")
+        merged = np.zeros((clip.shape[0],) + tuple(g["out_shape"]), dtype=np.uint8)
+        dp = 0
+        for rank in range(world):
+            out, m = P.retarget_video_tensor(dev, cfg, shard=(rank, world))
+            assert [list(r) for r in m.runs] == g["runs"]
+            dp += m.dp_passes
+            host = out.cpu().numpy()
+            for s, n in sharding.owned_spans(m.runs, rank, world, "buffered", clip.shape[0]):
+                merged[s:s + n] = host[s:s + n]
+        assert dp == g["dp_passes"]
+        bad = [t for t in range(merged.shape[0]) if sha(merged[t]) != g["frames_sha"][t]]
+        assert not bad, f"{name}: {len(bad)} frames differ"
