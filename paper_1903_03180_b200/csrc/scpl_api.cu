@@ -721,8 +721,8 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   const bool host_in = frames_host != nullptr, host_out = out_host != nullptr;
   const bool buffered = P.mode == 2;
   // Priorities: the scan feeds everything (it releases the runs), so codes and scan get the
-  // highest; carve groups get higher priorities the later they start -- the last group is
-  // the critical path, the early ones have slack, and the carve passes compete for whole SMs.
+  // highest; carve groups are ordered by start frame (see dispatch) -- the carve passes
+  // compete for whole SMs.
   // Levels: prio_hi (scan) .. prio_lo; carve groups use prio_hi+1 .. prio_lo (or all if the
   // range is tiny), kStreamsPerLevel streams each.
   if (!ctx->prio_known) {
@@ -876,7 +876,12 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     Group& G = groups.emplace_back();
     {  // later groups (by first frame) on higher-priority streams
       const int ta0 = runs[r0].first;
-      const int level = std::min(nlevels - 1, (int)((long)ta0 * nlevels / std::max(T, 1)));
+      int level = std::min(nlevels - 1, (int)((long)ta0 * nlevels / std::max(T, 1)));
+      // a device clip's runs are all closed within the scan, and then every group competes for
+      // SMs: the earliest groups go first (measured ~2% faster on C2 than the other order, and
+      // equal priorities are ~30% slower); a host clip's last group closes alone after the
+      // copies and is the critical path, so there the later groups go first
+      if (!host_in) level = nlevels - 1 - level;
       G.st = ctx->s_carve[level * kStreamsPerLevel + (next_stream++ % kStreamsPerLevel)];
     }
     cudaStream_t gs = G.st;
