@@ -47,7 +47,7 @@ constexpr int kOwn = kWin - 2 * kXRows;           // 128 owned columns per DP wa
 constexpr int kDpWarps = 4;                       // DP warps per CTA: one per SM sub-partition
 constexpr int kRingW = kWin + 16;                 // ring row: a 16-aligned superset of the window
 constexpr int kIntInf = 0x3fffffff;
-constexpr int kMaxWarps = 12;                    // 384 threads: up to 168 registers per thread
+constexpr int kMaxWarps = 8;                     // 256 threads (<= 128 registers): room on the SM for row and scan CTAs
 
 // Fine-grained DP timers (SCPL_CARVE_PROF builds only): clock64 reads and a local-memory
 // accumulator array would otherwise sit on the DP's critical path.
@@ -975,7 +975,7 @@ __device__ __forceinline__ void dirty_row(const CarveRun& R, const uint8_t* lum,
 
 // One DP pass + select + trace for every active run (one cluster per run).  Per-run state
 // (width, iters, removed) is read at entry and written back at exit.
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) carve_pass_kernel(CarveRun* __restrict__ runs, int CL) {
+__global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun* __restrict__ runs, int CL) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int ws[32];
   __shared__ __align__(8) uint64_t s_xbar[2];

@@ -84,9 +84,13 @@ constexpr float kScanSqrtDelta = 1.4143e-5f;  // > sqrt(kScanDelta)
 
 constexpr int kLeafLanes = 16;     // lanes per leaf: accumulator j = lanes j (first half) and j + 8
 constexpr int kHalfMax = 8;        // elements per lane and accumulator half (a leaf has <= 16 per accumulator)
-constexpr int kStatStages = 8;
+constexpr int kStatStages = 4;
 constexpr int kStatStageBytes = (256 / kLeafLanes) * 128 * 2;  // one CTA's pixels of one frame
-constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatStages;
+// ring, its barriers, the A / B energy tables; screened windows add (sum std~, sum bound) per
+// candidate and warp (kStatRed per candidate).  ~21 KB at spec 8: a scan CTA fits on an SM
+// next to a resident carve-pass CTA.
+constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatStages + 2 * 256 * sizeof(double);
+constexpr size_t kStatRed = 16 * sizeof(double);
 
 // numpy's leaf sum (pairwise_sum, n <= 128): r[j] = a[j] + a[j+8] + ... (sequential), then
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail elements in order.  Here lane
@@ -110,7 +114,8 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
                                                   double* __restrict__ leafsum, double* asum, double* bsum) {
   extern __shared__ __align__(128) uint8_t st_ring[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(st_ring + kStatStages * kStatStageBytes);
-  __shared__ double A[256], B[256];
+  double* A = reinterpret_cast<double*>(bars + kStatStages);
+  double* B = A + 256;
   for (int k = threadIdx.x; k < 256; k += blockDim.x) {
     A[k] = __dmul_rn(wm, (double)k);
     B[k] = __dmul_rn(wg, (double)k);
@@ -200,7 +205,7 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
   }
 
   const int g0 = lane & ~15;  // first lane of this leaf's group
-  __shared__ double red[APPROX ? kScanMaxL * 16 : 1];  // per candidate and warp: (sum std~, sum bound)
+  double* red = B + 256;  // APPROX: per candidate and warp, (sum std~, sum bound)
   for (int c = 0; c < L; ++c, ++ci) {
     const int t = s + n_acc + c;
     const int n = n_acc + c + 1;
@@ -559,7 +564,8 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   stats_smem_attr();
-  window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem, cs>>>(S, leaves, nleaves);
+  window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem + spec * kStatRed, cs>>>(
+      S, leaves, nleaves);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, cs>>>(nullptr, nleaves, vnodes, nullptr, S);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
@@ -585,7 +591,8 @@ void run_scan_host(ScanState* S, const int2* leaves, int nleaves, const PwVnode*
                               cudaMemcpyDeviceToHost, st));
     SCPL_CUDA(cudaStreamSynchronize(st));
     if (*h_L <= 0) break;
-    window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem, st>>>(S, leaves, nleaves);
+    window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem + spec * kStatRed, st>>>(
+        S, leaves, nleaves);
     SCPL_CHECK_LAUNCH();
     fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, st>>>(nullptr, nleaves, vnodes, nullptr, S);
     SCPL_CHECK_LAUNCH();
