@@ -619,27 +619,13 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
     }
     DP_PROF(4, DP_CLOCK() - tx);
     if (active) {
-      // exchange-block end: owned ce into this CTA's buffer; halo columns straight into the
-      // adjacent CTAs' buffers with st.async, completing bytes on their exchange barrier
+      // exchange-block end: owned ce into this CTA's buffer (the halo sends follow the barrier;
+      // tiny widths: cluster stores before a cluster barrier)
       T* dst = ceX + (size_t)(xc & 1) * pitch;
 #pragma unroll
       for (int k = 0; k < kC; ++k)
         if (own[k]) dst[j0 + k] = ce[k];
-      if (nb_mode) {
-        // only the CTA's first / last warp owns columns within kXRows of a CTA edge
-        if (send_lo) {
-          const uint32_t rd = map_rank_pure(dst, rank - 1), rb = map_rank_pure(&xbar[xm & 1], rank - 1);
-#pragma unroll
-          for (int k = 0; k < kC; ++k)
-            if (own[k] && j0 + k < g.cta_lo + kXRows) st_async_addr(rd + (uint32_t)((j0 + k) * sizeof(T)), ce[k], rb);
-        }
-        if (send_hi) {
-          const uint32_t rd = map_rank_pure(dst, rank + 1), rb = map_rank_pure(&xbar[xm & 1], rank + 1);
-#pragma unroll
-          for (int k = 0; k < kC; ++k)
-            if (own[k] && j0 + k >= g.cta_hi - kXRows) st_async_addr(rd + (uint32_t)((j0 + k) * sizeof(T)), ce[k], rb);
-        }
-      } else {
+      if (!nb_mode) {
 #pragma unroll 1
         for (int q = 0; q < CL; ++q) {
           if (q == (int)rank) continue;
@@ -658,6 +644,25 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");  // this CTA's DP warps' values
     else
       cluster_sync();
+    if (nb_mode && active) {
+      // halo columns straight into the adjacent CTAs' buffers with st.async, completing bytes
+      // on their exchange barrier -- after the local barrier, so the sends (edge warps only)
+      // do not hold up this CTA's other warps; only the CTA's first / last warp owns columns
+      // within kXRows of a CTA edge
+      T* dst = ceX + (size_t)(xc & 1) * pitch;
+      if (send_lo) {
+        const uint32_t rd = map_rank_pure(dst, rank - 1), rb = map_rank_pure(&xbar[xm & 1], rank - 1);
+#pragma unroll
+        for (int k = 0; k < kC; ++k)
+          if (own[k] && j0 + k < g.cta_lo + kXRows) st_async_addr(rd + (uint32_t)((j0 + k) * sizeof(T)), ce[k], rb);
+      }
+      if (send_hi) {
+        const uint32_t rd = map_rank_pure(dst, rank + 1), rb = map_rank_pure(&xbar[xm & 1], rank + 1);
+#pragma unroll
+        for (int k = 0; k < kC; ++k)
+          if (own[k] && j0 + k >= g.cta_hi - kXRows) st_async_addr(rd + (uint32_t)((j0 + k) * sizeof(T)), ce[k], rb);
+      }
+    }
     DP_PROF(6, DP_CLOCK() - tx);
     if (active && last_pbi >= 0) {
       store_pw(last_pbi, last_nr);
@@ -1268,7 +1273,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
   }
 }
 
+// Programmatic dependent launch: the row kernels and the loop check are launched while the
+// kernel before them drains (their CTAs wait here for its results), hiding a launch latency per
+// kernel boundary of every carve iteration.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(kCompWarps * 32) carve_compact_kernel(CarveRun* __restrict__ runs) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t csm[];
   const CarveRun& R = runs[blockIdx.y];
   const int b = R.b;
@@ -1296,6 +1307,7 @@ __global__ void __launch_bounds__(kCompWarps * 32) carve_compact_kernel(CarveRun
 }
 
 __global__ void __launch_bounds__(kRowWarps * 32) carve_dirty_kernel(CarveRun* __restrict__ runs) {
+  pdl_wait();
   const CarveRun& R = runs[blockIdx.y];
   const int b = R.b;
   if (b == 0 || R.width <= R.target) return;  // no further pass reads this gradient
@@ -1560,10 +1572,22 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   SCPL_CHECK_LAUNCH();
   const size_t csmem = carve_compact_smem(pitch);
   smem_optin(reinterpret_cast<const void*>(carve_compact_kernel));
-  carve_compact_kernel<<<dim3(cdiv(rows, kCompWarps), nruns, max_fr), kCompWarps * 32, csmem, st>>>(runs_d);
-  dim3 rgrid(cdiv(rows, kRowWarps), nruns, max_fr);
+  cudaLaunchAttribute pa[1];
+  pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pa[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t rc = {};
+  rc.gridDim = dim3(cdiv(rows, kCompWarps), nruns, max_fr);
+  rc.blockDim = dim3(kCompWarps * 32);
+  rc.dynamicSmemBytes = csmem;
+  rc.stream = st;
+  rc.attrs = pa;
+  rc.numAttrs = 1;
+  SCPL_CUDA(cudaLaunchKernelEx(&rc, carve_compact_kernel, runs_d));
   SCPL_CHECK_LAUNCH();
-  carve_dirty_kernel<<<rgrid, kRowWarps * 32, 0, st>>>(runs_d);
+  rc.gridDim = dim3(cdiv(rows, kRowWarps), nruns, max_fr);
+  rc.blockDim = dim3(kRowWarps * 32);
+  rc.dynamicSmemBytes = 0;
+  SCPL_CUDA(cudaLaunchKernelEx(&rc, carve_dirty_kernel, runs_d));
   SCPL_CHECK_LAUNCH();
   if (reaverage) launch_carve_mean(runs_d, nruns, rows, st);
 }
@@ -1588,6 +1612,7 @@ void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st)
 // target (bounded by max_iters: every pass removes at least one seam).
 __global__ void carve_check_kernel(const CarveRun* __restrict__ runs, int nruns, int max_iters, int* iters,
                                    cudaGraphConditionalHandle loop) {
+  pdl_wait();
   __shared__ int any;
   if (threadIdx.x == 0) any = 0;
   __syncthreads();
@@ -1621,8 +1646,18 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
   const long before = g_launches.load();
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage);
-  carve_check_kernel<<<1, 256, 0, cs>>>(runs_d, nruns, max_iters, iters_d, h);
-  SCPL_CUDA(cudaGetLastError());
+  {
+    cudaLaunchAttribute pa[1];
+    pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pa[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cc = {};
+    cc.gridDim = dim3(1);
+    cc.blockDim = dim3(256);
+    cc.stream = cs;
+    cc.attrs = pa;
+    cc.numAttrs = 1;
+    SCPL_CUDA(cudaLaunchKernelEx(&cc, carve_check_kernel, (const CarveRun*)runs_d, nruns, max_iters, iters_d, h));
+  }
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
   g_launches.store(before);  // counted per executed iteration by the caller
   cudaGraphExec_t ex;
