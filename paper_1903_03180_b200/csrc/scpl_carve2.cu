@@ -465,8 +465,8 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       for (int st = 0; st < S - 1 && st < nstage; ++st) dp_issue_stage<F64>(Rg, plane, rows, st, g.win_lo, ring, bars);
   }
   // Exchange protocol (nb_mode): exchange e alternates between two mbarriers (e & 1); a
-  // CTA announces the bytes of exchange e + 1 at the end of block e, before its own sends
-  // (for e = 0, before the cluster barrier that precedes the pass).
+  // CTA announces the bytes of exchange e + 1 at the end of block e, right after its local
+  // barrier (for e = 0, before the cluster barrier that precedes the pass).
   const uint32_t halo_bytes = nb_mode ? halo_bytes_for(w, CL, rank, (int)sizeof(T)) : 0u;
   // wait for stage st (issuing the one S-1 ahead first) and return its ring rows
   auto stage_rows = [&](int st) -> const uint8_t* {
@@ -608,15 +608,6 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       DP_PROF(2, DP_CLOCK() - tx);
       tx = DP_CLOCK();
     }
-    // announce the next exchange's bytes, then let the block's data go out.  The named
-    // barrier orders the announcement (a) after every local warp's wait on the exchange that
-    // last used this mbarrier -- otherwise a phase that completes at once (no halo bytes, or
-    // bytes already in) could advance the barrier twice past a slow waiter's parity -- and
-    // (b) before any local warp's sends, so a neighbour's complete_tx follows the expect_tx
-    if (nb_mode) {
-      if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
-      asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");
-    }
     DP_PROF(4, DP_CLOCK() - tx);
     if (active) {
       // exchange-block end: owned ce into this CTA's buffer (the halo sends follow the barrier;
@@ -640,10 +631,17 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
       }
     }
     DP_PROF(5, DP_CLOCK() - tx);
-    if (nb_mode)
-      asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");  // this CTA's DP warps' values
-    else
+    // One barrier per exchange: this CTA's DP warps' values are in its buffer, and every local
+    // warp has passed its wait on exchange e-1 (block start), so thread 0 may announce the
+    // bytes of exchange e+1 on the barrier slot e-1 used (a phase completing at once can no
+    // longer overtake a slow waiter's parity).  The announcement and the neighbours' sends
+    // may land in either order: the barrier's transaction count is signed.
+    if (nb_mode) {
+      asm volatile("bar.sync 2, %0;" ::"r"(ndp * 32) : "memory");
+      if (threadIdx.x == 0 && xb + 1 < nx) mbar_arrive_tx(&xbar[(xm + 1) & 1], halo_bytes);
+    } else {
       cluster_sync();
+    }
     if (nb_mode && active) {
       // halo columns straight into the adjacent CTAs' buffers with st.async, completing bytes
       // on their exchange barrier -- after the local barrier, so the sends (edge warps only)
