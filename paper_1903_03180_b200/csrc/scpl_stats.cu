@@ -218,7 +218,12 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
 #pragma unroll
       for (int k = 0; k <= kHalfMax; ++k) {
         if (valid(k)) {
-          const double e = energy_of(ct[off(k)], pure, A, B);
+          // the tables' products recomputed on the fp64 pipe (A[d] == fl(wm * d) exactly): no
+          // bank-conflicted table loads
+          const uint32_t code = ct[off(k)];
+          const double e = pure ? (double)(code & 255u)
+                                : fmin(__dadd_rn(__dmul_rn(wm, (double)(code >> 8)), __dmul_rn(wg, (double)(code & 255u))),
+                                       255.0);
           S[k] = __dadd_rn(S[k], e);
           Q[k] = __dadd_rn(Q[k], __dmul_rn(e, e));
           const double m = __dmul_rn(S[k], rn);
