@@ -15,7 +15,12 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libscpl.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["scpl_energy.cu", "scpl_stats.cu", "scpl_carve2.cu", "scpl_replay.cu", "scpl_tables.cu", "scpl_api.cu"]
+# (source, object, extra flags): the carve TU is compiled once per DP window width (kc6, kc4)
+SOURCES = [("scpl_energy.cu", "scpl_energy.o", []), ("scpl_stats.cu", "scpl_stats.o", []),
+           ("scpl_carve2.cu", "scpl_carve2.o", ["-DSCPL_KC=6"]),
+           ("scpl_carve2.cu", "scpl_carve2_kc4.o", ["-DSCPL_KC=4"]),
+           ("scpl_replay.cu", "scpl_replay.o", []), ("scpl_tables.cu", "scpl_tables.o", []),
+           ("scpl_api.cu", "scpl_api.o", [])]
 HEADERS = ["scpl_common.cuh", "scpl_kernels.h", os.path.join("..", "..", "include", "scpl.h")]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -31,12 +36,13 @@ def _newest(paths):
     return max(os.path.getmtime(p) for p in paths)
 
 
-def _compile(src: str, force: bool) -> str:
-    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+def _compile(entry, force: bool) -> str:
+    src, objname, extra = entry
+    obj = os.path.join(BUILD, objname)
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= _newest(deps):
         return obj
-    cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

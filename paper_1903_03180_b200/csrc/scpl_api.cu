@@ -258,12 +258,12 @@ void scan_chunk(scpl_ctx* ctx, ScanStream& S, int c, int avail, cudaStream_t st)
   else
     SCPL_CUDA(cudaGraphLaunch(S.graph, st));
   // (SM copies into mapped pinned memory: no copy-engine queueing behind the clip's copies)
-  launch_word_copy(&S.h_n[c], reinterpret_cast<uint8_t*>(ctx->scan) + offsetof(ScanState, nruns), sizeof(int), st);
-  launch_word_copy(S.h_runs, S.runs_d.p, sizeof(int) * 2 * S.T, st);
+  kc6::launch_word_copy(&S.h_n[c], reinterpret_cast<uint8_t*>(ctx->scan) + offsetof(ScanState, nruns), sizeof(int), st);
+  kc6::launch_word_copy(S.h_runs, S.runs_d.p, sizeof(int) * 2 * S.T, st);
 }
 
 void scan_end(scpl_ctx* ctx, ScanStream& S, cudaStream_t st) {
-  launch_word_copy(S.h_state, ctx->scan, sizeof(ScanState), st);
+  kc6::launch_word_copy(S.h_state, ctx->scan, sizeof(ScanState), st);
 }
 
 // after the stream is done
@@ -289,6 +289,7 @@ struct CarveSet {
   int max_fr = 1;           // most frames carved together by one run (reaverage)
   bool reaverage = false;
   bool has_uniform = false;  // U holds a uniform map for the first pass (else the mean gradient)
+  int kc = 6;                // DP window variant (scpl_carve2.cu: kc6 / kc4)
   long long prof[4] = {0, 0, 0, 0};
   scpl_ctx* ctx = nullptr;
   std::array<int, 8> loop_key{};
@@ -315,9 +316,21 @@ struct CarveSet {
   }
 };
 
+// DP window variant of a carve set: kc4 (64 owned columns per DP warp, 8 CTAs for 1080p) when
+// at most two runs carve together -- a lone run's pass chain is the critical path and SMs are
+// free -- else kc6 (128 owned columns: half the SMs per run, for many concurrent runs).
+// SCPL_CARVE_KC=4|6 forces one.
+int carve_variant(int nruns, int cols) {
+  if (const char* e = getenv("SCPL_CARVE_KC")) return atoi(e) == 4 && cols <= 8 * 4 * 64 ? 4 : 6;
+  return nruns <= 2 && cols <= 8 * 4 * 64 ? 4 : 6;
+}
+int carve_cluster(int kc, int nruns, int cols, int num_sms) {
+  return kc == 4 ? kc4::carve_cluster_size(nruns, cols, num_sms) : kc6::carve_cluster_size(nruns, cols, num_sms);
+}
+
 // nfr (nullable): frames carved together per run (reaverage_energy), else one each
 void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kmax, bool with_U, bool dbg,
-                 int cl, cudaStream_t st, const int* nfr = nullptr, bool reaverage = false) {
+                 int cl, cudaStream_t st, const int* nfr = nullptr, bool reaverage = false, int kc = 6) {
   SCPL_ARG(cols <= 4096, "frames wider than 4096 columns (in the carve orientation) are not supported");
   // int-pass keys hold the path cost (<= 255 per row) above 9 bits of direction data
   SCPL_ARG(rows <= 8192, "frames taller than 8192 rows (in the carve orientation) are not supported");
@@ -354,10 +367,11 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   S.max_fr = max_fr;
   S.reaverage = reaverage;
   S.has_uniform = uniform_given;
+  S.kc = kc;
   S.runs.assign(nruns, CarveRun{});
   uint8_t* base = S.mem.as<uint8_t>();
   size_t plane_off = 0;
-  const int stage = carve_stage_dtab(rows, pitch, cl) ? 1 : 0;
+  const int stage = (kc == 4 ? kc4::carve_stage_dtab(rows, pitch, cl) : kc6::carve_stage_dtab(rows, pitch, cl)) ? 1 : 0;
   for (int r = 0; r < nruns; ++r) {
     uint8_t* p = base + planes_bytes + per * r;
     auto take = [&](size_t bytes) {
@@ -396,7 +410,10 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
       R.cols = reinterpret_cast<int16_t*>(take((size_t)cols * 2));
       R.costs = reinterpret_cast<double*>(take((size_t)cols * 8));
     }
-    encode_carve_tensor_maps(R);
+    if (kc == 4)
+      kc4::encode_carve_tensor_maps(R);
+    else
+      kc6::encode_carve_tensor_maps(R);
   }
 }
 
@@ -417,7 +434,8 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   }
   const bool graph = S.cols > S.target && !host_loops();
   S.ctx = ctx;
-  S.loop_key = {nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr, (int)S.reaverage + 2 * graph};
+  S.loop_key = {nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
+                (int)S.reaverage + 2 * graph + 4 * (S.kc == 4)};
   auto it = ctx->loop_pool.find(S.loop_key);
   if (it != ctx->loop_pool.end()) {
     S.loop = it->second;
@@ -434,16 +452,17 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   int* iters_d = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(S.loop.mem) + sizeof(CarveRun) * nruns);
   std::memcpy(h_runs, S.runs.data(), sizeof(CarveRun) * nruns);
   // run states and the zeroed counter from mapped pinned memory
-  launch_word_copy(runs_d, h_runs, sizeof(CarveRun) * nruns + sizeof(int), st);
+  kc6::launch_word_copy(runs_d, h_runs, sizeof(CarveRun) * nruns + sizeof(int), st);
   if (S.reaverage && !S.has_uniform)  // first pass on the mean gradient too (pipeline.py:289-290)
-    launch_carve_mean(runs_d, nruns, S.rows, st);
+    kc6::launch_carve_mean(runs_d, nruns, S.rows, st);
   if (S.cols > S.target && host_loops()) {  // bursts of 8 iterations, host checks the widths
     int done_iters = 0;
     while (true) {
       for (int k = 0; k < 8; ++k)
-        launch_carve_iteration(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, st, S.max_fr, S.reaverage);
+        (S.kc == 4 ? kc4::launch_carve_iteration : kc6::launch_carve_iteration)(runs_d, nruns, S.rows, S.pitch, S.cols,
+                                                                               S.cl, st, S.max_fr, S.reaverage);
       done_iters += 8;
-      launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns, st);
+      kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns, st);
       SCPL_CUDA(cudaStreamSynchronize(st));
       bool all = true;
       for (int r = 0; r < nruns; ++r) all &= h_runs[r].width <= h_runs[r].target;
@@ -451,12 +470,12 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
     }
   } else if (graph) {
     if (!S.loop.ex)
-      S.loop.ex = build_carve_loop(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d,
-                                   S.max_fr, S.reaverage);
+      S.loop.ex = (S.kc == 4 ? kc4::build_carve_loop : kc6::build_carve_loop)(
+          runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage);
     SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
-  launch_carve_index(runs_d, nruns, S.rows, st);
-  launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns + sizeof(int), st);  // states + counter
+  kc6::launch_carve_index(runs_d, nruns, S.rows, st);
+  kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns + sizeof(int), st);  // states + counter
 }
 
 // after the stream is done: run states back into S.runs, launch accounting, profile
@@ -464,7 +483,7 @@ void carve_finish(CarveSet& S) {
   const int nruns = (int)S.runs.size();
   if (nruns == 0) return;
   std::memcpy(S.runs.data(), S.h_runs, sizeof(CarveRun) * nruns);
-  g_launches.fetch_add((long)carve_kernels_per_iteration(S.reaverage) * *S.h_iters, std::memory_order_relaxed);
+  g_launches.fetch_add((long)kc6::carve_kernels_per_iteration(S.reaverage) * *S.h_iters, std::memory_order_relaxed);
   for (auto& R : S.runs)
     if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;
@@ -641,9 +660,11 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
     SCPL_ARG(target <= w, "target width exceeds frame width");
     SCPL_ARG(h >= 1 && w >= 1, "empty frame");
     CarveSet S;
-    carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, carve_cluster_size(1, w, ctx->num_sms), st);
+    const int kc = carve_variant(1, w);
+    carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, carve_cluster(kc, 1, w, ctx->num_sms), st, nullptr,
+                false, kc);
     CarveRun& R = S.runs[0];
-    launch_run_setup(frame, h, w, channels, 0, nullptr, R, st);
+    kc6::launch_run_setup(frame, h, w, channels, 0, nullptr, R, st);
     if (energy)
       SCPL_CUDA(cudaMemcpy2DAsync(const_cast<double*>(R.U), sizeof(double) * R.pitch, energy, sizeof(double) * w,
                                   sizeof(double) * w, h, cudaMemcpyDeviceToDevice, st));
@@ -916,8 +937,9 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       std::vector<int> nfr;
       if (rea)
         for (int r = r0; r < r1; ++r) nfr.push_back(runs[r].second);
+      const int kc = carve_variant(nr, cols);
       carve_alloc(S, nr, rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
-                  carve_cluster_size(nr, cols, ctx->num_sms), gs, rea ? nfr.data() : nullptr, rea);
+                  carve_cluster(kc, nr, cols, ctx->num_sms), gs, rea ? nfr.data() : nullptr, rea, kc);
       hmark("group setup");
       const size_t fbytes = (size_t)curH * curW * C;
       for (int r = r0; r < r1; ++r) {
@@ -929,7 +951,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
         for (int f = 0; f < R.nfr; ++f) {
           const uint16_t* fcodes =
               (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)(s0 + f) * h * w : nullptr;
-          launch_run_setup(cur + fbytes * (s0 + f - cur_t0), curH, curW, C, height ? 1 : 0, fcodes, R, gs, f);
+          kc6::launch_run_setup(cur + fbytes * (s0 + f - cur_t0), curH, curW, C, height ? 1 : 0, fcodes, R, gs, f);
         }
         if (with_U)
           launch_uniform(codes.as<uint16_t>(), h, w, s0, runs[r].second, 1, P.w_motion, P.w_grad, height ? 1 : 0,

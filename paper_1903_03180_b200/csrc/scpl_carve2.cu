@@ -38,12 +38,25 @@
 #include "scpl_common.cuh"
 #include "scpl_kernels.h"
 
-namespace scpl {
+// Compiled twice (build_ext.py): SCPL_KC = 6 (namespace scpl::kc6, the default: 128 owned
+// columns per DP warp, fewest SMs per run) and SCPL_KC = 4 (scpl::kc4: 64 owned columns, a third
+// fewer instructions per DP row on twice the SMs -- for runs carved alone, where SMs are free).
+#ifndef SCPL_KC
+#define SCPL_KC 6
+#endif
+#if SCPL_KC == 4
+#define SCPL_KC_NS kc4
+#else
+#define SCPL_KC_NS kc6
+#endif
 
-constexpr int kC = 6;                             // columns per lane in a DP warp window
-constexpr int kWin = 32 * kC;                     // 192-column window
+namespace scpl {
+namespace SCPL_KC_NS {
+
+constexpr int kC = SCPL_KC;                       // columns per lane in a DP warp window
+constexpr int kWin = 32 * kC;                     // 192-column window (kC = 6)
 constexpr int kXRows = 32;                        // rows between boundary exchanges (= halo)
-constexpr int kOwn = kWin - 2 * kXRows;           // 128 owned columns per DP warp
+constexpr int kOwn = kWin - 2 * kXRows;           // 128 owned columns per DP warp (kC = 6)
 constexpr int kDpWarps = 4;                       // DP warps per CTA: one per SM sub-partition
 constexpr int kRingW = kWin + 16;                 // ring row: a 16-aligned superset of the window
 constexpr int kIntInf = 0x3fffffff;
@@ -1671,4 +1684,5 @@ void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st) 
   SCPL_CHECK_LAUNCH();
 }
 
+}  // namespace SCPL_KC_NS
 }  // namespace scpl

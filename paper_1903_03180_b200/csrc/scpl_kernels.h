@@ -102,23 +102,30 @@ struct alignas(64) CarveRun {
   int b;                // size of the batch selected by the latest pass (0: none)
   long long cyc_dp, cyc_sel;  // SM cycles of the DP and select/trace phases, summed over passes
 };
-// planes of frame f of the run's stack (f > 0 only with reaverage_energy)
-void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes,
-                      const CarveRun& R, cudaStream_t st, int f = 0);
-void launch_carve_mean(CarveRun* runs_d, int nruns, int rows, cudaStream_t st);
-int carve_cluster_size(int nruns, int width, int num_sms);
-void encode_carve_tensor_maps(CarveRun& R);
-void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
-                            int max_fr = 1, bool reaverage = false);
-void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st);
-// dst/src: device or mapped pinned host memory; bytes rounded up to whole words (4-aligned)
-void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);
-// carve_kernels_per_iteration() kernels per executed iteration; iters_d counts them
-cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
-                                 int* iters_d, int max_fr = 1, bool reaverage = false);
-bool carve_stage_dtab(int rows, int pitch, int cl);
-int carve_kernels_per_iteration(bool reaverage);
-int carve_warps(int width, int cl);
+// carve launchers (scpl_carve2.cu), compiled once per DP window width: kc6 (default) and kc4
+#define SCPL_CARVE_DECLS \
+  void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes, \
+                        const CarveRun& R, cudaStream_t st, int f = 0); \
+  void launch_carve_mean(CarveRun* runs_d, int nruns, int rows, cudaStream_t st); \
+  int carve_cluster_size(int nruns, int width, int num_sms); \
+  void encode_carve_tensor_maps(CarveRun& R); \
+  void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st, \
+                              int max_fr = 1, bool reaverage = false); \
+  void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st); \
+  void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st); \
+  cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters, \
+                                   int* iters_d, int max_fr = 1, bool reaverage = false); \
+  bool carve_stage_dtab(int rows, int pitch, int cl); \
+  int carve_kernels_per_iteration(bool reaverage); \
+  int carve_warps(int width, int cl); \
+
+namespace kc6 {
+SCPL_CARVE_DECLS
+}
+namespace kc4 {
+SCPL_CARVE_DECLS
+}
+#undef SCPL_CARVE_DECLS
 
 void launch_replay(const uint8_t* in, uint8_t* out, int T, int H, int W, int C, const int16_t* idx, int stride,
                    int tw, int transposed, cudaStream_t st);
