@@ -316,13 +316,18 @@ struct CarveSet {
   }
 };
 
-// DP window variant of a carve set: kc4 (64 owned columns per DP warp, 8 CTAs for 1080p) when
-// at most two runs carve together -- a lone run's pass chain is the critical path and SMs are
-// free -- else kc6 (128 owned columns: half the SMs per run, for many concurrent runs).
-// SCPL_CARVE_KC=4|6 forces one.
-int carve_variant(int nruns, int cols) {
-  if (const char* e = getenv("SCPL_CARVE_KC")) return atoi(e) == 4 && cols <= 8 * 4 * 64 ? 4 : 6;
-  return nruns <= 2 && cols <= 8 * 4 * 64 ? 4 : 6;
+// DP window variant of a carve set: kc4 (64 owned columns per DP warp, 8 CTAs for 1080p: a third
+// fewer instructions per DP row, so a shorter pass chain) when SMs are plentiful, else kc6 (128
+// owned columns: half the SMs per run).  "Plentiful": the clip's runs, extrapolated from this
+// group's density (nruns over `span` of the T frames), would hold at most half the SMs with kc4
+// clusters -- long runs (C4, C5, a lone last run) yes, C2's burst of 4-frame runs no.  A single
+// run is always kc4.  SCPL_CARVE_KC=4|6 forces one.
+int carve_variant(int nruns, int cols, int span, int T, int num_sms) {
+  if (cols > 8 * 4 * 64) return 6;  // kc4 covers up to 2048 columns with 8 CTAs
+  if (const char* e = getenv("SCPL_CARVE_KC")) return atoi(e) == 4 ? 4 : 6;
+  if (nruns <= 1) return 4;
+  const double est_runs = (double)nruns * T / std::max(1, span);
+  return est_runs * kc4::carve_cluster_size(1, cols, num_sms) <= 0.5 * num_sms ? 4 : 6;
 }
 int carve_cluster(int kc, int nruns, int cols, int num_sms) {
   return kc == 4 ? kc4::carve_cluster_size(nruns, cols, num_sms) : kc6::carve_cluster_size(nruns, cols, num_sms);
@@ -660,7 +665,7 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
     SCPL_ARG(target <= w, "target width exceeds frame width");
     SCPL_ARG(h >= 1 && w >= 1, "empty frame");
     CarveSet S;
-    const int kc = carve_variant(1, w);
+    const int kc = carve_variant(1, w, 1, 1, ctx->num_sms);
     carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, carve_cluster(kc, 1, w, ctx->num_sms), st, nullptr,
                 false, kc);
     CarveRun& R = S.runs[0];
@@ -937,7 +942,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       std::vector<int> nfr;
       if (rea)
         for (int r = r0; r < r1; ++r) nfr.push_back(runs[r].second);
-      const int kc = carve_variant(nr, cols);
+      const int kc = carve_variant(nr, cols, tb - ta, T, ctx->num_sms);
       carve_alloc(S, nr, rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
                   carve_cluster(kc, nr, cols, ctx->num_sms), gs, rea ? nfr.data() : nullptr, rea, kc);
       hmark("group setup");
