@@ -15,10 +15,11 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libscpl.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-# (source, object, extra flags): the carve TU is compiled once per DP window width (kc6, kc4)
+# (source, object, extra flags): the carve TU is compiled once per DP window width (kc6, kc4, kc3)
 SOURCES = [("scpl_energy.cu", "scpl_energy.o", []), ("scpl_stats.cu", "scpl_stats.o", []),
            ("scpl_carve2.cu", "scpl_carve2.o", ["-DSCPL_KC=6"]),
            ("scpl_carve2.cu", "scpl_carve2_kc4.o", ["-DSCPL_KC=4"]),
+           ("scpl_carve2.cu", "scpl_carve2_kc3.o", ["-DSCPL_KC=3"]),
            ("scpl_replay.cu", "scpl_replay.o", []), ("scpl_tables.cu", "scpl_tables.o", []),
            ("scpl_api.cu", "scpl_api.o", [])]
 HEADERS = ["scpl_common.cuh", "scpl_kernels.h", os.path.join("..", "..", "include", "scpl.h")]

@@ -316,21 +316,31 @@ struct CarveSet {
   }
 };
 
-// DP window variant of a carve set: kc4 (64 owned columns per DP warp, 8 CTAs for 1080p: a third
-// fewer instructions per DP row, so a shorter pass chain) when SMs are plentiful, else kc6 (128
-// owned columns: half the SMs per run).  "Plentiful": the clip's runs, extrapolated from this
-// group's density (nruns over `span` of the T frames), would hold at most half the SMs with kc4
-// clusters -- long runs (C4, C5, a lone last run) yes, C2's burst of 4-frame runs no.  A single
-// run is always kc4.  SCPL_CARVE_KC=4|6 forces one.
-int carve_variant(int nruns, int cols, int span, int T, int num_sms) {
-  if (cols > 8 * 4 * 64) return 6;  // kc4 covers up to 2048 columns with 8 CTAs
-  if (const char* e = getenv("SCPL_CARVE_KC")) return atoi(e) == 4 ? 4 : 6;
-  if (nruns <= 1) return 4;
-  const double est_runs = (double)nruns * T / std::max(1, span);
-  return est_runs * kc4::carve_cluster_size(1, cols, num_sms) <= 0.5 * num_sms ? 4 : 6;
-}
+// DP window variants (scpl_carve2.cu compiled per width): kc6 = 128 owned columns per DP warp
+// (4 CTAs for 1080p), kc4 = 64 (8 CTAs), kc3 = 32 (15 CTAs, a non-portable cluster).  The DP row
+// is latency-bound on one warp per SM sub-partition, so narrower windows shorten a pass (fewer
+// instructions per row) at the price of SM-time.  A group takes the narrowest variant whose
+// clusters, for the clip's runs extrapolated from this group's density (nruns over `span` of
+// the T frames; a host clip's last group: just its own runs), would hold at most half the SMs --
+// kc3 only for a group of one run: long runs (C4, C5, a lone last run) go narrow, C2's burst of
+// 4-frame runs stays kc6.
+// SCPL_CARVE_KC=3|4|6 forces one.
+#define SCPL_CARVE_FN(kc, fn) ((kc) == 4 ? kc4::fn : (kc) == 3 ? kc3::fn : kc6::fn)
 int carve_cluster(int kc, int nruns, int cols, int num_sms) {
-  return kc == 4 ? kc4::carve_cluster_size(nruns, cols, num_sms) : kc6::carve_cluster_size(nruns, cols, num_sms);
+  return SCPL_CARVE_FN(kc, carve_cluster_size)(nruns, cols, num_sms);
+}
+int carve_variant(int nruns, int cols, int span, int T, int num_sms, bool final_group) {
+  const bool fit4 = cols <= 8 * 4 * 64, fit3 = cols <= 16 * 4 * 32;
+  if (const char* e = getenv("SCPL_CARVE_KC")) {
+    const int k = atoi(e);
+    return k == 3 && fit3 ? 3 : (k == 3 || k == 4) && fit4 ? 4 : 6;
+  }
+  // the last group of a clip (scan finished) carves with nothing left to come
+  const double est_runs = final_group ? (double)nruns : (double)nruns * T / std::max(1, span);
+  auto fits = [&](int kc) { return est_runs * carve_cluster(kc, 1, cols, num_sms) <= 0.5 * num_sms; };
+  if (nruns <= 1 && fit3 && fits(3)) return 3;
+  if (fit4 && fits(4)) return 4;
+  return 6;
 }
 
 // nfr (nullable): frames carved together per run (reaverage_energy), else one each
@@ -376,7 +386,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   S.runs.assign(nruns, CarveRun{});
   uint8_t* base = S.mem.as<uint8_t>();
   size_t plane_off = 0;
-  const int stage = (kc == 4 ? kc4::carve_stage_dtab(rows, pitch, cl) : kc6::carve_stage_dtab(rows, pitch, cl)) ? 1 : 0;
+  const int stage = SCPL_CARVE_FN(kc, carve_stage_dtab)(rows, pitch, cl) ? 1 : 0;
   for (int r = 0; r < nruns; ++r) {
     uint8_t* p = base + planes_bytes + per * r;
     auto take = [&](size_t bytes) {
@@ -415,10 +425,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
       R.cols = reinterpret_cast<int16_t*>(take((size_t)cols * 2));
       R.costs = reinterpret_cast<double*>(take((size_t)cols * 8));
     }
-    if (kc == 4)
-      kc4::encode_carve_tensor_maps(R);
-    else
-      kc6::encode_carve_tensor_maps(R);
+    SCPL_CARVE_FN(kc, encode_carve_tensor_maps)(R);
   }
 }
 
@@ -440,7 +447,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   const bool graph = S.cols > S.target && !host_loops();
   S.ctx = ctx;
   S.loop_key = {nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
-                (int)S.reaverage + 2 * graph + 4 * (S.kc == 4)};
+                (int)S.reaverage + 2 * graph + 4 * S.kc};
   auto it = ctx->loop_pool.find(S.loop_key);
   if (it != ctx->loop_pool.end()) {
     S.loop = it->second;
@@ -464,8 +471,8 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
     int done_iters = 0;
     while (true) {
       for (int k = 0; k < 8; ++k)
-        (S.kc == 4 ? kc4::launch_carve_iteration : kc6::launch_carve_iteration)(runs_d, nruns, S.rows, S.pitch, S.cols,
-                                                                               S.cl, st, S.max_fr, S.reaverage);
+        SCPL_CARVE_FN(S.kc, launch_carve_iteration)(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, st, S.max_fr,
+                                                    S.reaverage);
       done_iters += 8;
       kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns, st);
       SCPL_CUDA(cudaStreamSynchronize(st));
@@ -475,8 +482,8 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
     }
   } else if (graph) {
     if (!S.loop.ex)
-      S.loop.ex = (S.kc == 4 ? kc4::build_carve_loop : kc6::build_carve_loop)(
-          runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage);
+      S.loop.ex = SCPL_CARVE_FN(S.kc, build_carve_loop)(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl,
+                                                        S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage);
     SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
   kc6::launch_carve_index(runs_d, nruns, S.rows, st);
@@ -665,7 +672,7 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
     SCPL_ARG(target <= w, "target width exceeds frame width");
     SCPL_ARG(h >= 1 && w >= 1, "empty frame");
     CarveSet S;
-    const int kc = carve_variant(1, w, 1, 1, ctx->num_sms);
+    const int kc = carve_variant(1, w, 1, 1, ctx->num_sms, true);
     carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, carve_cluster(kc, 1, w, ctx->num_sms), st, nullptr,
                 false, kc);
     CarveRun& R = S.runs[0];
@@ -897,7 +904,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   // 3. carve + replay, one run group at a time as runs close
   std::vector<std::pair<int, int>> runs;
   int next_stream = 0;
-  auto dispatch = [&](int r0, int r1, cudaEvent_t ready) {
+  auto dispatch = [&](int r0, int r1, cudaEvent_t ready, bool final_group) {
     if (r1 <= r0) return;
     Group& G = groups.emplace_back();
     {  // later groups (by first frame) on higher-priority streams
@@ -942,7 +949,7 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       std::vector<int> nfr;
       if (rea)
         for (int r = r0; r < r1; ++r) nfr.push_back(runs[r].second);
-      const int kc = carve_variant(nr, cols, tb - ta, T, ctx->num_sms);
+      const int kc = carve_variant(nr, cols, tb - ta, T, ctx->num_sms, final_group);
       carve_alloc(S, nr, rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
                   carve_cluster(kc, nr, cols, ctx->num_sms), gs, rea ? nfr.data() : nullptr, rea, kc);
       hmark("group setup");
@@ -1005,17 +1012,19 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
       for (int r = (int)runs.size(); r < n; ++r) runs.push_back({scan.h_runs[2 * r], scan.h_runs[2 * r + 1]});
       if (shards > 1) {  // this rank's runs (round-robin by run index), each as it closes
         for (int r = done; r < n; ++r)
-          if (r % shards == P.shard_rank) dispatch(r, r + 1, ev_chunk[c]);
+          if (r % shards == P.shard_rank) dispatch(r, r + 1, ev_chunk[c], host_in && c + 1 == nchunk);
         done = n;
       } else if (n - done >= min_group || (c + 1 == nchunk && n > done)) {
-        dispatch(done, n, ev_chunk[c]);
+        // (a device clip's scan ends long before its groups do: only a host clip's last group,
+        // closed after the copies, carves with the GPU to itself)
+        dispatch(done, n, ev_chunk[c], host_in && c + 1 == nchunk);
         done = n;
       }
     }
   } else {
     for (int t = 0; t < T; ++t) runs.push_back({t, 1});
     // sharded: a contiguous block of frames per rank
-    dispatch((int)((long)T * P.shard_rank / shards), (int)((long)T * (P.shard_rank + 1) / shards), ev_scan);
+    dispatch((int)((long)T * P.shard_rank / shards), (int)((long)T * (P.shard_rank + 1) / shards), ev_scan, false);
   }
   SCPL_CUDA(cudaStreamWaitEvent(st, ev_scan, 0));
   for (Group& G : groups) {

@@ -46,6 +46,8 @@
 #endif
 #if SCPL_KC == 4
 #define SCPL_KC_NS kc4
+#elif SCPL_KC == 3
+#define SCPL_KC_NS kc3
 #else
 #define SCPL_KC_NS kc6
 #endif
@@ -521,8 +523,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
     }
     if constexpr (!F64) {
 #pragma unroll
-      for (int k = 0; k < kC; k += 2)
-        *reinterpret_cast<int2*>(&stg[2 * kWin + lane * kC + k]) = make_int2(ce[k] & kSumMask, ce[k + 1] & kSumMask);
+      for (int k = 0; k < kC; ++k) stg[2 * kWin + lane * kC + k] = (uint32_t)(ce[k] & kSumMask);
     }
     if (hbar) {
       if (lane == 0) {
@@ -1524,14 +1525,17 @@ int carve_dp_warps(int width, int cl) {
   return (per + kOwn - 1) / kOwn;
 }
 
+// kc3 (32 owned columns per DP warp) needs up to 16 CTAs per run: a non-portable cluster size
+constexpr int kMaxCluster = SCPL_KC == 3 ? 16 : 8;
+
 int carve_cluster_size(int nruns, int width, int num_sms) {
-  // one DP warp per SM sub-partition: kDpWarps x 128 columns per CTA, at most 8 CTAs
+  // one DP warp per SM sub-partition: kDpWarps x kOwn columns per CTA
   int cl = (width + kOwn * kDpWarps - 1) / (kOwn * kDpWarps);
   if (const char* e = getenv("SCPL_CARVE_CL")) {  // experiments: fewer CTAs, more DP warps each
     const int want = atoi(e);
-    if (want >= 1 && want <= 8 && carve_dp_warps(width, want) <= kMaxWarps) cl = want;
+    if (want >= 1 && want <= kMaxCluster && carve_dp_warps(width, want) <= kMaxWarps) cl = want;
   }
-  return cl < 1 ? 1 : (cl > 8 ? 8 : cl);
+  return cl < 1 ? 1 : (cl > kMaxCluster ? kMaxCluster : cl);
 }
 
 
@@ -1567,6 +1571,12 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   size_t smem = carve_smem_bytes(rows, pitch, stage, cl, dpw);
   SCPL_ARG(smem <= 227 * 1024, "carve plane too large for shared memory");
   smem_optin(reinterpret_cast<const void*>(carve_pass_kernel));
+  if (cl > 8) {
+    static bool nonportable = false;
+    if (!nonportable)
+      SCPL_CUDA(cudaFuncSetAttribute(carve_pass_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    nonportable = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nruns * cl);
   cfg.blockDim = dim3(kMaxWarps * 32);

@@ -125,6 +125,9 @@ SCPL_CARVE_DECLS
 namespace kc4 {
 SCPL_CARVE_DECLS
 }
+namespace kc3 {
+SCPL_CARVE_DECLS
+}
 #undef SCPL_CARVE_DECLS
 
 void launch_replay(const uint8_t* in, uint8_t* out, int T, int H, int W, int C, const int16_t* idx, int stride,
