@@ -317,7 +317,8 @@ struct CarveSet {
 };
 
 // DP window variants (scpl_carve2.cu compiled per width): kc6 = 128 owned columns per DP warp
-// (4 CTAs for 1080p), kc4 = 64 (8 CTAs), kc3 = 32 (15 CTAs, a non-portable cluster).  The DP row
+// (4 CTAs for 1080p), kc4 = 64 (8 CTAs; 15 at 4K), kc3 = 32 (15 CTAs at 1080p); more than 8
+// CTAs is a non-portable cluster size.  The DP row
 // is latency-bound on one warp per SM sub-partition, so narrower windows shorten a pass (fewer
 // instructions per row) at the price of SM-time.  A group takes the narrowest variant whose
 // clusters, for the clip's runs extrapolated from this group's density (nruns over `span` of
@@ -330,7 +331,7 @@ int carve_cluster(int kc, int nruns, int cols, int num_sms) {
   return SCPL_CARVE_FN(kc, carve_cluster_size)(nruns, cols, num_sms);
 }
 int carve_variant(int nruns, int cols, int span, int T, int num_sms, bool final_group) {
-  const bool fit4 = cols <= 8 * 4 * 64, fit3 = cols <= 16 * 4 * 32;
+  const bool fit4 = cols <= 16 * 4 * 64, fit3 = cols <= 16 * 4 * 32;
   if (const char* e = getenv("SCPL_CARVE_KC")) {
     const int k = atoi(e);
     return k == 3 && fit3 ? 3 : (k == 3 || k == 4) && fit4 ? 4 : 6;

@@ -1525,8 +1525,9 @@ int carve_dp_warps(int width, int cl) {
   return (per + kOwn - 1) / kOwn;
 }
 
-// kc3 (32 owned columns per DP warp) needs up to 16 CTAs per run: a non-portable cluster size
-constexpr int kMaxCluster = SCPL_KC == 3 ? 16 : 8;
+// the narrow variants need up to 16 CTAs per run (kc3 at 1080p, kc4 at 4K): a non-portable
+// cluster size
+constexpr int kMaxCluster = SCPL_KC <= 4 ? 16 : 8;
 
 int carve_cluster_size(int nruns, int width, int num_sms) {
   // one DP warp per SM sub-partition: kDpWarps x kOwn columns per CTA
