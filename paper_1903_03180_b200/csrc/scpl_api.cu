@@ -323,8 +323,7 @@ struct CarveSet {
 // instructions per row) at the price of SM-time.  A group takes the narrowest variant whose
 // clusters, for the clip's runs extrapolated from this group's density (nruns over `span` of
 // the T frames; a host clip's last group: just its own runs), would hold at most half the SMs --
-// kc3 only for a group of one run: long runs (C4, C5, a lone last run) go narrow, C2's burst of
-// 4-frame runs stays kc6.
+// long runs (C4, C5, a lone last run) go narrow, C2's burst of 4-frame runs stays kc6.
 // SCPL_CARVE_KC=3|4|6 forces one.
 #define SCPL_CARVE_FN(kc, fn) ((kc) == 4 ? kc4::fn : (kc) == 3 ? kc3::fn : kc6::fn)
 int carve_cluster(int kc, int nruns, int cols, int num_sms) {
@@ -339,7 +338,7 @@ int carve_variant(int nruns, int cols, int span, int T, int num_sms, bool final_
   // the last group of a clip (scan finished) carves with nothing left to come
   const double est_runs = final_group ? (double)nruns : (double)nruns * T / std::max(1, span);
   auto fits = [&](int kc) { return est_runs * carve_cluster(kc, 1, cols, num_sms) <= 0.5 * num_sms; };
-  if (nruns <= 1 && fit3 && fits(3)) return 3;
+  if (fit3 && fits(3)) return 3;
   if (fit4 && fits(4)) return 4;
   return 6;
 }
