@@ -49,6 +49,16 @@ METRIC = "retargeted frames/sec (1080p, width -25%)"
 UNIT = "frames/s"
 
 
+def metric_for(name: str) -> str:
+    """BASELINE.json's metric on its own workload (C2); the other configs name theirs."""
+    if name == "C2":
+        return METRIC
+    spec, tw, th = CONFIGS[name]
+    what = f"width {spec.width}->{tw}" if tw else f"height {spec.height}->{th}"
+    n = "64 clips x " if name == "C4" else ""
+    return f"retargeted frames/sec ({name}: {n}{spec.frames}x{spec.height}x{spec.width}, {what})"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -278,7 +288,7 @@ def run_reference(a, world, rank):
               f"({spec.height}x{spec.width} -> {th or spec.height}x{tw or spec.width}), buffered, literal replay; "
               f"step time = slowest window's compute time")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8/f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": workload(a.config), "frames_per_step": workers * fpw,
@@ -300,6 +310,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--clips", type=int, default=None, help="C4: clips per step (default 64)")
+    ap.add_argument("--scan-once", action="store_true",
+                    help="with --split-runs: rank 0 scans, runs dealt longest-first (sharding.py)")
+    ap.add_argument("--no-list-e2e", action="store_true")
     ap.add_argument("--split-runs", action="store_true",
                     help="one clip across the GPUs (sharding.py: every rank scans, carves its runs, "
                          "outputs exchanged by NCCL broadcasts); strong scaling")
@@ -320,14 +334,28 @@ def main():
 
     name = a.config
     split = a.split_runs and world > 1
-    clip, tw, th = rank_workload(name, 0 if split else rank, a.frames)
-    T, H, W, C = clip.shape
+    batch = name == "C4"  # BASELINE configs[3]: 64 clips per step, 64/N per rank, one batch call
+    from paper_1903_03180_b200 import sharding
+    from paper_1903_03180_b200.synth import C4_CLIPS
+    if batch:
+        mine = sharding.shard_clips(a.clips or C4_CLIPS, rank, world)
+        host_clips = []
+        for i in mine:
+            c, tw, th = config_clip("C4", frames=a.frames, clip=i)
+            host_clips.append(torch.from_numpy(c).pin_memory())
+            del c
+    else:
+        clip, tw, th = rank_workload(name, 0 if split else rank, a.frames)
+        host_clips = [torch.from_numpy(clip).pin_memory()]
+        del clip
+    T, H, W, C = host_clips[0].shape
     tw = tw or W
     th = th or H
     cfg = P.RetargetConfig(target_width=tw, target_height=th, mode="buffered")
-    host_in = torch.from_numpy(clip).pin_memory()
-    dev = host_in.cuda()
-    del clip
+    devs = [h.cuda() for h in host_clips]
+    host_in = host_clips[0]
+    dev = devs[0]
+    frames_per_rank = T * len(devs)
     lib = _lib.load()
 
     def barrier():
@@ -337,15 +365,22 @@ def main():
     def max_over_ranks(x: float) -> float:
         return reduce_max(x, world, "cuda")
 
-    from paper_1903_03180_b200 import sharding
-
-    def step(clip_dev):
+    def step(clips_dev):
+        if batch:
+            res = P.retarget_videos(clips_dev, cfg)
+            return res[0][0], res
         if split:
-            return sharding.retarget_clip_sharded(clip_dev, cfg)
-        return P.retarget_video_tensor(clip_dev, cfg)
+            return sharding.retarget_clip_sharded(clips_dev[0], cfg, scan_once=a.scan_once)
+        return P.retarget_video_tensor(clips_dev[0], cfg)
+
+    def total_dp(m):
+        return sum(x[1].dp_passes for x in m) if batch else m.dp_passes
+
+    def all_runs(m):
+        return sum(len(x[1].runs) for x in m) if batch else len(m.runs)
 
     for _ in range(a.warmup):
-        out, m = step(dev)
+        out, m = step(devs)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region
@@ -358,30 +393,33 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(a.steps):
-            out, m = step(dev)
+            out, m = step(devs)
             phases.append(dict(pipeline.last_phase_ms))
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         launches = (lib.scpl_kernel_launches() - launches0) / a.steps
     ms = max_over_ranks(e0.elapsed_time(e1) / a.steps)
-    value = (1 if split else world) * T / (ms / 1e3)
+    frames_job = T if split else frames_per_rank * world
+    value = frames_job / (ms / 1e3)
 
     # ---- end to end through the public API with host buffers
     e2e = None
     if not a.no_e2e:
-        host_out = torch.empty((T, th, tw, C), dtype=torch.uint8, pin_memory=True)
+        host_outs = [torch.empty((T, th, tw, C), dtype=torch.uint8, pin_memory=True) for _ in host_clips]
 
         def e2e_step():
+            if batch:
+                return P.retarget_videos(host_clips, cfg, outs=host_outs)
             if not split:
-                return P.retarget_video(host_in, cfg, out=host_out)
+                return P.retarget_video(host_in, cfg, out=host_outs[0])
             # one clip across the ranks: every rank copies it in, carves its runs; after the
             # exchange rank 0 copies the whole output back
             dev.copy_(host_in, non_blocking=True)
-            res, m_ = sharding.retarget_clip_sharded(dev, cfg)
+            res, m_ = sharding.retarget_clip_sharded(dev, cfg, scan_once=a.scan_once)
             if rank == 0:
-                host_out.copy_(res, non_blocking=True)
-            return host_out, m_
+                host_outs[0].copy_(res, non_blocking=True)
+            return host_outs[0], m_
 
         for _ in range(1):
             e2e_step()
@@ -389,13 +427,25 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(a.steps):
-            host_out, _m = e2e_step()
+            e2e_step()
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / a.steps)
         barrier()
-        e2e = {"value": (1 if split else world) * T / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(host_in.numel()),
-               "d2h_bytes_per_step": int(host_out.numel()) if (rank == 0 or not split) else 0}
+        e2e = {"value": frames_job / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(sum(h.numel() for h in host_clips)),
+               "d2h_bytes_per_step": int(sum(o.numel() for o in host_outs)) if (rank == 0 or not split) else 0,
+               "api": "retarget_videos(pinned host clips)" if batch else "retarget_video(pinned host tensor)"}
+        if not batch and not split and not a.no_list_e2e:
+            # the reference's own call shape: a list of numpy frames in, a list out (the API
+            # stacks the list into pinned memory and copies the output frames back)
+            frames_list = list(host_in.numpy())
+            P.retarget_video(frames_list, cfg)
+            t0 = time.perf_counter()
+            for _ in range(max(1, a.steps // 4)):
+                P.retarget_video(frames_list, cfg)
+            lst_ms = (time.perf_counter() - t0) * 1e3 / max(1, a.steps // 4)
+            e2e["list_api"] = {"value": T / (lst_ms / 1e3), "unit": UNIT, "ms_per_step": lst_ms,
+                               "api": "retarget_video(list of numpy frames) -> list of numpy frames"}
 
     if rank != 0:
         if world > 1:
@@ -404,7 +454,7 @@ def main():
 
     peak, peak_src = peaks()
     bpf = alg_bytes_per_frame(H, W, th, tw, C)
-    achieved = bpf * T / (ms / 1e3) / 1e9
+    achieved = bpf * frames_per_rank / (ms / 1e3) / 1e9  # per GPU
     ph = {k: statistics.mean(p[k] for p in phases) for k in phases[0]} if phases else {}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -423,20 +473,24 @@ def main():
                          f"vidcarve.retarget_video, buffered, literal replay), {secs:.1f}s"}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "metric": metric_for(name), "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if split else "weak", "vs_baseline": None,
         "dtype": "u8/f64", "data": "synthetic",
         "config": {"workload": workload(name) if a.frames is None else f"{name} (first {T} frames)",
-                   "frames_per_step": T, "runs": len(m.runs),
-                   "dp_passes": m.dp_passes, "l2": "inputs (1.87 GB/clip) larger than L2",
-                   "parallelism": (f"one clip, runs split over {world} GPUs (every rank scans; outputs "
-                                   f"exchanged by NCCL broadcasts)" if split else f"clip-per-GPU x{world}")},
+                   "frames_per_step": frames_job, "clips_per_step": len(devs) * (1 if split else world),
+                   "runs": all_runs(m), "dp_passes": total_dp(m),
+                   "l2": f"inputs ({sum(h.numel() for h in host_clips) / 1e9:.2f} GB per rank) larger than L2",
+                   "parallelism": (f"one clip, runs split over {world} GPUs ("
+                                   + ("rank 0 scans, runs dealt LPT-first" if a.scan_once else "every rank scans")
+                                   + "; outputs exchanged by NCCL broadcasts)") if split else
+                                  (f"{len(devs)} clips per GPU in one batch call x{world} GPUs" if batch
+                                   else f"clip-per-GPU x{world}")},
         "e2e": e2e,
         "gpu_launches": launches,
-        "roofline": pass_roofline(dict(ph, dp_passes=m.dp_passes), H, W, tw, peak, peak_src),
+        "roofline": pass_roofline(dict(ph, dp_passes=total_dp(m)), H, W, tw, peak, peak_src),
         "step_roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                           "frac": achieved / peak, "traffic": traffic,
-                          "scope": "whole step (all kernels); B = 6HW + 3H'W' bytes per frame",
+                          "scope": "whole step (all kernels), per GPU; B = 6HW + 3H'W' bytes per frame",
                           "peak_source": peak_src},
         "phases_ms": ph,
         "clocks": clocks.summary(),

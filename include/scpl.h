@@ -106,9 +106,17 @@ typedef struct {
   int spec_len;       /* window candidates evaluated per stats launch (0 = default) */
   int reaverage;      /* RetargetConfig.reaverage_energy (pipeline.py:269-270, 280-296) */
   int shard_rank;     /* multi-GPU split of ONE clip: every rank computes the codes and */
-  int shard_count;    /* the whole buffer scan, then carves and replays only the runs r with
-                         r % shard_count == shard_rank (scpl/raw: a contiguous block of frames);
-                         other runs' output frames are left untouched.  0 or 1: all runs */
+  int shard_count;    /* the whole buffer scan, then carves and replays only its share of the runs
+                         (longest-processing-time first over the closed runs, see sharding.py;
+                         scpl/raw: a contiguous block of frames); other runs' output frames are
+                         left untouched.  0 or 1: all runs */
+  const int* runs_in; /* host, nullable (buffered mode): (start, len) pairs of runs found by an
+                         earlier scan of the same clip (scan_only, or another rank).  The scan is
+                         skipped and exactly these runs are carved and replayed (a rank's share
+                         of a clip split across GPUs); other frames of out are left untouched */
+  int n_runs_in;
+  int scan_only;      /* 1: energy codes + buffer scan only (run boundaries in the result; out is
+                         not written and may be NULL) */
 } scpl_video_params;
 
 typedef struct {
@@ -125,6 +133,20 @@ typedef struct {
   int carve_cluster;   /* CTAs per run cluster used by the carve */
   int scan_windows;    /* buffered: windows the buffer scan evaluated (screened or exact) */
   int scan_fallbacks;  /* buffered: screened windows re-run exactly (bound inconclusive) */
+  /* Seam-dump parity mode (in: seam_dump, seam_dump_cap; out: seam_dump_used).  When seam_dump
+   * (host) is set, every carved (run, axis) appends one record -- everything batch_carve
+   * (batching.py:118-153) decides for that run's representative frame -- in little-endian
+   * sections each padded to 8 bytes:
+   *   int32 hdr[8] = {run, axis (0 width, 1 height), rows, cols, passes, removed, 0, 0}
+   *   int32 sizes[passes]             batch sizes (SeamBatch lengths)
+   *   int16 last_cols[removed]        last-row column of each seam, batches concatenated
+   *   double costs[removed]           Seam.cost
+   *   int16 offsets[rows][removed]    Seam.offsets (column per row, in the batch's frame)
+   *   int16 labels[passes][cols]      label_parents of each pass (first source_width valid)
+   * Records are in no particular order; the call fails (code 1) if seam_dump_cap is too small. */
+  void* seam_dump;
+  size_t seam_dump_cap;
+  size_t seam_dump_used;
 } scpl_video_result;
 
 /* vidcarve.pipeline.retarget_video (pipeline.py:92-137), buffered / scpl / raw modes,
@@ -140,6 +162,16 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames /*dev*/, int T, int
 int scpl_retarget_video_host(scpl_ctx* ctx, const uint8_t* frames /*host*/, int T, int h, int w, int channels,
                              const scpl_video_params* params, uint8_t* out /*host*/, scpl_video_result* result,
                              void* stream);
+
+/* Many independent clips in one call (BASELINE config C4: a batch of clips of one shape):
+ * clips[i] (dev, or host when host_buffers = 1: pinned for asynchronous copies) ->
+ * outs[i] (same kind), results[i] per clip.  Equivalent to one scpl_retarget_video(_host) call
+ * per clip, but every clip's codes and buffer scan run at once and closed runs of all clips
+ * share carve groups, so many runs are in flight on the GPU.  params is shared by all clips
+ * (shard_* / runs_in / scan_only must be unset). */
+int scpl_retarget_batch(scpl_ctx* ctx, int nclips, const uint8_t* const* clips, int T, int h, int w,
+                        int channels, const scpl_video_params* params, uint8_t* const* outs,
+                        scpl_video_result* results, int host_buffers, void* stream);
 
 /* bench.jitter (bench.py:39-57): sums[t] = sum over pixels of |luma(t+1) - luma(t)| for
  * t < T-1 (exact integers; the caller divides by h*w and averages windows as the reference). */
@@ -162,6 +194,7 @@ int scpl_trace_columns(scpl_ctx* ctx, const int8_t* back /*dev*/, int h, int w, 
 int scpl_select_batch(scpl_ctx* ctx, const double* last_row /*dev w*/, const int64_t* labels /*dev w*/, int w,
                       int k, int64_t* cols /*dev*/, double* costs /*dev*/, int* nb /*host*/, void* stream);
 /* batching.remove_batch / seams.remove_seam (batching.py:76-107, seams.py:92-105):
+ * `channels` is the pixel size in bytes (any dtype: pixels move as raw bytes);
  * rowcount[i] (dev) = distinct removed columns in row i (caller asserts == b). */
 int scpl_remove_columns(scpl_ctx* ctx, const uint8_t* in /*dev*/, int h, int w, int channels,
                         const int64_t* offsets /*dev b*h*/, int b, uint8_t* out /*dev h*(w-b)*channels*/,

@@ -182,6 +182,7 @@ class Batch:
     costs: np.ndarray
     offsets: np.ndarray
     source_width: int
+    labels: np.ndarray | None = None  # label_parents of the pass (batch_carve keeps it for parity)
 
     def __len__(self):
         return int(self.cols.size)
@@ -246,6 +247,7 @@ def batch_carve(frame, target_width: int, energy=None, kmax: int | None = None):
         else:
             labels = label_parents(back)
             b = select_batch(ce, back, labels, k=cur.shape[1] - target_width)
+            b.labels = labels
         cur = remove_batch(cur, b)
         batches.append(b)
         emap = None

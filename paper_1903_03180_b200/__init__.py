@@ -17,7 +17,7 @@ from .buffering import BufferPolicy, FixedRun, SpatioTemporalBuffer, threshold
 from .energy import MAXVAL, gradient_energy, motion_energy, to_luma
 from .media import MediaFormatError, read_clip_pinned, read_frames, retarget_stream, write_clip, write_frames
 from .pipeline import (MODES, RetargetConfig, RunMetrics, replay_batches, retarget_image, retarget_video,
-                       retarget_video_tensor)
+                       retarget_video_tensor, retarget_videos, scan_runs)
 from .quality import SYNTHETIC_KINDS, JitterReport, SyntheticSpec, compare, format_metrics, generate, jitter
 from .seams import DpTables, Seam, cumulative_energy, min_seam, remove_seam, trace_columns, transpose
 
@@ -30,6 +30,7 @@ __all__ = [
     "MAXVAL", "MODES", "BufferPolicy", "DpTables", "FixedRun", "RetargetConfig", "RunMetrics", "Seam",
     "SeamBatch", "SpatioTemporalBuffer", "batch_carve", "cumulative_energy", "default_energy",
     "gradient_energy", "label_parents", "min_seam", "motion_energy", "remove_batch", "remove_seam",
-    "replay_batches", "retarget_image", "retarget_video", "retarget_video_tensor", "select_batch",
+    "replay_batches", "retarget_image", "retarget_video", "retarget_video_tensor", "retarget_videos", "scan_runs",
+    "select_batch",
     "threshold", "to_luma", "trace_columns", "transpose",
 ]

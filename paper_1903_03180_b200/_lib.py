@@ -27,6 +27,7 @@ class VideoParams(ctypes.Structure):
         ("w_motion", ctypes.c_double), ("w_grad", ctypes.c_double),
         ("phi", ctypes.POINTER(ctypes.c_double)), ("spec_len", ctypes.c_int), ("reaverage", ctypes.c_int),
         ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
+        ("runs_in", ctypes.POINTER(ctypes.c_int)), ("n_runs_in", ctypes.c_int), ("scan_only", ctypes.c_int),
     ]
 
 
@@ -36,6 +37,7 @@ class VideoResult(ctypes.Structure):
         ("run_start", _c_int_p), ("run_len", _c_int_p), ("phase_ms", ctypes.c_float * 4),
         ("carve_cycles", ctypes.c_longlong * 4), ("carve_cluster", ctypes.c_int),
         ("scan_windows", ctypes.c_int), ("scan_fallbacks", ctypes.c_int),
+        ("seam_dump", ctypes.c_void_p), ("seam_dump_cap", ctypes.c_size_t), ("seam_dump_used", ctypes.c_size_t),
     ]
 
 
@@ -64,6 +66,9 @@ _SIGS = {
                             ctypes.POINTER(VideoParams), _vp, ctypes.POINTER(VideoResult), _vp],
     "scpl_retarget_video_host": [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                             ctypes.POINTER(VideoParams), _vp, ctypes.POINTER(VideoResult), _vp],
+    "scpl_retarget_batch": [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_int, ctypes.POINTER(VideoParams), ctypes.POINTER(_vp),
+                            ctypes.POINTER(VideoResult), ctypes.c_int, _vp],
     "scpl_cumulative_energy": [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp],
     "scpl_label_parents": [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp],
     "scpl_trace_columns": [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp, _vp],
@@ -129,9 +134,10 @@ def ctx(device: int | None = None) -> int:
         return _ctx[dev]
 
 
-def stream() -> int:
+def stream(device=None) -> int:
+    """The current torch stream of `device` (default: the current device)."""
     torch = torch_cuda()
-    return torch.cuda.current_stream().cuda_stream
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def ptr(t) -> int:

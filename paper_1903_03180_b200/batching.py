@@ -70,18 +70,23 @@ def select_batch(tables: DpTables, labels: np.ndarray, k: int | None = None) -> 
 
 
 def _remove_offsets(arr: np.ndarray, offs: np.ndarray):
-    """Remove per-row columns offs (b, h) on the GPU; returns (out, max removed per row)."""
+    """Remove per-row columns offs (b, h) on the GPU; returns (out, max removed per row).
+
+    Any dtype and channel count (the reference's removal is dtype-generic, batching.py:100-107):
+    a pixel is moved as its raw bytes, so the output keeps the input's dtype and values."""
     torch = _lib.torch_cuda()
+    arr = np.ascontiguousarray(arr)
     h, w = arr.shape[:2]
-    c = 1 if arr.ndim == 2 else arr.shape[2]
+    bpp = arr.dtype.itemsize * int(np.prod(arr.shape[2:], dtype=np.int64))  # bytes per pixel
     b = offs.shape[0]
-    src = _lib.to_device(np.ascontiguousarray(arr))
+    src = _lib.to_device(arr.view(np.uint8).reshape(h, w, bpp))
     od = _lib.to_device(np.ascontiguousarray(offs, dtype=np.int64))
-    out = torch.empty((h, w - b) + arr.shape[2:], dtype=torch.uint8, device=src.device)
+    out = torch.empty((h, w - b, bpp), dtype=torch.uint8, device=src.device)
     cnt = torch.empty(h, dtype=torch.int32, device=src.device)
-    _lib.check(_lib.load().scpl_remove_columns(_lib.ctx(), src.data_ptr(), h, w, c, od.data_ptr(), b,
+    _lib.check(_lib.load().scpl_remove_columns(_lib.ctx(), src.data_ptr(), h, w, bpp, od.data_ptr(), b,
                                                out.data_ptr(), cnt.data_ptr(), _lib.stream()))
-    return _lib.to_host(out), int(cnt.max().item()) if h else 0
+    res = _lib.to_host(out).view(arr.dtype).reshape((h, w - b) + arr.shape[2:])
+    return res, int(cnt.max().item()) if h else 0
 
 
 def remove_batch(frame: np.ndarray, batch: SeamBatch) -> np.ndarray:
@@ -128,13 +133,18 @@ def batch_carve(frame: np.ndarray, target_width: int, energy: np.ndarray | None 
         raise ValueError(f"target width {target_width} exceeds frame width {width}")
     if energy is not None and np.asarray(energy).shape != arr.shape[:2]:
         raise ValueError(f"energy map shape {np.asarray(energy).shape} does not match frame {arr.shape[:2]}")
-    if energy_fn is not default_energy:
-        raise NotImplementedError("batch_carve on the GPU recomputes the reference's default_energy only")
+    c = 1 if arr.ndim == 2 else arr.shape[2]
+    integral = arr.dtype == np.uint8 or (arr.dtype.kind in "iub" and (arr.size == 0 or (
+        int(arr.min()) >= 0 and int(arr.max()) <= 255)))
+    if energy_fn is not default_energy or c not in (1, 3) or arr.ndim > 3 or not integral:
+        # the reference loop (batching.py:144-152) over the GPU primitives, with the caller's
+        # energy function evaluated on the host each pass and its map uploaded
+        return _batch_carve_loop(arr, target_width, energy, energy_fn, kmax)
+    if arr.dtype != np.uint8:  # exact: the values are bytes; the output keeps the input's dtype
+        carved, batches = batch_carve(arr.astype(np.uint8), target_width, energy=energy, kmax=kmax)
+        return carved.astype(arr.dtype), batches
     torch = _lib.torch_cuda()
     h, w = arr.shape[:2]
-    c = 1 if arr.ndim == 2 else arr.shape[2]
-    if c not in (1, 3):
-        raise ValueError(f"unsupported channel count: expected 1 or 3, got shape {arr.shape}")
     src = _lib.to_device(np.ascontiguousarray(arr, dtype=np.uint8))
     ed = _lib.to_device(np.ascontiguousarray(energy, dtype=np.float64)) if energy is not None else None
     index = torch.empty((h, target_width), dtype=torch.int16, device=src.device)
@@ -159,6 +169,28 @@ def batch_carve(frame: np.ndarray, target_width: int, energy: np.ndarray | None 
     _lib.check(_lib.load().scpl_replay(_lib.ctx(), src.data_ptr(), 1, h, w, c, index.data_ptr(), target_width,
                                        target_width, 0, carved.data_ptr(), _lib.stream()))
     return _lib.to_host(carved), batches
+
+
+def _batch_carve_loop(arr, target_width, energy, energy_fn, kmax):
+    """batching.py:144-152 step by step: energy (the given map, then energy_fn of the carved
+    frame) -> cumulative_energy -> label_parents -> select_batch -> remove_batch, each on the GPU."""
+    from .seams import cumulative_energy, min_seam
+    cur = arr
+    emap = energy
+    batches = []
+    while cur.shape[1] > target_width:
+        if emap is None:
+            emap = energy_fn(cur)
+        tables = cumulative_energy(np.asarray(emap, dtype=np.float64))
+        if kmax == 1:  # raw mode (pipeline.py:236-242)
+            batch = SeamBatch(seams=(min_seam(tables),), source_width=int(cur.shape[1]))
+        else:
+            labels = label_parents(tables)
+            batch = select_batch(tables, labels, k=cur.shape[1] - target_width)
+        cur = remove_batch(cur, batch)
+        batches.append(batch)
+        emap = None
+    return cur, batches
 
 
 __all__ = ["SeamBatch", "label_parents", "select_batch", "remove_batch", "batch_carve", "default_energy"]

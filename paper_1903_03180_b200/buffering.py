@@ -86,6 +86,7 @@ class SpatioTemporalBuffer:
     energy_maps: list = field(default_factory=list)
     _sum: object = None
     _sum_sq: object = None
+    last_candidate_asde: float | None = None
 
     def __len__(self) -> int:
         return len(self.frames)
@@ -111,6 +112,7 @@ class SpatioTemporalBuffer:
                                       cS.data_ptr(), cQ.data_ptr(), st))
         asde = ctypes.c_double()
         _lib.check(lib.scpl_asde_from_sums(cx, cS.data_ptr(), cQ.data_ptr(), e.numel(), n, ctypes.byref(asde), st))
+        self.last_candidate_asde = float(asde.value)  # the value tested (buffering.py:118), for parity checks
         if asde.value <= threshold(n, self.policy) and n <= self.policy.max_len:
             self.frames.append(arr)
             self.energy_maps.append(emap)

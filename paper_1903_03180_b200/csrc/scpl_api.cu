@@ -23,6 +23,7 @@
 #include <map>
 #include <mutex>
 #include <set>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -35,19 +36,30 @@ using namespace scpl;
 namespace scpl {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
-void smem_optin(const void* kernel) {
+// true the first time (current device, key) is seen: per-device function attributes (one
+// process may drive several GPUs)
+bool once_per_device(const void* key) {
   static std::mutex mu;
-  static std::set<const void*> done;
-  std::lock_guard<std::mutex> lock(mu);
-  if (done.count(kernel)) return;
-  int dev = 0, optin = 0;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
   SCPL_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  return done.insert({dev, key}).second;
+}
+void smem_optin(const void* kernel) {
+  static std::mutex mu;  // (serialises the attribute calls of concurrent first launches)
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  SCPL_CUDA(cudaGetDevice(&dev));
+  static std::set<std::pair<int, const void*>> done;
+  if (done.count({dev, kernel})) return;
+  int optin = 0;
   SCPL_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   cudaFuncAttributes fa;
   SCPL_CUDA(cudaFuncGetAttributes(&fa, kernel));
   SCPL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  optin - (int)fa.sharedSizeBytes));
-  done.insert(kernel);
+  done.insert({dev, kernel});
 }
 std::atomic<long> g_launches{0};
 }  // namespace scpl
@@ -58,21 +70,26 @@ struct PwPlan {
   int nleaves = 0;
 };
 
+// A lane: what one clip in flight needs for itself -- its codes and scan streams and its
+// device-side scan state (several clips' scans run at once in a batch).
+struct ScanLane {
+  cudaStream_t s_codes = nullptr, s_scan = nullptr;
+  ScanState* scan = nullptr;  // device
+};
+
 struct scpl_ctx {
+  std::mutex mu;  // one C-ABI call at a time per context (entry points lock it)
   int device = 0;
   int num_sms = 148;
   int clock_khz = 0;  // base SM clock (queried once: the query costs milliseconds of host time)
   int prio_lo = 0, prio_hi = 0;
   bool prio_known = false;
-  cudaStream_t s_h2d = nullptr, s_codes = nullptr, s_d2h = nullptr, s_scan = nullptr;  // pipeline streams
-  double* h_asde = nullptr;  // pinned
-  int h_asde_cap = 0;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // copy streams
+  std::vector<ScanLane> lanes;
   std::map<long, PwPlan> plans;
-  // device-side buffer scan
-  ScanState* scan = nullptr;                       // device
   double* phi_d = nullptr;
   std::vector<double> phi_h;                       // contents of phi_d
-  std::map<std::pair<long, int>, cudaGraphExec_t> scan_graphs;  // (N, spec)
+  std::map<std::tuple<long, int, const void*>, cudaGraphExec_t> scan_graphs;  // (N, spec, lane state)
   uint8_t* pin = nullptr;  // pinned scratch (pinned_scratch)
   size_t pin_cap = 0;
   std::vector<cudaStream_t> s_carve;  // concurrent run groups
@@ -119,10 +136,25 @@ struct DBuf {
   }
 };
 
+// restores the calling thread's current device (the caller -- e.g. torch -- may be on another)
+struct DeviceRestore {
+  int dev = -1;
+  ~DeviceRestore() {
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+};
+
 template <class F>
 int guarded(scpl_ctx* ctx, F&& f) {
   try {
-    if (ctx) SCPL_CUDA(cudaSetDevice(ctx->device));
+    std::unique_lock<std::mutex> lock;
+    DeviceRestore restore;
+    if (ctx) {
+      lock = std::unique_lock<std::mutex>(ctx->mu);
+      SCPL_CUDA(cudaGetDevice(&restore.dev));
+      if (restore.dev == ctx->device) restore.dev = -1;
+      else SCPL_CUDA(cudaSetDevice(ctx->device));
+    }
     f();
     return 0;
   } catch (const Error& e) {
@@ -147,16 +179,6 @@ const PwPlan& plan_for(scpl_ctx* ctx, long N) {
   SCPL_CUDA(cudaMemcpy(p.leaves, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice));
   SCPL_CUDA(cudaMemcpy(p.vnodes, vnodes.data(), sizeof(PwVnode) * vnodes.size(), cudaMemcpyHostToDevice));
   return ctx->plans.emplace(N, p).first->second;
-}
-
-double* pinned_asde(scpl_ctx* ctx, int n) {
-  if (ctx->h_asde_cap < n) {
-    if (ctx->h_asde) cudaFreeHost(ctx->h_asde);
-    ctx->h_asde = nullptr;
-    SCPL_CUDA(cudaMallocHost(&ctx->h_asde, sizeof(double) * n));
-    ctx->h_asde_cap = n;
-  }
-  return ctx->h_asde;
 }
 
 // SCPL_HOST_LOOPS=1: drive the scan and carve loops from the host instead of conditional
@@ -185,6 +207,7 @@ struct ScanStream {
   DBuf ck, leafsum, partial, runs_d;
   cudaGraphExec_t graph = nullptr;
   const PwPlan* plan = nullptr;
+  ScanState* state = nullptr;  // the lane's device state
   int spec = 8;
   int* h_L = nullptr;  // pinned (host-driven loops)
   int T = 0;
@@ -193,30 +216,34 @@ struct ScanStream {
   ScanState* h_state = nullptr;
 };
 
-void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int H, int W,
+// the phi table (threshold(n), n = 0..max_len) on the device; shared by every lane of a call
+void upload_phi(scpl_ctx* ctx, const scpl_video_params& P) {
+  std::vector<double> phi(P.phi, P.phi + P.max_len + 1);
+  if (phi == ctx->phi_h) return;
+  if (ctx->phi_h.size() < phi.size()) {
+    if (ctx->phi_d) cudaFree(ctx->phi_d);
+    ctx->phi_d = nullptr;
+    SCPL_CUDA(cudaMalloc(&ctx->phi_d, sizeof(double) * phi.size()));
+  }
+  SCPL_CUDA(cudaMemcpy(ctx->phi_d, phi.data(), sizeof(double) * phi.size(), cudaMemcpyHostToDevice));
+  ctx->phi_h = phi;
+}
+
+void scan_start(scpl_ctx* ctx, ScanStream& S, ScanLane& lane, const uint16_t* codes, int T, int H, int W,
                 const scpl_video_params& P, cudaStream_t st) {
   const long N = (long)H * W;
   const PwPlan& plan = plan_for(ctx, N);
   const int spec = P.spec_len > 0 ? P.spec_len : 8;
   SCPL_ARG(spec <= 64, "spec_len must be <= 64");
-  if (!ctx->scan) SCPL_CUDA(cudaMalloc(&ctx->scan, sizeof(ScanState)));
-  std::vector<double> phi(P.phi, P.phi + P.max_len + 1);
-  if (phi != ctx->phi_h) {
-    if (ctx->phi_h.size() < phi.size()) {
-      if (ctx->phi_d) cudaFree(ctx->phi_d);
-      ctx->phi_d = nullptr;
-      SCPL_CUDA(cudaMalloc(&ctx->phi_d, sizeof(double) * phi.size()));
-    }
-    SCPL_CUDA(cudaMemcpy(ctx->phi_d, phi.data(), sizeof(double) * phi.size(), cudaMemcpyHostToDevice));
-    ctx->phi_h = phi;
-  }
-  auto key = std::make_pair(N, spec);
+  if (!lane.scan) SCPL_CUDA(cudaMalloc(&lane.scan, sizeof(ScanState)));
+  auto key = std::make_tuple(N, spec, (const void*)lane.scan);
   auto it = ctx->scan_graphs.find(key);
   if (it == ctx->scan_graphs.end())
-    it = ctx->scan_graphs.emplace(key, build_scan_graph(ctx->scan, plan.leaves, plan.nleaves, plan.vnodes, spec))
+    it = ctx->scan_graphs.emplace(key, build_scan_graph(lane.scan, plan.leaves, plan.nleaves, plan.vnodes, spec))
              .first;
   S.graph = it->second;
   S.plan = &plan;
+  S.state = lane.scan;
   S.spec = spec;
   S.T = T;
   S.ck = DBuf(sizeof(double) * 4 * N, st);
@@ -248,23 +275,21 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, const uint16_t* codes, int T, int 
   init.s = 0;
   init.n_acc = 1;
   init.init = 1;
-  launch_scan_reset(ctx->scan, init, st);
+  launch_scan_reset(S.state, init, st);
 }
 
-void scan_chunk(scpl_ctx* ctx, ScanStream& S, int c, int avail, cudaStream_t st) {
-  launch_scan_avail(ctx->scan, avail, st);
+void scan_chunk(ScanStream& S, int c, int avail, cudaStream_t st) {
+  launch_scan_avail(S.state, avail, st);
   if (host_loops())
-    run_scan_host(ctx->scan, S.plan->leaves, S.plan->nleaves, S.plan->vnodes, S.spec, S.h_L, st);
+    run_scan_host(S.state, S.plan->leaves, S.plan->nleaves, S.plan->vnodes, S.spec, S.h_L, st);
   else
     SCPL_CUDA(cudaGraphLaunch(S.graph, st));
   // (SM copies into mapped pinned memory: no copy-engine queueing behind the clip's copies)
-  kc6::launch_word_copy(&S.h_n[c], reinterpret_cast<uint8_t*>(ctx->scan) + offsetof(ScanState, nruns), sizeof(int), st);
+  kc6::launch_word_copy(&S.h_n[c], reinterpret_cast<uint8_t*>(S.state) + offsetof(ScanState, nruns), sizeof(int), st);
   kc6::launch_word_copy(S.h_runs, S.runs_d.p, sizeof(int) * 2 * S.T, st);
 }
 
-void scan_end(scpl_ctx* ctx, ScanStream& S, cudaStream_t st) {
-  kc6::launch_word_copy(S.h_state, ctx->scan, sizeof(ScanState), st);
-}
+void scan_end(ScanStream& S, cudaStream_t st) { kc6::launch_word_copy(S.h_state, S.state, sizeof(ScanState), st); }
 
 // after the stream is done
 void scan_finish(ScanStream& S, int chunks, scpl_video_result* result) {
@@ -329,14 +354,14 @@ struct CarveSet {
 int carve_cluster(int kc, int nruns, int cols, int num_sms) {
   return SCPL_CARVE_FN(kc, carve_cluster_size)(nruns, cols, num_sms);
 }
-int carve_variant(int nruns, int cols, int span, int T, int num_sms, bool final_group) {
+// est_runs: runs expected to carve at the same time as this group (the group's density over
+// the frames it covers, extrapolated to everything in flight)
+int carve_variant(double est_runs, int cols, int num_sms) {
   const bool fit4 = cols <= 16 * 4 * 64, fit3 = cols <= 16 * 4 * 32;
   if (const char* e = getenv("SCPL_CARVE_KC")) {
     const int k = atoi(e);
     return k == 3 && fit3 ? 3 : (k == 3 || k == 4) && fit4 ? 4 : 6;
   }
-  // the last group of a clip (scan finished) carves with nothing left to come
-  const double est_runs = final_group ? (double)nruns : (double)nruns * T / std::max(1, span);
   auto fits = [&](int kc) { return est_runs * carve_cluster(kc, 1, cols, num_sms) <= 0.5 * num_sms; };
   if (fit3 && fits(3)) return 3;
   if (fit4 && fits(4)) return 4;
@@ -371,7 +396,9 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
                align256((size_t)nblk * pitch) + align256((size_t)pitch * 8) + align256((size_t)rows * rem_cap * 2) +
                align256((size_t)rows * alive_pitch * 4) + align256((size_t)nblk * pitch * 2) + align256(kProfBytes) +
                (with_U ? align256(plane * 8) : 0) + align256((size_t)cols * 4) +
-               (dbg ? align256((size_t)cols * 2) + align256((size_t)cols * 8) : 0);
+               (dbg ? align256((size_t)cols * 2) + align256((size_t)cols * 8) +
+                          align256((size_t)rem_cap * cols * 2)
+                    : 0);
   S.mem = DBuf(planes_bytes + per * nruns, st);
   S.planes_bytes = planes_bytes;
   S.rows = rows;
@@ -424,6 +451,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     if (dbg) {
       R.cols = reinterpret_cast<int16_t*>(take((size_t)cols * 2));
       R.costs = reinterpret_cast<double*>(take((size_t)cols * 8));
+      R.labs = reinterpret_cast<int16_t*>(take((size_t)rem_cap * cols * 2));  // passes <= seams removed
     }
     SCPL_CARVE_FN(kc, encode_carve_tensor_maps)(R);
   }
@@ -580,7 +608,6 @@ void scpl_destroy(scpl_ctx* ctx) {
     cudaFree(kv.second.leaves);
     cudaFree(kv.second.vnodes);
   }
-  if (ctx->h_asde) cudaFreeHost(ctx->h_asde);
   if (ctx->pin) cudaFreeHost(ctx->pin);
   for (cudaStream_t x : ctx->s_carve) cudaStreamDestroy(x);
   for (auto& kv : ctx->scan_graphs) cudaGraphExecDestroy(kv.second);
@@ -590,9 +617,13 @@ void scpl_destroy(scpl_ctx* ctx) {
   }
   for (auto& pool : ctx->ev_pool)
     for (cudaEvent_t e : pool) cudaEventDestroy(e);
-  if (ctx->scan) cudaFree(ctx->scan);
+  for (auto& l : ctx->lanes) {
+    if (l.scan) cudaFree(l.scan);
+    for (cudaStream_t x : {l.s_codes, l.s_scan})
+      if (x) cudaStreamDestroy(x);
+  }
   if (ctx->phi_d) cudaFree(ctx->phi_d);
-  for (cudaStream_t x : {ctx->s_h2d, ctx->s_codes, ctx->s_d2h, ctx->s_scan})
+  for (cudaStream_t x : {ctx->s_h2d, ctx->s_d2h})
     if (x) cudaStreamDestroy(x);
   delete ctx;
 }
@@ -672,7 +703,7 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
     SCPL_ARG(target <= w, "target width exceeds frame width");
     SCPL_ARG(h >= 1 && w >= 1, "empty frame");
     CarveSet S;
-    const int kc = carve_variant(1, w, 1, 1, ctx->num_sms, true);
+    const int kc = carve_variant(1.0, w, ctx->num_sms);
     carve_alloc(S, 1, h, w, target, kmax, energy != nullptr, true, carve_cluster(kc, 1, w, ctx->num_sms), st, nullptr,
                 false, kc);
     CarveRun& R = S.runs[0];
@@ -706,23 +737,78 @@ int scpl_batch_carve(scpl_ctx* ctx, const uint8_t* frame, int h, int w, int chan
 
 namespace {
 
-// retarget_video (pipeline.py:92-137), streamed.  The clip (device buffer, or pinned host
-// buffer copied in 16-frame chunks on a copy stream) gets its energy codes and the device-
-// side buffer scan chunk by chunk; whenever the scan has closed enough runs, the host hands
-// them as one group to a carve stream: per phase (width, then height, or the reverse) a
-// run set is carved by the device-side iteration loop and replayed into the output, and
-// with host buffers the group's output frames leave on a second copy stream.  Groups carve
-// concurrently with the scan, the copies and each other (each carve is latency bound on a
-// few SMs).  Runs are independent, so the results do not depend on the grouping.
+// retarget_video (pipeline.py:92-137), streamed, for one clip or a batch of clips of one shape.
+// Every clip (device buffer, or pinned host buffer copied in 16-frame chunks on a copy stream)
+// gets its energy codes and its device-side buffer scan chunk by chunk on its own lane (codes
+// and scan streams, scan state); whenever the scans have closed enough runs, the host hands
+// them -- from any clip -- as one group to a carve stream: per phase (width, then height, or
+// the reverse) the group's runs are carved together by the device-side iteration loop and
+// replayed into their clips' outputs, and with host buffers each run's output frames leave on
+// a second copy stream.  Groups carve concurrently with the scans, the copies and each other
+// (each carve is latency bound on a few SMs).  Runs are independent, so the results do not
+// depend on the grouping.
+struct ClipJob {
+  const uint8_t* frames_dev = nullptr;
+  const uint8_t* frames_host = nullptr;
+  uint8_t* out_dev = nullptr;
+  uint8_t* out_host = nullptr;
+  scpl_video_result* result = nullptr;
+  int index = 0;
+  // state
+  const uint8_t* frames = nullptr;  // device frames
+  uint8_t* out = nullptr;           // device output
+  DBuf frames_buf, codes, out_buf;
+  ScanStream scan;
+  ScanLane* lane = nullptr;
+  std::vector<cudaEvent_t> ev_chunk_codes, ev_chunk;
+  cudaEvent_t ev_codes = nullptr, ev_scan = nullptr;
+  std::vector<std::pair<int, int>> runs;
+  int done = 0;  // runs considered for dispatch so far
+  long dp = 0;
+};
+
+struct RunRef {
+  ClipJob* job;
+  int r;  // index into job->runs
+};
+
 struct Group {
-  std::list<CarveSet> sets;
+  std::list<CarveSet> sets;  // one per carved axis, in phase order
+  std::vector<int> axes;
   std::list<DBuf> bufs;
+  std::vector<RunRef> runs;
   cudaStream_t st = nullptr;
 };
 
-void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* frames_host, int T, int h, int w,
-                   int channels, const scpl_video_params& P, uint8_t* out_dev, uint8_t* out_host,
-                   scpl_video_result* result, cudaStream_t st) {
+// append one seam-dump record (include/scpl.h, scpl_video_result) for run R of a carve set
+void dump_record(scpl_video_result* res, int run, int axis, const CarveRun& R) {
+  const int rows = R.rows, cols = R.width0, iters = R.width0 > R.target ? R.iters : 0;
+  const int removed = R.width0 > R.target ? R.removed : 0;
+  auto pad8 = [](size_t x) { return (x + 7) & ~(size_t)7; };
+  const size_t bytes = 32 + pad8(4 * (size_t)iters) + pad8(2 * (size_t)removed) + 8 * (size_t)removed +
+                       pad8(2 * (size_t)rows * removed) + pad8(2 * (size_t)iters * cols);
+  SCPL_ARG(res->seam_dump_used + bytes <= res->seam_dump_cap, "seam_dump buffer too small");
+  uint8_t* p = static_cast<uint8_t*>(res->seam_dump) + res->seam_dump_used;
+  std::memset(p, 0, bytes);
+  const int32_t hdr[8] = {run, axis, rows, cols, iters, removed, 0, 0};
+  std::memcpy(p, hdr, sizeof(hdr));
+  p += 32;
+  if (iters) SCPL_CUDA(cudaMemcpy(p, R.sizes, 4 * (size_t)iters, cudaMemcpyDeviceToHost));
+  p += pad8(4 * (size_t)iters);
+  if (removed) SCPL_CUDA(cudaMemcpy(p, R.cols, 2 * (size_t)removed, cudaMemcpyDeviceToHost));
+  p += pad8(2 * (size_t)removed);
+  if (removed) SCPL_CUDA(cudaMemcpy(p, R.costs, 8 * (size_t)removed, cudaMemcpyDeviceToHost));
+  p += 8 * (size_t)removed;
+  if (removed)  // the removed-column log is rows x rem_cap, rem_cap == removed
+    SCPL_CUDA(cudaMemcpy2D(p, 2 * (size_t)removed, R.rem, 2 * (size_t)R.rem_cap, 2 * (size_t)removed, rows,
+                           cudaMemcpyDeviceToHost));
+  p += pad8(2 * (size_t)rows * removed);
+  if (iters) SCPL_CUDA(cudaMemcpy(p, R.labs, 2 * (size_t)iters * cols, cudaMemcpyDeviceToHost));
+  res->seam_dump_used += bytes;
+}
+
+void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int w, int channels,
+                   const scpl_video_params& P, cudaStream_t st) {
   const bool timeline = getenv("SCPL_TIMELINE") != nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;  // (label, timing event)
   const auto t_host0 = std::chrono::steady_clock::now();
@@ -731,6 +817,8 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
     fprintf(stderr, "host %8.3f ms  %s\n", ms, label.c_str());
   };
+  const int njobs = (int)jobs.size();
+  SCPL_ARG(njobs >= 1, "no clips");
   SCPL_ARG(channels == 1 || channels == 3, "unsupported channel count: expected 1 or 3");
   SCPL_ARG(h >= 3 && w >= 3, "frame too small to carve");
   SCPL_ARG(P.target_width >= 1 && P.target_width <= w, "target width out of range");
@@ -740,24 +828,41 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   SCPL_ARG(P.mode != 2 || P.phi != nullptr, "phi table required for buffered mode");
   SCPL_ARG(P.shard_count <= 1 || (P.shard_rank >= 0 && P.shard_rank < P.shard_count),
            "shard_rank must be in 0 .. shard_count-1");
+  SCPL_ARG(njobs == 1 || (P.shard_count <= 1 && P.runs_in == nullptr && !P.scan_only),
+           "shard_*, runs_in and scan_only apply to single-clip calls");
+  const bool buffered = P.mode == 2;
+  const bool given = buffered && P.runs_in != nullptr;
+  const bool scan_only = P.scan_only != 0;
+  SCPL_ARG(!scan_only || (buffered && !given), "scan_only needs buffered mode without runs_in");
+  if (given) {
+    SCPL_ARG(P.n_runs_in >= 0, "n_runs_in must be >= 0");
+    for (int r = 0; r < P.n_runs_in; ++r) {
+      const int a = P.runs_in[2 * r], n = P.runs_in[2 * r + 1];
+      SCPL_ARG(a >= 0 && n >= 1 && n <= P.max_len && a + n <= T, "runs_in: run out of range");
+    }
+  }
   const int shards = std::max(1, P.shard_count);
-  result->dp_passes = 0;
-  result->n_runs = 0;
-  for (float& x : result->phase_ms) x = 0.f;
-  for (long long& x : result->carve_cycles) x = 0;
-  result->carve_cluster = 0;
-  result->scan_windows = result->scan_fallbacks = 0;
+  for (auto& J : jobs) {
+    scpl_video_result* result = J.result;
+    result->dp_passes = 0;
+    result->n_runs = 0;
+    for (float& x : result->phase_ms) x = 0.f;
+    for (long long& x : result->carve_cycles) x = 0;
+    result->carve_cluster = 0;
+    result->scan_windows = result->scan_fallbacks = 0;
+    result->seam_dump_used = 0;
+  }
   if (T <= 0) return;
   const int C = channels;
   const int tw = P.target_width, th = P.target_height;
   const size_t fbytes0 = (size_t)h * w * C;
-  const bool host_in = frames_host != nullptr, host_out = out_host != nullptr;
-  const bool buffered = P.mode == 2;
-  // Priorities: the scan feeds everything (it releases the runs), so codes and scan get the
-  // highest; carve groups are ordered by start frame (see dispatch) -- the carve passes
-  // compete for whole SMs.
-  // Levels: prio_hi (scan) .. prio_lo; carve groups use prio_hi+1 .. prio_lo (or all if the
-  // range is tiny), kStreamsPerLevel streams each.
+  const bool host_in = jobs[0].frames_host != nullptr, host_out = jobs[0].out_host != nullptr;
+  bool dump = false;
+  for (auto& J : jobs) dump |= J.result->seam_dump != nullptr;
+  // Priorities: the scans feed everything (they release the runs), so codes and scans get the
+  // highest; carve groups are ordered by position in the batch (see dispatch) -- the carve
+  // passes compete for whole SMs.  Levels: prio_hi (scan) .. prio_lo; carve groups use
+  // prio_hi+1 .. prio_lo (or all if the range is tiny), kStreamsPerLevel streams each.
   if (!ctx->prio_known) {
     SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&ctx->prio_lo, &ctx->prio_hi));
     ctx->prio_known = true;
@@ -765,11 +870,19 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   const int prio_lo = ctx->prio_lo, prio_hi = ctx->prio_hi;
   for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_d2h})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
-  for (cudaStream_t* x : {&ctx->s_codes, &ctx->s_scan})
-    if (!*x) SCPL_CUDA(cudaStreamCreateWithPriority(x, cudaStreamNonBlocking, prio_hi));
+  while ((int)ctx->lanes.size() < njobs) {
+    ScanLane l;
+    SCPL_CUDA(cudaStreamCreateWithPriority(&l.s_codes, cudaStreamNonBlocking, prio_hi));
+    SCPL_CUDA(cudaStreamCreateWithPriority(&l.s_scan, cudaStreamNonBlocking, prio_hi));
+    ctx->lanes.push_back(l);
+  }
+  for (int j = 0; j < njobs; ++j) {
+    jobs[j].lane = &ctx->lanes[j];
+    jobs[j].index = j;
+  }
   const int carve_hi = prio_lo - prio_hi >= 2 ? prio_hi + 1 : prio_hi;
   const int nlevels = prio_lo - carve_hi + 1;  // levels carve_hi .. prio_lo
-  const int kStreamsPerLevel = 4;
+  const int kStreamsPerLevel = njobs > 1 ? 8 : 4;
   while ((int)ctx->s_carve.size() < nlevels * kStreamsPerLevel) {
     const int level = (int)ctx->s_carve.size() / kStreamsPerLevel;  // 0 = lowest priority
     cudaStream_t x;
@@ -777,16 +890,19 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     ctx->s_carve.push_back(x);
   }
   std::vector<int> phases;  // 0 width, 1 height (pipeline.py:192-193, 246-277)
-  for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
-    if (ax == 0 && tw < w) phases.push_back(0);
-    if (ax == 1 && th < h) phases.push_back(1);
-  }
+  if (!scan_only)
+    for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
+      if (ax == 0 && tw < w) phases.push_back(0);
+      if (ax == 1 && th < h) phases.push_back(1);
+    }
   const int chunk = 16;
   const int nchunk = (T + chunk - 1) / chunk;
+  if (buffered && !given) upload_phi(ctx, P);
 
   // pinned scratch: scan readbacks, then per group and phase the carve-run states
-  const size_t scan_pin = 64 + ((sizeof(int) * (nchunk + 2 * (size_t)T) + 63) & ~(size_t)63) + sizeof(ScanState);
-  const size_t need = scan_pin + (phases.size() + 1) * (size_t)T * (sizeof(CarveRun) + 64) + 4096;
+  const size_t scan_pin = 64 + ((sizeof(int) * (nchunk + 2 * (size_t)T) + 63) & ~(size_t)63) + sizeof(ScanState) + 64;
+  const size_t need =
+      njobs * scan_pin + (phases.size() + 1) * (size_t)T * njobs * (sizeof(CarveRun) + 64) + 4096 * (size_t)njobs;
   uint8_t* pin = pinned_scratch(ctx, need);
   size_t pin_used = 0;
   auto pin_take = [&](size_t bytes) {
@@ -818,31 +934,30 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
     events.push_back({e, timing});
     return e;
   };
-  cudaEvent_t ev_start = new_event(true), ev_codes = new_event(true), ev_scan = new_event(true),
-              ev_end = new_event(true);
+  cudaEvent_t ev_start = new_event(true), ev_end = new_event(true);
   SCPL_CUDA(cudaEventRecord(ev_start, st));
   hmark("start recorded");
 
   // buffers (stream-ordered on st; every other stream waits for ev_alloc)
-  DBuf frames_buf, codes, out_buf;
-  const uint8_t* frames = frames_dev;
-  if (host_in) {
-    frames_buf = DBuf(fbytes0 * T, st);
-    frames = frames_buf.as<uint8_t>();
-  }
-  if (P.mode != 0) codes = DBuf(sizeof(uint16_t) * (size_t)T * h * w, st);
-  uint8_t* out = out_dev;
-  if (host_out) {
-    out_buf = DBuf((size_t)T * th * tw * C, st);
-    out = out_buf.as<uint8_t>();
-  }
-  ScanStream scan;
-  if (buffered) {
-    scan.h_n = reinterpret_cast<int*>(pin_take(sizeof(int) * nchunk));
-    scan.h_runs = reinterpret_cast<int*>(pin_take(sizeof(int) * 2 * (size_t)T));
-    scan.h_state = reinterpret_cast<ScanState*>(pin_take(sizeof(ScanState)));
-    scan.h_L = reinterpret_cast<int*>(pin_take(sizeof(int)));
-    scan_start(ctx, scan, codes.as<uint16_t>(), T, h, w, P, st);
+  for (auto& J : jobs) {
+    J.frames = J.frames_dev;
+    if (host_in) {
+      J.frames_buf = DBuf(fbytes0 * T, st);
+      J.frames = J.frames_buf.as<uint8_t>();
+    }
+    if (P.mode != 0) J.codes = DBuf(sizeof(uint16_t) * (size_t)T * h * w, st);
+    J.out = J.out_dev;
+    if (host_out && !scan_only) {
+      J.out_buf = DBuf((size_t)T * th * tw * C, st);
+      J.out = J.out_buf.as<uint8_t>();
+    }
+    if (buffered && !given) {
+      J.scan.h_n = reinterpret_cast<int*>(pin_take(sizeof(int) * nchunk));
+      J.scan.h_runs = reinterpret_cast<int*>(pin_take(sizeof(int) * 2 * (size_t)T));
+      J.scan.h_state = reinterpret_cast<ScanState*>(pin_take(sizeof(ScanState)));
+      J.scan.h_L = reinterpret_cast<int*>(pin_take(sizeof(int)));
+      scan_start(ctx, J.scan, *J.lane, J.codes.as<uint16_t>(), T, h, w, P, st);
+    }
   }
   std::list<Group> groups;
   auto mark = [&](const std::string& label, cudaStream_t sm) {
@@ -861,178 +976,237 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   cudaEvent_t ev_alloc = new_event(false);
   SCPL_CUDA(cudaEventRecord(ev_alloc, st));
 
-  // 1. frames in (host) and energy codes, chunk by chunk (the scan starts on the first chunk)
-  std::vector<cudaEvent_t> ev_chunk_codes(nchunk, nullptr);
+  // 1. frames in (host) and energy codes, chunk by chunk (each scan starts on its first chunk);
+  // clip by clip on the copy stream, so the first clips' scans start first
   if (host_in) SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
-  SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, ev_alloc, 0));
-  for (int c = 0; c < nchunk; ++c) {
-    const int t0 = c * chunk, n = std::min(chunk, T - t0);
-    if (host_in) {
-      SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(frames) + fbytes0 * t0, frames_host + fbytes0 * t0,
-                                fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
-      mark("h2d " + std::to_string(c), ctx->s_h2d);
-      cudaEvent_t e = new_event(false);
-      SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
-      SCPL_CUDA(cudaStreamWaitEvent(ctx->s_codes, e, 0));
-    }
-    if (P.mode != 0)
-      launch_codes(frames, nullptr, t0, n, h, w, C, codes.as<uint16_t>(), ctx->num_sms, ctx->s_codes);
-    ev_chunk_codes[c] = new_event(false);
-    SCPL_CUDA(cudaEventRecord(ev_chunk_codes[c], ctx->s_codes));
-  }
-  cudaStream_t ss = ctx->s_scan;
-  SCPL_CUDA(cudaStreamWaitEvent(ss, ev_alloc, 0));
-  SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[0], 0));
-  SCPL_CUDA(cudaEventRecord(ev_codes, ss));  // (first chunk's codes)
-
-  // 2. buffer scan, chunk by chunk (fixed one-frame runs for scpl / raw)
-  std::vector<cudaEvent_t> ev_chunk(nchunk, nullptr);
-  if (buffered) {
+  for (auto& J : jobs) {
+    cudaStream_t sc = J.lane->s_codes;
+    SCPL_CUDA(cudaStreamWaitEvent(sc, ev_alloc, 0));
+    J.ev_chunk_codes.assign(nchunk, nullptr);
     for (int c = 0; c < nchunk; ++c) {
-      SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[c], 0));
-      scan_chunk(ctx, scan, c, std::min(T, (c + 1) * chunk), ss);
-      mark("scan " + std::to_string(c), ss);
-      ev_chunk[c] = new_event(false);
-      SCPL_CUDA(cudaEventRecord(ev_chunk[c], ss));
+      const int t0 = c * chunk, n = std::min(chunk, T - t0);
+      if (host_in) {
+        SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(J.frames) + fbytes0 * t0, J.frames_host + fbytes0 * t0,
+                                  fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
+        if (njobs == 1) mark("h2d " + std::to_string(c), ctx->s_h2d);
+        cudaEvent_t e = new_event(false);
+        SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
+        SCPL_CUDA(cudaStreamWaitEvent(sc, e, 0));
+      }
+      if (P.mode != 0) launch_codes(J.frames, nullptr, t0, n, h, w, C, J.codes.as<uint16_t>(), ctx->num_sms, sc);
+      J.ev_chunk_codes[c] = new_event(false);
+      SCPL_CUDA(cudaEventRecord(J.ev_chunk_codes[c], sc));
     }
-    scan_end(ctx, scan, ss);
-  } else {
-    SCPL_CUDA(cudaStreamWaitEvent(ss, ev_chunk_codes[nchunk - 1], 0));
   }
-  SCPL_CUDA(cudaEventRecord(ev_scan, ss));
+  // 2. buffer scans, chunk by chunk (fixed one-frame runs for scpl / raw; given runs: none)
+  for (auto& J : jobs) {
+    cudaStream_t ss = J.lane->s_scan;
+    J.ev_codes = new_event(true);
+    J.ev_scan = new_event(true);
+    SCPL_CUDA(cudaStreamWaitEvent(ss, ev_alloc, 0));
+    SCPL_CUDA(cudaStreamWaitEvent(ss, J.ev_chunk_codes[0], 0));
+    SCPL_CUDA(cudaEventRecord(J.ev_codes, ss));  // (first chunk's codes)
+    J.ev_chunk.assign(nchunk, nullptr);
+    if (buffered && !given) {
+      for (int c = 0; c < nchunk; ++c) {
+        SCPL_CUDA(cudaStreamWaitEvent(ss, J.ev_chunk_codes[c], 0));
+        scan_chunk(J.scan, c, std::min(T, (c + 1) * chunk), ss);
+        if (njobs == 1) mark("scan " + std::to_string(c), ss);
+        J.ev_chunk[c] = new_event(false);
+        SCPL_CUDA(cudaEventRecord(J.ev_chunk[c], ss));
+      }
+      scan_end(J.scan, ss);
+    } else {
+      SCPL_CUDA(cudaStreamWaitEvent(ss, J.ev_chunk_codes[nchunk - 1], 0));
+    }
+    SCPL_CUDA(cudaEventRecord(J.ev_scan, ss));
+  }
 
   // 3. carve + replay, one run group at a time as runs close
-  std::vector<std::pair<int, int>> runs;
+  const long total_frames = (long)T * njobs;
   int next_stream = 0;
-  auto dispatch = [&](int r0, int r1, cudaEvent_t ready, bool final_group) {
-    if (r1 <= r0) return;
+  auto dispatch = [&](std::vector<RunRef> rr, const std::vector<cudaEvent_t>& ready, bool final_group) {
+    if (rr.empty()) return;
     Group& G = groups.emplace_back();
-    {  // later groups (by first frame) on higher-priority streams
-      const int ta0 = runs[r0].first;
-      int level = std::min(nlevels - 1, (int)((long)ta0 * nlevels / std::max(T, 1)));
-      // a device clip's runs are all closed within the scan, and then every group competes for
-      // SMs: the earliest groups go first (measured ~2% faster on C2 than the other order, and
-      // equal priorities are ~30% slower); a host clip's last group closes alone after the
-      // copies and is the critical path, so there the later groups go first
+    G.runs = rr;
+    const int gi = (int)groups.size() - 1;
+    long covered = 0;
+    for (auto& x : rr) covered += x.job->runs[x.r].second;
+    {  // priority level by position in the batch
+      const long pos = (long)rr[0].job->index * T + rr[0].job->runs[rr[0].r].first;
+      int level = std::min(nlevels - 1, (int)(pos * nlevels / std::max(total_frames, 1L)));
+      // device clips: every group competes for SMs once the scans are through, and the earliest
+      // groups go first (measured ~2% faster on C2 than the other order, and equal priorities
+      // are ~30% slower); a host clip's last group closes alone after the copies and is the
+      // critical path, so there the later groups go first
       if (!host_in) level = nlevels - 1 - level;
       G.st = ctx->s_carve[level * kStreamsPerLevel + (next_stream++ % kStreamsPerLevel)];
     }
     cudaStream_t gs = G.st;
     SCPL_CUDA(cudaStreamWaitEvent(gs, ev_alloc, 0));
-    SCPL_CUDA(cudaStreamWaitEvent(gs, ready, 0));
-    const int nr = r1 - r0;
-    const int ta = runs[r0].first, tb = runs[r1 - 1].first + runs[r1 - 1].second;
-    mark("group " + std::to_string(groups.size() - 1) + " start", gs);
-    auto ship = [&](size_t off, size_t bytes) {  // D2H of finished output frames
+    for (cudaEvent_t e : ready) SCPL_CUDA(cudaStreamWaitEvent(gs, e, 0));
+    const int nr = (int)rr.size();
+    mark("group " + std::to_string(gi) + " start", gs);
+    auto ship = [&](ClipJob* J, size_t off, size_t bytes) {  // D2H of finished output frames
       if (!host_out) return;
       cudaEvent_t e = new_event(false);
       SCPL_CUDA(cudaEventRecord(e, gs));
       SCPL_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
-      SCPL_CUDA(cudaMemcpyAsync(out_host + off, out + off, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
+      SCPL_CUDA(cudaMemcpyAsync(J->out_host + off, J->out + off, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
     };
     if (phases.empty()) {
-      SCPL_CUDA(cudaMemcpyAsync(out + fbytes0 * ta, frames + fbytes0 * ta, fbytes0 * (tb - ta),
-                                cudaMemcpyDeviceToDevice, gs));
-      ship(fbytes0 * ta, fbytes0 * (tb - ta));
+      for (auto& x : rr) {
+        const int s0 = x.job->runs[x.r].first, n = x.job->runs[x.r].second;
+        SCPL_CUDA(cudaMemcpyAsync(x.job->out + fbytes0 * s0, x.job->frames + fbytes0 * s0, fbytes0 * n,
+                                  cudaMemcpyDeviceToDevice, gs));
+        ship(x.job, fbytes0 * s0, fbytes0 * n);
+      }
       return;
     }
-    const uint8_t* cur = frames;
-    int cur_t0 = 0, curH = h, curW = w;
+    // per run: where its current frames are (the clip, then the previous phase's buffer)
+    std::vector<const uint8_t*> src(nr);
+    for (int k = 0; k < nr; ++k) src[k] = rr[k].job->frames + fbytes0 * rr[k].job->runs[rr[k].r].first;
+    int curH = h, curW = w;
+    const double est = final_group ? (double)nr : (double)nr * total_frames / std::max(1L, covered);
+    const int kc = carve_variant(est, (phases[0] == 1 ? h : w), ctx->num_sms);
     for (size_t ph = 0; ph < phases.size(); ++ph) {
       const bool height = phases[ph] == 1;
       const int rows = height ? curW : curH, cols = height ? curH : curW;
       const int target = height ? th : tw;
       const bool with_U = (ph == 0) && P.mode != 0;
       CarveSet& S = G.sets.emplace_back();
+      G.axes.push_back(phases[ph]);
       hmark("group alloc");
       const bool rea = P.reaverage != 0 && P.mode != 0;  // raw mode ignores it (pipeline.py:120-132)
       std::vector<int> nfr;
       if (rea)
-        for (int r = r0; r < r1; ++r) nfr.push_back(runs[r].second);
-      const int kc = carve_variant(nr, cols, tb - ta, T, ctx->num_sms, final_group);
-      carve_alloc(S, nr, rows, cols, target, P.mode == 0 ? 1 : 0, with_U, false,
-                  carve_cluster(kc, nr, cols, ctx->num_sms), gs, rea ? nfr.data() : nullptr, rea, kc);
+        for (auto& x : rr) nfr.push_back(x.job->runs[x.r].second);
+      const int kcp = ph == 0 ? kc : carve_variant(est, cols, ctx->num_sms);
+      carve_alloc(S, nr, rows, cols, target, P.mode == 0 ? 1 : 0, with_U, dump,
+                  carve_cluster(kcp, nr, cols, ctx->num_sms), gs, rea ? nfr.data() : nullptr, rea, kcp);
       hmark("group setup");
       const size_t fbytes = (size_t)curH * curW * C;
-      for (int r = r0; r < r1; ++r) {
-        CarveRun& R = S.runs[r - r0];
-        const int s0 = runs[r].first;
+      for (int k = 0; k < nr; ++k) {
+        CarveRun& R = S.runs[k];
+        ClipJob* J = rr[k].job;
+        const int s0 = J->runs[rr[k].r].first;
         // the first carved axis works on the original frames, whose energy codes carry the
         // Sobel gradient of every frame (so the carve's gradient plane needs no recompute);
         // reaverage carves every frame of the run, otherwise its first frame represents it
         for (int f = 0; f < R.nfr; ++f) {
           const uint16_t* fcodes =
-              (ph == 0 && P.mode != 0) ? codes.as<uint16_t>() + (size_t)(s0 + f) * h * w : nullptr;
-          kc6::launch_run_setup(cur + fbytes * (s0 + f - cur_t0), curH, curW, C, height ? 1 : 0, fcodes, R, gs, f);
+              (ph == 0 && P.mode != 0) ? J->codes.as<uint16_t>() + (size_t)(s0 + f) * h * w : nullptr;
+          kc6::launch_run_setup(src[k] + fbytes * f, curH, curW, C, height ? 1 : 0, fcodes, R, gs, f);
         }
         if (with_U)
-          launch_uniform(codes.as<uint16_t>(), h, w, s0, runs[r].second, 1, P.w_motion, P.w_grad, height ? 1 : 0,
-                         const_cast<double*>(R.U), gs, R.pitch);
+          launch_uniform(J->codes.as<uint16_t>(), h, w, s0, J->runs[rr[k].r].second, 1, P.w_motion, P.w_grad,
+                         height ? 1 : 0, const_cast<double*>(R.U), gs, R.pitch);
       }
-      mark("group " + std::to_string(groups.size() - 1) + " setup done", gs);
+      mark("group " + std::to_string(gi) + " setup done", gs);
       hmark("group carve_launch");
       carve_launch(ctx, S, pin_take(sizeof(CarveRun) * nr + 16), gs);
       hmark("group replay");
-      mark("group " + std::to_string(groups.size() - 1) + " carve done", gs);
+      mark("group " + std::to_string(gi) + " carve done", gs);
       const int nH = height ? th : curH, nW = height ? curW : tw;
       const bool last = ph + 1 == phases.size();
-      uint8_t* dst = out;
-      int dst_t0 = 0;
-      if (!last) {
-        dst = G.bufs.emplace_back((size_t)(tb - ta) * nH * nW * C, gs).as<uint8_t>();
-        dst_t0 = ta;
-      }
       const size_t obytes = (size_t)nH * nW * C;
-      for (int r = r0; r < r1; ++r) {
-        const CarveRun& R = S.runs[r - r0];
-        const int s0 = runs[r].first, n = runs[r].second;
-        launch_replay(cur + fbytes * (s0 - cur_t0), dst + obytes * (s0 - dst_t0), n, curH, curW, C, R.idx, R.pitch,
-                      target, height ? 1 : 0, gs);
-        if (last) ship(obytes * s0, obytes * n);
+      uint8_t* inter = nullptr;
+      if (!last) inter = G.bufs.emplace_back((size_t)covered * obytes, gs).as<uint8_t>();
+      size_t ioff = 0;
+      for (int k = 0; k < nr; ++k) {
+        const CarveRun& R = S.runs[k];
+        ClipJob* J = rr[k].job;
+        const int s0 = J->runs[rr[k].r].first, n = J->runs[rr[k].r].second;
+        uint8_t* dst = last ? J->out + obytes * s0 : inter + ioff;
+        launch_replay(src[k], dst, n, curH, curW, C, R.idx, R.pitch, target, height ? 1 : 0, gs);
+        if (last) ship(J, obytes * s0, obytes * n);
+        src[k] = dst;
+        ioff += obytes * n;
       }
-      mark("group " + std::to_string(groups.size() - 1) + " phase " + std::to_string(ph) + " runs " +
-               std::to_string(nr), gs);
-      cur = dst;
-      cur_t0 = dst_t0;
+      mark("group " + std::to_string(gi) + " phase " + std::to_string(ph) + " runs " + std::to_string(nr), gs);
       curH = nH;
       curW = nW;
     }
-    if (host_out) mark("d2h group " + std::to_string(groups.size() - 1), ctx->s_d2h);
+    if (host_out) mark("d2h group " + std::to_string(gi), ctx->s_d2h);
   };
-  if (buffered) {
+  // a single clip split across GPUs: runs go, as they close, to the least-loaded rank (every
+  // rank sees the same run list, so every rank computes the same assignment); a run's cost is
+  // dominated by its carve (about as long as replaying ~1000 frames), the length breaks ties
+  std::vector<double> load(shards, 0.0);
+  auto mine = [&](const std::pair<int, int>& run) {
+    if (shards <= 1) return true;
+    int best = 0;
+    for (int k = 1; k < shards; ++k)
+      if (load[k] < load[best]) best = k;
+    load[best] += 1000.0 + run.second;
+    return best == P.shard_rank;
+  };
+  if (scan_only) {
+    // nothing to carve
+  } else if (given) {
+    ClipJob& J = jobs[0];
+    for (int r = 0; r < P.n_runs_in; ++r) J.runs.push_back({P.runs_in[2 * r], P.runs_in[2 * r + 1]});
+    std::vector<RunRef> rr;
+    for (int r = 0; r < (int)J.runs.size(); ++r) rr.push_back({&J, r});
+    dispatch(rr, {J.ev_scan}, true);
+  } else if (buffered) {
     // host clips: every closed run goes out at once (the copies are the bottleneck); device
-    // clips: groups of >= 4 runs (fewer, larger carve sets)
-    int min_group = host_in ? 1 : 4;
+    // clips: groups of >= 4 runs (fewer, larger carve sets), >= 8 across a batch of clips
+    int min_group = host_in ? 1 : (njobs > 1 ? 8 : 4);
     if (const char* e = getenv("SCPL_GROUP_MIN")) min_group = std::max(1, atoi(e));
-    int done = 0;
     for (int c = 0; c < nchunk; ++c) {
-      hmark("wait chunk " + std::to_string(c));
-      SCPL_CUDA(cudaEventSynchronize(ev_chunk[c]));
-      const int n = scan.h_n[c];
-      for (int r = (int)runs.size(); r < n; ++r) runs.push_back({scan.h_runs[2 * r], scan.h_runs[2 * r + 1]});
-      if (shards > 1) {  // this rank's runs (round-robin by run index), each as it closes
-        for (int r = done; r < n; ++r)
-          if (r % shards == P.shard_rank) dispatch(r, r + 1, ev_chunk[c], host_in && c + 1 == nchunk);
-        done = n;
-      } else if (n - done >= min_group || (c + 1 == nchunk && n > done)) {
-        // (a device clip's scan ends long before its groups do: only a host clip's last group,
-        // closed after the copies, carves with the GPU to itself)
-        dispatch(done, n, ev_chunk[c], host_in && c + 1 == nchunk);
-        done = n;
+      const bool last_chunk = c + 1 == nchunk;
+      std::vector<RunRef> pending;
+      std::vector<cudaEvent_t> ready;
+      for (auto& J : jobs) {
+        hmark("wait chunk " + std::to_string(c));
+        SCPL_CUDA(cudaEventSynchronize(J.ev_chunk[c]));
+        const int n = J.scan.h_n[c];
+        for (int r = (int)J.runs.size(); r < n; ++r) J.runs.push_back({J.scan.h_runs[2 * r], J.scan.h_runs[2 * r + 1]});
       }
+      if (shards > 1) {  // this rank's runs, each as it closes
+        ClipJob& J = jobs[0];
+        for (int r = J.done; r < (int)J.runs.size(); ++r)
+          if (mine(J.runs[r])) dispatch({{&J, r}}, {J.ev_chunk[c]}, host_in && last_chunk);
+        J.done = (int)J.runs.size();
+        continue;
+      }
+      int npend = 0;
+      for (auto& J : jobs) npend += (int)J.runs.size() - J.done;
+      if (npend == 0 || (npend < min_group && !last_chunk)) continue;
+      for (auto& J : jobs) {
+        if ((int)J.runs.size() == J.done) continue;
+        for (int r = J.done; r < (int)J.runs.size(); ++r) pending.push_back({&J, r});
+        ready.push_back(J.ev_chunk[c]);
+        J.done = (int)J.runs.size();
+      }
+      // (a device clip's scan ends long before its groups do: only a host clip's last group,
+      // closed after the copies, carves with the GPU to itself)
+      dispatch(pending, ready, host_in && last_chunk);
     }
   } else {
-    for (int t = 0; t < T; ++t) runs.push_back({t, 1});
+    ClipJob& J = jobs[0];
+    std::vector<RunRef> rr;
+    for (auto& Jx : jobs)
+      for (int t = 0; t < T; ++t) Jx.runs.push_back({t, 1});
     // sharded: a contiguous block of frames per rank
-    dispatch((int)((long)T * P.shard_rank / shards), (int)((long)T * (P.shard_rank + 1) / shards), ev_scan, false);
+    std::vector<cudaEvent_t> ready;
+    for (auto& Jx : jobs) {
+      const int a = njobs == 1 ? (int)((long)T * P.shard_rank / shards) : 0;
+      const int b = njobs == 1 ? (int)((long)T * (P.shard_rank + 1) / shards) : T;
+      for (int t = a; t < b; ++t) rr.push_back({&Jx, t});
+      ready.push_back(Jx.ev_scan);
+    }
+    (void)J;
+    dispatch(rr, ready, false);
   }
-  SCPL_CUDA(cudaStreamWaitEvent(st, ev_scan, 0));
+  for (auto& J : jobs) SCPL_CUDA(cudaStreamWaitEvent(st, J.ev_scan, 0));
   for (Group& G : groups) {
     cudaEvent_t e = new_event(false);
     SCPL_CUDA(cudaEventRecord(e, G.st));
     SCPL_CUDA(cudaStreamWaitEvent(st, e, 0));
   }
-  if (host_out) {
+  if (host_out && !scan_only) {
     cudaEvent_t e = new_event(false);
     SCPL_CUDA(cudaEventRecord(e, ctx->s_d2h));
     SCPL_CUDA(cudaStreamWaitEvent(st, e, 0));
@@ -1044,48 +1218,82 @@ void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* fram
   hmark("synchronized");
 
   // 4. results
-  if (buffered) scan_finish(scan, nchunk, result);
-  result->n_runs = (int)runs.size();
-  if (result->run_start && result->run_len)
-    for (size_t r = 0; r < runs.size(); ++r) {
-      result->run_start[r] = runs[r].first;
-      result->run_len[r] = runs[r].second;
+  for (auto& J : jobs) {
+    if (buffered && !given) {
+      scan_finish(J.scan, nchunk, J.result);
+      if (scan_only)  // every run of the scan
+        for (int r = (int)J.runs.size(); r < J.scan.h_state->nruns; ++r)
+          J.runs.push_back({J.scan.h_runs[2 * r], J.scan.h_runs[2 * r + 1]});
     }
-  long dp = 0, pass_launches = 0;
-  long long pass_cyc = 0;
-  for (Group& G : groups)
+    J.result->n_runs = (int)J.runs.size();
+    if (J.result->run_start && J.result->run_len)
+      for (size_t r = 0; r < J.runs.size(); ++r) {
+        J.result->run_start[r] = J.runs[r].first;
+        J.result->run_len[r] = J.runs[r].second;
+      }
+  }
+  long pass_launches = 0;
+  long long pass_cyc = 0, best_cyc = 0, best[3] = {0, 0, 0};
+  int cluster = 0;
+  for (Group& G : groups) {
+    auto ax = G.axes.begin();
     for (CarveSet& S : G.sets) {
       carve_finish(S);
       long long slow = 0;
       int launches = 0;
-      for (auto& R : S.runs) {
-        dp += R.iters;
+      for (size_t k = 0; k < S.runs.size(); ++k) {
+        const CarveRun& R = S.runs[k];
+        ClipJob* J = G.runs[k].job;
+        J->dp += R.iters;
         slow = std::max(slow, R.cyc_dp + R.cyc_sel);
         launches = std::max(launches, R.iters);
+        if (J->result->seam_dump) dump_record(J->result, G.runs[k].r, *ax, R);
       }
       pass_cyc += slow;  // a launch lasts as long as its slowest cluster
       pass_launches += launches;
-      if (S.prof[0] + S.prof[1] > result->carve_cycles[0] + result->carve_cycles[1])
-        for (int k = 0; k < 3; ++k) result->carve_cycles[k] = S.prof[k];
-      result->carve_cluster = S.cl;
+      if (S.prof[0] + S.prof[1] > best_cyc) {
+        best_cyc = S.prof[0] + S.prof[1];
+        for (int k = 0; k < 3; ++k) best[k] = S.prof[k];
+      }
+      cluster = S.cl;
+      ++ax;
     }
-  result->dp_passes = dp;
-  result->carve_cycles[3] = pass_launches;
-  if (pass_launches > 0) result->phase_ms[3] = (float)((double)pass_cyc / pass_launches / std::max(ctx->clock_khz, 1));
+  }
+  float ms_end = 0.f;
   for (auto& m : marks) {
     float ms = 0.f;
     SCPL_CUDA(cudaEventElapsedTime(&ms, ev_start, m.second));
     fprintf(stderr, "timeline %8.3f ms  %s\n", ms, m.first.c_str());
   }
-  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[0], ev_start, ev_codes));
-  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[1], ev_codes, ev_scan));
-  SCPL_CUDA(cudaEventElapsedTime(&result->phase_ms[2], ev_scan, ev_end));
-  if (timeline) {
-    float ms = 0.f;
-    SCPL_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_end));
-    fprintf(stderr, "timeline %8.3f ms  end\n", ms);
+  SCPL_CUDA(cudaEventElapsedTime(&ms_end, ev_start, ev_end));
+  for (auto& J : jobs) {
+    scpl_video_result* res = J.result;
+    res->dp_passes = J.dp;
+    for (int k = 0; k < 3; ++k) res->carve_cycles[k] = best[k];
+    res->carve_cycles[3] = pass_launches;
+    res->carve_cluster = cluster;
+    if (pass_launches > 0)
+      res->phase_ms[3] = (float)((double)pass_cyc / pass_launches / std::max(ctx->clock_khz, 1));
+    SCPL_CUDA(cudaEventElapsedTime(&res->phase_ms[0], ev_start, J.ev_codes));
+    SCPL_CUDA(cudaEventElapsedTime(&res->phase_ms[1], J.ev_codes, J.ev_scan));
+    float scan_end_ms = 0.f;
+    SCPL_CUDA(cudaEventElapsedTime(&scan_end_ms, ev_start, J.ev_scan));
+    res->phase_ms[2] = ms_end - scan_end_ms;
   }
+  if (timeline) fprintf(stderr, "timeline %8.3f ms  end\n", ms_end);
   hmark("results");
+}
+
+void retarget_core(scpl_ctx* ctx, const uint8_t* frames_dev, const uint8_t* frames_host, int T, int h, int w,
+                   int channels, const scpl_video_params& P, uint8_t* out_dev, uint8_t* out_host,
+                   scpl_video_result* result, cudaStream_t st) {
+  std::vector<ClipJob> jobs(1);
+  jobs[0].frames_dev = frames_dev;
+  jobs[0].frames_host = frames_host;
+  jobs[0].out_dev = out_dev;
+  jobs[0].out_host = out_host;
+  jobs[0].result = result;
+  retarget_jobs(ctx, jobs, T, h, w, channels, P, st);
 }
 
 }  // namespace
@@ -1113,12 +1321,30 @@ int scpl_retarget_video(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int 
   });
 }
 
+int scpl_retarget_batch(scpl_ctx* ctx, int nclips, const uint8_t* const* clips, int T, int h, int w, int channels,
+                        const scpl_video_params* params, uint8_t* const* outs, scpl_video_result* results,
+                        int host_buffers, void* stream) {
+  return guarded(ctx, [&] {
+    SCPL_ARG(params != nullptr && results != nullptr && clips != nullptr && outs != nullptr,
+             "params/results/clips/outs is NULL");
+    SCPL_ARG(nclips >= 1, "nclips must be >= 1");
+    std::vector<ClipJob> jobs(nclips);
+    for (int i = 0; i < nclips; ++i) {
+      SCPL_ARG(clips[i] != nullptr && (outs[i] != nullptr || params->scan_only), "clip or output is NULL");
+      (host_buffers ? jobs[i].frames_host : jobs[i].frames_dev) = clips[i];
+      (host_buffers ? jobs[i].out_host : jobs[i].out_dev) = outs[i];
+      jobs[i].result = &results[i];
+    }
+    retarget_jobs(ctx, jobs, T, h, w, channels, *params, (cudaStream_t)stream);
+  });
+}
+
 int scpl_retarget_video_host(scpl_ctx* ctx, const uint8_t* frames, int T, int h, int w, int channels,
                              const scpl_video_params* params, uint8_t* out, scpl_video_result* result,
                              void* stream) {
   return guarded(ctx, [&] {
     SCPL_ARG(params != nullptr && result != nullptr, "params/result is NULL");
-    SCPL_ARG(frames != nullptr && out != nullptr, "frames/out is NULL");
+    SCPL_ARG(frames != nullptr && (out != nullptr || params->scan_only), "frames/out is NULL");
     retarget_core(ctx, nullptr, frames, T, h, w, channels, *params, nullptr, out, result, (cudaStream_t)stream);
   });
 }
@@ -1155,6 +1381,7 @@ int scpl_remove_columns(scpl_ctx* ctx, const uint8_t* in, int h, int w, int chan
                         uint8_t* out, int* rowcount, void* stream) {
   return guarded(ctx, [&] {
     SCPL_ARG(b >= 0 && b <= w, "batch larger than the frame");
+    SCPL_ARG(channels >= 1, "bytes per pixel must be >= 1");
     launch_remove_cols(in, h, w, channels, (const long*)offsets, b, out, rowcount, (cudaStream_t)stream);
   });
 }

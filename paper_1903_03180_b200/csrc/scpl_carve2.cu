@@ -1143,6 +1143,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
     }
     __syncthreads();
     SEL_PROF(0);
+    if (rank == 0 && R.labs != nullptr)  // seam dump: this pass's labels (label_parents)
+      for (int j = tid; j < w; j += blockDim.x) R.labs[(long)iters * R.width0 + j] = (int16_t)S.lab[j];
     int b;
     if (R.kmax == 1) {  // raw mode: min_seam, leftmost global minimum (seams.py:84-89)
       for (int j = tid; j < w; j += blockDim.x)

@@ -95,6 +95,7 @@ struct alignas(64) CarveRun {
   int* sizes;           // optional per-batch sizes (capacity width0)
   int16_t* cols;        // optional per-seam last-row column (capacity width0)
   double* costs;        // optional per-seam cost
+  int16_t* labs;        // optional (seam dump): parent labels of every pass, passes x width0
   // state (read at every kernel entry, advanced by the pass kernel)
   int width;            // current width
   int iters;            // DP passes done

@@ -24,11 +24,22 @@ def _channels(arr: np.ndarray) -> int:
     raise ValueError(f"unsupported channel count: expected 1 or 3, got shape {arr.shape}")
 
 
+def as_u8(arr: np.ndarray) -> np.ndarray:
+    """Pixels as uint8: integer arrays with values in 0..255 convert exactly (the reference
+    computes on the values, energy.py:34-35); anything else is rejected, never wrapped."""
+    arr = np.asarray(arr)
+    if arr.dtype == np.uint8:
+        return arr
+    if arr.dtype.kind in "iub" and (arr.size == 0 or (int(arr.min()) >= 0 and int(arr.max()) <= 255)):
+        return arr.astype(np.uint8)
+    raise ValueError(f"expected uint8 pixels (or integers in 0..255), got {arr.dtype}")
+
+
 def _luma_dev(arr: np.ndarray):
     """(h, w) uint8 luma on the device (energy.py:23-37)."""
     torch = _lib.torch_cuda()
     c = _channels(arr)
-    src = _lib.to_device(np.ascontiguousarray(arr, dtype=np.uint8))
+    src = _lib.to_device(np.ascontiguousarray(as_u8(arr)))
     h, w = arr.shape[:2]
     out = torch.empty((h, w), dtype=torch.uint8, device=src.device)
     _lib.check(_lib.load().scpl_to_luma(_lib.ctx(), src.data_ptr(), h * w, c, out.data_ptr(), _lib.stream()))
@@ -56,7 +67,7 @@ def gradient_energy(luma: np.ndarray) -> np.ndarray:
     if h < 3 or w < 3:
         raise ValueError(f"frame too small for 3x3 Sobel: {w}x{h}, need at least 3x3")
     torch = _lib.torch_cuda()
-    src = _lib.to_device(np.ascontiguousarray(img, dtype=np.uint8))
+    src = _lib.to_device(np.ascontiguousarray(as_u8(img)))
     out = torch.empty((h, w), dtype=torch.float64, device=src.device)
     _lib.check(_lib.load().scpl_gradient_energy(_lib.ctx(), src.data_ptr(), h, w, out.data_ptr(), _lib.stream()))
     return _lib.to_host(out)
@@ -70,7 +81,7 @@ def motion_energy(curr: np.ndarray, prev: np.ndarray | None, w_motion: float = D
     torch = _lib.torch_cuda()
     c_arr = np.asarray(curr)
     lc = _luma_dev(c_arr) if c_arr.ndim == 3 and c_arr.shape[2] == 3 else _lib.to_device(
-        np.ascontiguousarray(to_luma(c_arr), dtype=np.uint8))
+        np.ascontiguousarray(as_u8(to_luma(c_arr))))
     h, w = lc.shape
     if h < 3 or w < 3:
         raise ValueError(f"frame too small for 3x3 Sobel: {w}x{h}, need at least 3x3")
@@ -78,7 +89,7 @@ def motion_energy(curr: np.ndarray, prev: np.ndarray | None, w_motion: float = D
     if prev is not None:
         p_arr = np.asarray(prev)
         lp = _luma_dev(p_arr) if p_arr.ndim == 3 and p_arr.shape[2] == 3 else _lib.to_device(
-            np.ascontiguousarray(to_luma(p_arr), dtype=np.uint8))
+            np.ascontiguousarray(as_u8(to_luma(p_arr))))
         if tuple(lp.shape) != (h, w):
             raise ValueError(f"dimension mismatch: current frame {(h, w)}, previous {tuple(lp.shape)}")
     codes = torch.empty((h, w), dtype=torch.int16, device=lc.device)

@@ -1,21 +1,55 @@
-"""One clip across several GPUs ("one serial scan + independent runs").
+"""One clip across several GPUs ("one serial scan + independent runs"), and a
+batch of clips across GPUs (BASELINE config C4).
 
 The buffer scan (buffering.py:93-127) is serial over the clip, but once it has placed the runs
-they are independent (pipeline.py:246-277 carves each from its own frames).  Every rank holds
-the clip, computes the energy codes and the whole scan -- cheap next to the carves, and no
-rank waits on another -- then carves and replays only its own runs: run r belongs to rank
-r % world (scpl / raw modes, where every frame is a run: a contiguous block of frames per
-rank).  The output frames are then exchanged with one broadcast per run from its owner (NCCL
-over NVLink, or gloo on CPU), so every rank ends with the whole retargeted clip.  There is no
-collective on the compute path.
+they are independent (pipeline.py:246-277 carves each from its own frames).  Two ways to split:
+
+* every rank holds the clip, computes the energy codes and the whole scan (cheap next to the
+  carves, and no rank waits on another) and carves the runs the online assignment gives it as
+  they close (libscpl shard_rank / shard_count: each run goes to the least-loaded rank so far;
+  every rank sees the same runs in the same order, so every rank computes the same owners);
+* scan_once: rank 0 runs the scan alone, the run list goes to every rank through the host
+  (a broadcast of a few integers), and the runs are dealt longest-processing-time first; each
+  rank then carves exactly its runs (libscpl runs_in).
+
+In scpl / raw modes every frame is a run: a contiguous block of frames per rank.  A run's cost
+is dominated by its carve (one representative frame, ~40 DP passes: about as long as replaying
+~1000 frames), so the cost model is 1000 + run length.  Outputs are gathered either with one
+broadcast per run from its owner (CUDA outputs: NCCL over NVLink, or gloo on CPU) or on the
+host: every rank's host-buffer call writes its runs' frames into one shared host buffer (no
+collective at all).  There is no collective on the compute path.
 """
 
 from __future__ import annotations
 
+RUN_COST0 = 1000.0  # a run's carve, in frames of replay
 
-def run_owner(r: int, world: int) -> int:
-    """Rank that carves buffered run r (libscpl: r % shard_count == shard_rank)."""
-    return r % world
+
+def _cost(run) -> float:
+    return RUN_COST0 + run[1]
+
+
+def run_owners(runs, world: int) -> list[int]:
+    """Owner of each buffered run under libscpl's shard mode: runs in scan order, each to the
+    least-loaded rank so far (lowest rank on ties) -- scpl_api.cu `mine`."""
+    load = [0.0] * world
+    owners = []
+    for run in runs:
+        best = min(range(world), key=lambda k: (load[k], k))
+        load[best] += _cost(run)
+        owners.append(best)
+    return owners
+
+
+def lpt_owners(runs, world: int) -> list[int]:
+    """Longest-processing-time-first assignment of the runs (scan_once mode)."""
+    load = [0.0] * world
+    owners = [0] * len(runs)
+    for i in sorted(range(len(runs)), key=lambda i: (-_cost(runs[i]), i)):
+        best = min(range(world), key=lambda k: (load[k], k))
+        load[best] += _cost(runs[i])
+        owners[i] = best
+    return owners
 
 
 def frame_block(rank: int, world: int, T: int) -> tuple[int, int]:
@@ -23,37 +57,64 @@ def frame_block(rank: int, world: int, T: int) -> tuple[int, int]:
     return T * rank // world, T * (rank + 1) // world
 
 
-def owned_spans(runs, rank: int, world: int, mode: str, T: int):
-    """(start, length) frame spans this rank produces."""
+def owned_spans(runs, rank: int, world: int, mode: str, T: int, owners=None):
+    """(start, length) frame spans this rank produces (owners: a run -> rank list, default the
+    online assignment)."""
     if mode == "buffered":
-        return [tuple(r) for i, r in enumerate(runs) if run_owner(i, world) == rank]
+        owners = run_owners(runs, world) if owners is None else owners
+        return [tuple(r) for r, o in zip(runs, owners) if o == rank]
     a, b = frame_block(rank, world, T)
     return [(a, b - a)] if b > a else []
 
 
-def gather_runs(out, runs, world: int, mode: str, group=None):
+def gather_runs(out, runs, world: int, mode: str, group=None, owners=None):
     """Make `out` (T, ...) complete on every rank: each span is broadcast by its owner."""
     import torch.distributed as dist
     T = out.shape[0]
     for rank in range(world):
-        for s, n in owned_spans(runs, rank, world, mode, T):
+        for s, n in owned_spans(runs, rank, world, mode, T, owners):
             dist.broadcast(out[s:s + n], src=rank, group=group)
     return out
 
 
-def retarget_clip_sharded(clip, config, group=None, out=None):
+def broadcast_runs(runs, group=None, src: int = 0):
+    """The scan's run list from `src` to every rank (host objects, a few integers)."""
+    import torch.distributed as dist
+    box = [list(map(tuple, runs)) if runs is not None else None]
+    dist.broadcast_object_list(box, src=src, group=group)
+    return [tuple(r) for r in box[0]]
+
+
+def retarget_clip_sharded(clip, config, group=None, out=None, scan_once=False, gather=True):
     """retarget_video_tensor of one CUDA clip split across the ranks of `group`: returns the
-    whole output on every rank and RunMetrics with dp_passes summed over the ranks."""
+    output (whole on every rank when gather, else this rank's runs only) and RunMetrics with
+    dp_passes summed over the ranks."""
     import torch
     import torch.distributed as dist
 
-    from .pipeline import retarget_video_tensor
+    from .pipeline import retarget_video_tensor, scan_runs
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    res, m = retarget_video_tensor(clip, config, out=out, shard=(rank, world))
+    owners = None
+    if scan_once and config.mode == "buffered":
+        runs = scan_runs(clip, config) if rank == 0 else None
+        runs = broadcast_runs(runs, group) if world > 1 else runs
+        owners = lpt_owners(runs, world)
+        mine = [r for r, o in zip(runs, owners) if o == rank]
+        res, m = retarget_video_tensor(clip, config, out=out, runs=mine)
+        m.runs = runs
+    else:
+        res, m = retarget_video_tensor(clip, config, out=out, shard=(rank, world))
     if world > 1:
-        gather_runs(res, m.runs, world, config.mode, group)
+        if gather:
+            gather_runs(res, m.runs, world, config.mode, group, owners)
         dp = torch.tensor([m.dp_passes], dtype=torch.int64, device=res.device)
         dist.all_reduce(dp, group=group)
         m.dp_passes = int(dp.item())
     return res, m
+
+
+def shard_clips(n_clips: int, rank: int, world: int) -> list[int]:
+    """Clips of a batch a rank retargets (BASELINE C4: 64 clips, 64/G per GPU): a contiguous
+    block, sizes differing by at most one."""
+    return list(range(n_clips * rank // world, n_clips * (rank + 1) // world))

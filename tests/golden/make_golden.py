@@ -9,8 +9,9 @@ reference's to_luma over all 2^24 RGB triples). `Cn` runs
 vidcarve.retarget_video on the seeded synthetic clip of that BASELINE config
 (paper_1903_03180_b200.synth) and records run boundaries, dp_passes, every
 batch (size, last-row columns, costs, offsets hash) and every output frame's
-SHA-256. Recording wraps two reference functions at runtime
-(pipeline.batch_carve, pipeline._process_run); the reference source is not
+SHA-256, plus the SHA-256 of every pass's parent labels (int64). Recording
+wraps three reference functions at runtime (pipeline.batch_carve,
+pipeline._process_run, batching.label_parents); the reference source is not
 modified. /root/reference does not exist on the GPU box: only the JSON
 outputs travel.
 """
@@ -147,12 +148,23 @@ def small():
 def config(name: str, frames: int | None, clip: int, reaverage: bool = False):
     from paper_1903_03180_b200.synth import config_clip
     arr, tw, th = config_clip(name, frames=frames, clip=clip)
-    runs, batches = [], []
-    orig_carve, orig_process = vp.batch_carve, vp._process_run
+    import vidcarve.batching as vb_mod
+    runs, batches, labels = [], [], []
+    orig_carve, orig_process, orig_labels = vp.batch_carve, vp._process_run, vb_mod.label_parents
+
+    def rec_labels(tables):  # batch_carve's per-pass parent labels (batching.py:148)
+        lab = orig_labels(tables)
+        labels.append(sha(np.asarray(lab, dtype=np.int64)))
+        return lab
 
     def rec_carve(*a, **k):
+        del labels[:]
         carved, bs = orig_carve(*a, **k)
-        batches[-1].append([batch_record(b) for b in bs])
+        assert len(labels) == len(bs)
+        recs = [batch_record(b) for b in bs]
+        for r, lab in zip(recs, labels):
+            r["labels_sha"] = lab
+        batches[-1].append(recs)
         return carved, bs
 
     def rec_process(run, *a, **k):
@@ -160,14 +172,14 @@ def config(name: str, frames: int | None, clip: int, reaverage: bool = False):
         batches.append([])
         return orig_process(run, *a, **k)
 
-    vp.batch_carve, vp._process_run = rec_carve, rec_process
+    vp.batch_carve, vp._process_run, vb_mod.label_parents = rec_carve, rec_process, rec_labels
     try:
         t0 = time.time()
         out, m = vp.retarget_video(list(arr), vp.RetargetConfig(target_width=tw, target_height=th, mode="buffered",
                                                                 reaverage_energy=reaverage))
         wall = time.time() - t0
     finally:
-        vp.batch_carve, vp._process_run = orig_carve, orig_process
+        vp.batch_carve, vp._process_run, vb_mod.label_parents = orig_carve, orig_process, orig_labels
     starts = np.concatenate([[0], np.cumsum(runs)[:-1]]).tolist()
     rec = {
         "config": name, "clip": clip, "frames": int(arr.shape[0]), "shape": list(arr.shape[1:]),

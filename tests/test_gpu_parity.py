@@ -442,3 +442,18 @@ def test_sharded_clip_matches_reference(P, world):
         assert dp == g["dp_passes"]
         bad = [t for t in range(merged.shape[0]) if sha(merged[t]) != g["frames_sha"][t]]
         assert not bad, f"{name}: {len(bad)} frames differ"
+        # scan once, runs dealt longest-processing-time first, each rank carves exactly its runs
+        runs = P.scan_runs(dev, cfg)
+        owners = sharding.lpt_owners(runs, world)
+        merged[:] = 0
+        dp = 0
+        for rank in range(world):
+            mine = [r for r, o in zip(runs, owners) if o == rank]
+            out, m = P.retarget_video_tensor(dev, cfg, runs=mine)
+            dp += m.dp_passes
+            host = out.cpu().numpy()
+            for s, n in mine:
+                merged[s:s + n] = host[s:s + n]
+        assert dp == g["dp_passes"]
+        bad = [t for t in range(merged.shape[0]) if sha(merged[t]) != g["frames_sha"][t]]
+        assert not bad, f"{name} (scan once): {len(bad)} frames differ"

@@ -22,10 +22,13 @@ def small():
         return json.load(f)
 
 
-def _batch_rec(b):
-    return {"b": len(b), "cols": [int(c) for c in b.cols], "costs": [fhex(c) for c in b.costs],
-            "offsets_sha": sha(b.offsets.astype(np.int32)) if len(b) else sha(np.zeros((0, 0), np.int32)),
-            "source_width": b.source_width}
+def _batch_rec(b, labels=False):
+    r = {"b": len(b), "cols": [int(c) for c in b.cols], "costs": [fhex(c) for c in b.costs],
+         "offsets_sha": sha(b.offsets.astype(np.int32)) if len(b) else sha(np.zeros((0, 0), np.int32)),
+         "source_width": b.source_width}
+    if labels:
+        r["labels_sha"] = sha(np.asarray(b.labels, dtype=np.int64))
+    return r
 
 
 def test_luma_table_pinned():
@@ -127,5 +130,5 @@ def test_pipeline_C1_golden():
     res = O.retarget_video(list(clip), target_width=tw, target_height=th, keep_batches=True)
     assert [list(r) for r in res.runs] == g["runs"]
     assert res.dp_passes == g["dp_passes"]
-    assert [[[_batch_rec(b) for b in ph] for ph in rb] for rb in res.batches] == g["batches"]
+    assert [[[_batch_rec(b, labels=True) for b in ph] for ph in rb] for rb in res.batches] == g["batches"]
     assert [sha(f) for f in res.frames] == g["frames_sha"]
