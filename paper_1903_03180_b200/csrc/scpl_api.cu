@@ -475,7 +475,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   const bool graph = S.cols > S.target && !host_loops();
   S.ctx = ctx;
   S.loop_key = {nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
-                (int)S.reaverage + 2 * graph + 4 * S.kc};
+                (int)S.reaverage + 2 * graph + 4 * S.kc + 64 * (int)S.has_uniform};
   auto it = ctx->loop_pool.find(S.loop_key);
   if (it != ctx->loop_pool.end()) {
     S.loop = it->second;
@@ -498,9 +498,9 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   if (S.cols > S.target && host_loops()) {  // bursts of 8 iterations, host checks the widths
     int done_iters = 0;
     while (true) {
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < 8; ++k)  // (a uniform map's first pass is an fp64 one)
         SCPL_CARVE_FN(S.kc, launch_carve_iteration)(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, st, S.max_fr,
-                                                    S.reaverage);
+                                                    S.reaverage, done_iters + k == 0 && S.has_uniform);
       done_iters += 8;
       kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns, st);
       SCPL_CUDA(cudaStreamSynchronize(st));
@@ -511,7 +511,8 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   } else if (graph) {
     if (!S.loop.ex)
       S.loop.ex = SCPL_CARVE_FN(S.kc, build_carve_loop)(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl,
-                                                        S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage);
+                                                        S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage,
+                                                        S.has_uniform);
     SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
   kc6::launch_carve_index(runs_d, nruns, S.rows, st);
@@ -1025,8 +1026,10 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   // 3. carve + replay, one run group at a time as runs close
   const long total_frames = (long)T * njobs;
   int next_stream = 0;
-  auto dispatch = [&](std::vector<RunRef> rr, const std::vector<cudaEvent_t>& ready, bool final_group) {
+  auto dispatch = [&](std::vector<RunRef> rr, std::vector<cudaEvent_t> ready, bool final_group) {
     if (rr.empty()) return;
+    std::sort(ready.begin(), ready.end());
+    ready.erase(std::unique(ready.begin(), ready.end()), ready.end());
     Group& G = groups.emplace_back();
     G.runs = rr;
     const int gi = (int)groups.size() - 1;
@@ -1154,6 +1157,10 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
     // clips: groups of >= 4 runs (fewer, larger carve sets), >= 8 across a batch of clips
     int min_group = host_in ? 1 : (njobs > 1 ? 8 : 4);
     if (const char* e = getenv("SCPL_GROUP_MIN")) min_group = std::max(1, atoi(e));
+    // a batch's closed runs go out in groups of at most max_group (each group's carve loop is
+    // one serial chain of pass / row kernels: more groups, more chains in flight)
+    int max_group = njobs > 1 ? 8 : 1 << 30;
+    if (const char* e = getenv("SCPL_GROUP_MAX")) max_group = std::max(1, atoi(e));
     for (int c = 0; c < nchunk; ++c) {
       const bool last_chunk = c + 1 == nchunk;
       std::vector<RunRef> pending;
@@ -1176,13 +1183,22 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       if (npend == 0 || (npend < min_group && !last_chunk)) continue;
       for (auto& J : jobs) {
         if ((int)J.runs.size() == J.done) continue;
-        for (int r = J.done; r < (int)J.runs.size(); ++r) pending.push_back({&J, r});
-        ready.push_back(J.ev_chunk[c]);
+        for (int r = J.done; r < (int)J.runs.size(); ++r) {
+          pending.push_back({&J, r});
+          ready.push_back(J.ev_chunk[c]);
+          if ((int)pending.size() == max_group) {
+            dispatch(pending, ready, false);
+            pending.clear();
+            ready.clear();
+          }
+        }
         J.done = (int)J.runs.size();
       }
       // (a device clip's scan ends long before its groups do: only a host clip's last group,
       // closed after the copies, carves with the GPU to itself)
-      dispatch(pending, ready, host_in && last_chunk);
+      std::sort(ready.begin(), ready.end());
+      ready.erase(std::unique(ready.begin(), ready.end()), ready.end());
+      dispatch(pending, ready, host_in && last_chunk && njobs == 1);
     }
   } else {
     ClipJob& J = jobs[0];

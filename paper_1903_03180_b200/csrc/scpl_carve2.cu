@@ -1,4 +1,4 @@
-// K4-K7 (v2): the whole SCPL carve loop of a run in ONE persistent cluster kernel.
+// K4-K7: the SCPL carve loop of a run -- one cluster kernel per DP pass plus row kernels.
 //
 // Replaces batch_carve (batching.py:118-153) with everything it calls: cumulative_energy
 // (seams.py:39-65), label_parents (batching.py:39-46), select_batch (:49-73),
@@ -6,29 +6,29 @@
 // default_energy (:110-115).
 //
 // One thread-block cluster of CL CTAs (CL SMs) carves one run; runs are independent, so a
-// launch holds every run of a clip (grid = runs x CL).  Per DP pass:
+// launch holds every run of a carve group (grid = runs x CL).  Per pass (carve_pass_kernel):
 //
-//  1. DP, column-split.  Each warp owns 96 columns and computes a 128-column window
-//     (owned +-16) for 16 rows without any barrier: neighbours come from register shuffles,
-//     the window's valid region shrinks by one column per row, and after 16 rows exactly
-//     the owned columns remain valid ("trapezoid" tiling).  Every 16 rows (one path-word
-//     block) warps publish their owned cumulative energies to shared memory -- and the 16
-//     columns next to a CTA edge into the neighbour CTA through DSMEM -- then one cluster
-//     barrier.  The reference's argmin-first tie-break (seams.py:62) is strict '<' in the
-//     order -1, 0, +1.  Back pointers never leave registers: each column carries a 32-bit
-//     path word (2 bits per row) that is reset at every block start; at a block's last row
-//     the owned words and their landing deltas go to global memory.
-//     First pass of a buffered run: float64 on the uniform map (IEEE adds, no FMA);
-//     later passes: int32 on gradient energy (integer-valued, so bit-identical).
-//  2. Select (every CTA redundantly, no broadcast needed): labels by chaining the landing
+//  1. DP, column-split.  Each DP warp owns kOwn columns (128 / 64 / 32 for the kc6 / kc4 / kc3
+//     builds) and computes a window 64 columns wider for 32 rows without any barrier:
+//     neighbours come from register shuffles, the window's valid region shrinks by one column
+//     per row, and after 32 rows exactly the owned columns remain valid ("trapezoid" tiling).
+//     Every 32 rows warps publish their owned cumulative energies to shared memory -- and the
+//     32 columns next to a CTA edge into the neighbour CTA with st.async on its mbarrier.  The
+//     reference's argmin-first tie-break (seams.py:62) is strict '<' in the order -1, 0, +1.
+//     First pass of a buffered run: float64 on the uniform map (IEEE adds, no FMA), carrying
+//     path words; later passes: packed int keys on gradient energy (integer-valued, so
+//     bit-identical) with per-column choice words.  Block-end words and landing deltas go to
+//     global memory through helper warps.
+//  2. Select + trace (select_trace, every CTA redundantly): labels by chaining the landing
 //     deltas bottom-up (table staged in shared memory), per-parent leftmost minimum via
-//     shared-memory atomics (labels are monotone, so parents are segments), k-truncation
-//     by (cost, col), then each CTA decodes its share of (seam, block) path words into the
+//     shared-memory atomics (labels are monotone, so parents are segments), k-truncation by
+//     (cost, col), then each CTA decodes its share of (seam, block) pairs into the
 //     removed-column log.
-//  3. Compact, row-split: luma, gradient and the original-column index map drop the
-//     batch's columns in place (warp per row, 32-column chunks left to right).
-//  4. Gradient, row-split and incremental: a pixel's Sobel value changes only if a removed
-//     pixel of rows i-1..i+1 lay within one column of it; only those are recomputed.
+// Between passes (row kernels, whole GPU):
+//  3. Compact (carve_compact_kernel): luma and gradient drop the batch's columns in place.
+//  4. Gradient (carve_dirty_kernel), incremental: a pixel's Sobel value changes only if a
+//     removed pixel of rows i-1..i+1 lay within one column of it; only those are recomputed.
+// The original-column index map is rebuilt once per run at the end (carve_index_kernel).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -750,15 +750,43 @@ __device__ int block_excl_scan(int v, int* ws, int& total) {
 }
 
 // ------------------------------------------------------------------ the persistent kernel
+// Select-phase shared memory (after the DP; it reuses the DP's space).  Costs are doubles on
+// the fp64 pass and ints on the int passes (integer-valued ce, seams.py:39-65); per-parent
+// minima are atomicMin on the cost's bit pattern (costs >= 0 order as unsigned).  Column
+// indices (labels, candidates, selected seams) fit int16 (widths <= 4096).
+template <bool F64>
 struct SelSmem {
-  double* lce;
-  unsigned long long* segmin;
-  int* lab;
+  using Cost = std::conditional_t<F64, double, int>;
+  using Bits = std::conditional_t<F64, unsigned long long, unsigned int>;
+  Cost* lce;
+  Bits* segmin;
   int* segarg;
-  int* cand;
-  int* sel;
-  int8_t* dtab;    // staged delta table [nblk][pitch] (or nullptr: chain in global)
+  int16_t* lab;
+  int16_t* cand;
+  int16_t* sel;
+  int8_t* dtab;  // staged delta table [nblk][pitch] (or nullptr: chain in global)
+  static __host__ __device__ constexpr size_t bytes_per_col() { return 2 * sizeof(Cost) + 4 + 3 * 2; }
+  __device__ void carve(uint8_t* base, int pitch, bool stage) {
+    uint8_t* p = base;
+    lce = reinterpret_cast<Cost*>(p);
+    p += sizeof(Cost) * (size_t)pitch;
+    segmin = reinterpret_cast<Bits*>(p);
+    p += sizeof(Bits) * (size_t)pitch;
+    segarg = reinterpret_cast<int*>(p);
+    p += 4 * (size_t)pitch;
+    lab = reinterpret_cast<int16_t*>(p);
+    p += 2 * (size_t)pitch;
+    cand = reinterpret_cast<int16_t*>(p);
+    p += 2 * (size_t)pitch;
+    sel = reinterpret_cast<int16_t*>(p);
+    p += 2 * (size_t)pitch;
+    dtab = stage ? reinterpret_cast<int8_t*>(base + ((p - base + 15) & ~(size_t)15)) : nullptr;
+  }
 };
+template <bool F64>
+__host__ __device__ constexpr size_t sel_bytes(int pitch) {
+  return SelSmem<F64>::bytes_per_col() * (size_t)pitch + 16;
+}
 
 // warp-inclusive scan of v over lanes
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -774,8 +802,6 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 // Alive-column bitmask of one row (nw32 words, <= 32*kMaxAliveWordsPerLane): the lanes hold
 // words m = lane + 32u; wv/pre (per-warp smem) receive the words and exclusive popcounts.
 constexpr int kMaxAliveWordsPerLane = 4;  // widths up to 4096
-constexpr int kListCap = 192;             // per-warp staged removal-list entries per row
-constexpr int kWarpScratch = 1024 + 4096;  // wv + pre + (shift table | three staged row lists)
 __device__ __forceinline__ void alive_row_prefix(const uint32_t* row, int nw32, uint32_t* wv, int* pre) {
   const int lane = threadIdx.x & 31;
   int running = 0;
@@ -812,7 +838,6 @@ __device__ __forceinline__ int alive_select(const uint32_t* wv, const int* pre, 
 // half: a_t <= 4q + 3), prefix-sums it, and writes each output word as one funnel shift of
 // two source words -- or byte by byte when its shift changes inside the word.
 constexpr int kRowWarps = 8;
-constexpr int kMaxRowWords = 1024;  // widths up to 4096
 
 // The compaction CTA is small (kCompWarps warps, shared memory sized by the pitch) so that it
 // fits next to a resident pass CTA: the row kernels of one group then run on SMs that other
@@ -990,9 +1015,195 @@ __device__ __forceinline__ void dirty_row(const CarveRun& R, const uint8_t* lum,
                R.rem + (long)ib * R.rem_cap + off, b, wn, rows < 3 || wn < 3, stage);
 }
 
+// Select + trace of one pass (every CTA of the cluster redundantly; no broadcast needed):
+// labels (batching.py:39-46) by chaining the landing deltas, per-parent leftmost minimum
+// (:59-64), k-truncation by (cost, col) (:66-68), then the removed-column log (seams.py:68-81).
+// Returns the batch size.
+template <bool F64>
+__device__ int select_trace(const CarveRun& R, uint8_t* smem, int* ws, uint64_t* dbar, int w, int iters, int removed,
+                            uint32_t rank, int CL, int nblk) {
+  using Sel = SelSmem<F64>;
+  using Cost = typename Sel::Cost;
+  using Bits = typename Sel::Bits;
+  const int tid = threadIdx.x;
+  const int rows = R.rows, pitch = R.pitch;
+  const bool stage_dtab = R.stage_dtab != 0;
+  Sel S;
+  S.carve(smem, pitch, stage_dtab);
+  const int8_t* dsrc = R.delta;
+  if (stage_dtab && tid == 0) {
+    // one bulk copy of the whole landing-delta table; the DP's generic-proxy stores (every
+    // CTA, published by the cluster barrier) are ordered before the async-proxy read
+    fence_proxy_async_global();
+    mbar_arrive_tx(dbar, (uint32_t)((size_t)nblk * pitch));
+    bulk_g2s(S.dtab, R.delta, (uint32_t)((size_t)nblk * pitch), dbar);
+  }
+  for (int j = tid; j < w; j += blockDim.x) {
+    S.lce[j] = (Cost)R.lastce[j];
+    S.segmin[j] = ~(Bits)0;
+    S.segarg[j] = INT_MAX;
+  }
+  if (stage_dtab) {
+    mbar_wait(dbar, 0);
+    dsrc = S.dtab;
+  }
+  __syncthreads();
+  [[maybe_unused]] long long ts = DP_CLOCK();
+  // labels (batching.py:39-46): chain the block landing deltas, 8 columns per thread in flight
+  // (shared-memory table: 32-bit shared addresses, no generic-address resolution per step)
+  for (int jb = tid; jb < w; jb += 8 * blockDim.x) {
+    int c[8];
+    bool ok[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      c[u] = jb + u * (int)blockDim.x;
+      ok[u] = c[u] < w;
+      if (!ok[u]) c[u] = 0;
+    }
+    if (stage_dtab) {
+      uint32_t row = smem_u32(S.dtab) + (uint32_t)(nblk - 1) * (uint32_t)pitch;
+      for (int bl = nblk - 1; bl >= 0; --bl, row -= (uint32_t)pitch) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] += lds_s8(row + (uint32_t)c[u]);
+      }
+    } else {
+      for (int bl = nblk - 1; bl >= 0; --bl) {
+        const int8_t* drow = dsrc + (size_t)bl * pitch;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] += drow[c[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (ok[u]) S.lab[jb + u * blockDim.x] = (int16_t)c[u];
+  }
+  __syncthreads();
+  SEL_PROF(0);
+  if (rank == 0 && R.labs != nullptr)  // seam dump: this pass's labels (label_parents)
+    for (int j = tid; j < w; j += blockDim.x) R.labs[(long)iters * R.width0 + j] = S.lab[j];
+  auto bits = [](Cost v) -> Bits {
+    if constexpr (F64)
+      return (Bits)__double_as_longlong(v);
+    else
+      return (Bits)v;
+  };
+  int b;
+  if (R.kmax == 1) {  // raw mode: min_seam, leftmost global minimum (seams.py:84-89)
+    for (int j = tid; j < w; j += blockDim.x) atomicMin(&S.segmin[0], bits(S.lce[j]));
+    __syncthreads();
+    for (int j = tid; j < w; j += blockDim.x)
+      if (bits(S.lce[j]) == S.segmin[0]) atomicMin(&S.segarg[0], j);
+    __syncthreads();
+    if (tid == 0) S.sel[0] = (int16_t)S.segarg[0];
+    b = 1;
+  } else {
+    // per parent the leftmost strict minimum (batching.py:59-64); costs >= 0 order as unsigned
+    for (int j = tid; j < w; j += blockDim.x) atomicMin(&S.segmin[S.lab[j]], bits(S.lce[j]));
+    __syncthreads();
+    for (int j = tid; j < w; j += blockDim.x)
+      if (bits(S.lce[j]) == S.segmin[S.lab[j]]) atomicMin(&S.segarg[S.lab[j]], j);
+    __syncthreads();
+    SEL_PROF(1);
+    const int perq0 = (w + blockDim.x - 1) / blockDim.x;
+    int cnt = 0;
+    for (int u = 0; u < perq0; ++u) {
+      int l = tid * perq0 + u;
+      if (l < w && S.segarg[l] != INT_MAX) ++cnt;
+    }
+    int P;
+    int pos = block_excl_scan(cnt, ws, P);
+    for (int u = 0; u < perq0; ++u) {
+      int l = tid * perq0 + u;
+      if (l < w && S.segarg[l] != INT_MAX) S.cand[pos++] = (int16_t)S.segarg[l];
+    }
+    __syncthreads();
+    SEL_PROF(2);
+    const int k = w - R.target;
+    if (P <= k) {
+      for (int q = tid; q < P; q += blockDim.x) S.sel[q] = S.cand[q];
+      b = P;
+    } else {  // keep the k cheapest by (cost, col) (batching.py:66-68)
+      const int perq = (P + blockDim.x - 1) / blockDim.x;
+      unsigned keep = 0;
+      for (int u = 0; u < perq; ++u) {
+        int q = tid * perq + u;
+        if (q < P) {
+          const Cost cq = S.lce[S.cand[q]];
+          int rk = 0;
+          for (int o = 0; o < P; ++o) {
+            const Cost co = S.lce[S.cand[o]];
+            rk += (co < cq) || (co == cq && o < q);
+          }
+          if (rk < k) keep |= 1u << u;
+        }
+      }
+      int tot;
+      int p2 = block_excl_scan(__popc(keep), ws, tot);
+      for (int u = 0; u < perq; ++u)
+        if (keep >> u & 1u) S.sel[p2++] = S.cand[tid * perq + u];
+      b = k;
+    }
+  }
+  __syncthreads();
+  SEL_PROF(3);
+  // trace (seams.py:68-81): walk each seam's block-end columns through the staged deltas,
+  // keeping those of this CTA's blocks (bl % CL == rank); then decode (seam, block) pairs
+  // in parallel into the removed-column log
+  int16_t* log = R.rem;  // rows x rem_cap, this batch's columns at [removed, removed + b)
+  for (int s = tid; s < b; s += blockDim.x) {
+    int c = S.sel[s];
+    int next_mine = (nblk - 1) - ((nblk - 1 - (int)rank) % CL + CL) % CL;  // highest block with bl % CL == rank
+    for (int bl = nblk - 1; bl >= 0; --bl) {
+      if (bl == next_mine) {
+        R.cend[(long)bl * pitch + s] = (int16_t)c;
+        next_mine -= CL;
+      }
+      c += stage_dtab ? lds_s8(smem_u32(S.dtab) + (uint32_t)bl * (uint32_t)pitch + (uint32_t)c)
+                      : (int)dsrc[(size_t)bl * pitch + c];
+    }
+    if (rank == 0) log[removed + s] = (int16_t)c;  // row 0 (== the seam's label)
+  }
+  __syncthreads();
+  const int myblk = nblk > (int)rank ? (nblk - 1 - (int)rank) / CL + 1 : 0;
+  // each thread walks one (seam, block) pair: path words (fp64 pass: one word per pair) or the
+  // choice words of the columns the seam visits (int passes; L1/L2-resident, just written)
+  for (int q = tid; q < b * myblk; q += blockDim.x) {
+    int s = q / myblk, bl = (int)rank + (q - s * myblk) * CL;
+    int c = R.cend[(long)bl * pitch + s];
+    const uint64_t* pwb = R.pw + (long)bl * pitch;
+    int i_start = 1 + bl * kBlockRows;
+    int i_end = min(i_start + kBlockRows, rows) - 1;
+    if constexpr (F64) {  // path word of the seam's end column
+      uint64_t word = pwb[c];
+      for (int i = i_end; i >= i_start; --i) {
+        log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
+        c += (int)(word & 3u) - 1;
+        word >>= 2;
+      }
+    } else {
+      for (int i = i_end, qq = 0; i >= i_start; --i, ++qq) {
+        log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
+        c += (int)((pwb[c] >> (2 * qq)) & 3u) - 1;
+      }
+    }
+  }
+  SEL_PROF(4);
+  if (rank == 0 && R.cols != nullptr)
+    for (int s = tid; s < b; s += blockDim.x) {
+      R.cols[removed + s] = S.sel[s];
+      R.costs[removed + s] = (double)S.lce[S.sel[s]];
+    }
+  if (rank == 0 && tid == 0) R.sizes[iters] = b;  // every CTA reads them in the final phase
+  return b;
+}
+
 // One DP pass + select + trace for every active run (one cluster per run).  Per-run state
 // (width, iters, removed) is read at entry and written back at exit.
-__global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun* __restrict__ runs, int CL) {
+// fp64_smem: this launch's dynamic shared memory holds the fp64 layouts (a buffered run's first
+// pass, every pass with reaverage_energy); int-pass launches get the smaller int layout, so two
+// pass CTAs fit on an SM.
+__global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun* __restrict__ runs, int CL,
+                                                                       int fp64_smem) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int ws[32];
   __shared__ __align__(8) uint64_t s_xbar[2];
@@ -1010,7 +1221,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
   }
   const int rows = R.rows, pitch = R.pitch;
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
-  const bool stage_dtab = R.stage_dtab != 0;
   const int plane = 0;  // planes are compacted in place
   long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tp = clock64();
@@ -1019,6 +1229,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
   const int per = ((w + CL - 1) / CL + 15) & ~15;
   const int ndp = min(kMaxWarps, (per + kOwn - 1) / kOwn);
   const bool fp64 = R.U != nullptr && (iters == 0 || R.reaverage);  // reaverage: every pass on the mean
+  if (fp64 && !fp64_smem) __trap();  // (launcher bug: an int-sized launch reached an fp64 pass)
   if (tid == 0) {
     mbar_init(&s_xbar[0], 1);
     mbar_init(&s_xbar[1], 1);
@@ -1051,8 +1262,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
     const bool in_dp = wid < ndp || per < kXRows;
     // helper warps: the block-end global stores of DP warp (wid - ndp), off its critical path
     const bool helpers = per >= kXRows && 2 * ndp <= kMaxWarps;
-    uint8_t* ring = smem + 2 * sizeof(double) * (size_t)pitch;
-    uint32_t* pw_stage0 = reinterpret_cast<uint32_t*>(ring + (size_t)ndp * dp_ring_bytes<true>());
+    uint8_t* ring = smem + 2 * (fp64 ? 8 : 4) * (size_t)pitch;
+    uint32_t* pw_stage0 = reinterpret_cast<uint32_t*>(ring + (size_t)ndp * (fp64 ? dp_ring_bytes<true>()
+                                                                                 : dp_ring_bytes<false>()));
     if (in_dp) {
       const Geo g = geo(wid);
       uint32_t* pw_stage = pw_stage0 + wid * 2 * kPwStageWords;
@@ -1076,202 +1288,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
   long long t_dp = clock64() - tp;
   tp = clock64();
 
-    // ---------------- 2. select (redundant per CTA)
-    SelSmem S;
-    {
-      uint8_t* p = smem;
-      S.lce = reinterpret_cast<double*>(p);
-      p += 8 * (size_t)pitch;
-      S.segmin = reinterpret_cast<unsigned long long*>(p);
-      p += 8 * (size_t)pitch;
-      S.lab = reinterpret_cast<int*>(p);
-      p += 4 * (size_t)pitch;
-      S.segarg = reinterpret_cast<int*>(p);
-      p += 4 * (size_t)pitch;
-      S.cand = reinterpret_cast<int*>(p);
-      p += 4 * (size_t)pitch;
-      S.sel = reinterpret_cast<int*>(p);
-      p += 4 * (size_t)pitch;
-      S.dtab = stage_dtab ? reinterpret_cast<int8_t*>(p) : nullptr;
-    }
-    const int8_t* dsrc = R.delta;
-    if (stage_dtab && tid == 0) {
-      // one bulk copy of the whole landing-delta table; the DP's generic-proxy stores (every
-      // CTA, published by the cluster barrier) are ordered before the async-proxy read
-      fence_proxy_async_global();
-      mbar_arrive_tx(&s_dbar, (uint32_t)((size_t)nblk * pitch));
-      bulk_g2s(S.dtab, R.delta, (uint32_t)((size_t)nblk * pitch), &s_dbar);
-    }
-    for (int j = tid; j < w; j += blockDim.x) {
-      S.lce[j] = R.lastce[j];
-      S.segmin[j] = ~0ull;
-      S.segarg[j] = INT_MAX;
-    }
-    if (stage_dtab) {
-      mbar_wait(&s_dbar, 0);
-      dsrc = S.dtab;
-    }
-    __syncthreads();
-    [[maybe_unused]] long long ts = DP_CLOCK();
-    // labels (batching.py:39-46): chain the block landing deltas, 8 columns per thread in flight
-    // (shared-memory table: 32-bit shared addresses, no generic-address resolution per step)
-    for (int jb = tid; jb < w; jb += 8 * blockDim.x) {
-      int c[8];
-      bool ok[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        c[u] = jb + u * (int)blockDim.x;
-        ok[u] = c[u] < w;
-        if (!ok[u]) c[u] = 0;
-      }
-      if (stage_dtab) {
-        uint32_t row = smem_u32(S.dtab) + (uint32_t)(nblk - 1) * (uint32_t)pitch;
-        for (int bl = nblk - 1; bl >= 0; --bl, row -= (uint32_t)pitch) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) c[u] += lds_s8(row + (uint32_t)c[u]);
-        }
-      } else {
-        for (int bl = nblk - 1; bl >= 0; --bl) {
-          const int8_t* drow = dsrc + (size_t)bl * pitch;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) c[u] += drow[c[u]];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (ok[u]) S.lab[jb + u * blockDim.x] = c[u];
-    }
-    __syncthreads();
-    SEL_PROF(0);
-    if (rank == 0 && R.labs != nullptr)  // seam dump: this pass's labels (label_parents)
-      for (int j = tid; j < w; j += blockDim.x) R.labs[(long)iters * R.width0 + j] = (int16_t)S.lab[j];
-    int b;
-    if (R.kmax == 1) {  // raw mode: min_seam, leftmost global minimum (seams.py:84-89)
-      for (int j = tid; j < w; j += blockDim.x)
-        atomicMin(&S.segmin[0], (unsigned long long)__double_as_longlong(S.lce[j]));
-      __syncthreads();
-      for (int j = tid; j < w; j += blockDim.x)
-        if ((unsigned long long)__double_as_longlong(S.lce[j]) == S.segmin[0]) atomicMin(&S.segarg[0], j);
-      __syncthreads();
-      if (tid == 0) S.sel[0] = S.segarg[0];
-      b = 1;
-    } else {
-      // per parent the leftmost strict minimum (batching.py:59-64); doubles >= 0 order as u64
-      for (int j = tid; j < w; j += blockDim.x)
-        atomicMin(&S.segmin[S.lab[j]], (unsigned long long)__double_as_longlong(S.lce[j]));
-      __syncthreads();
-      for (int j = tid; j < w; j += blockDim.x)
-        if ((unsigned long long)__double_as_longlong(S.lce[j]) == S.segmin[S.lab[j]])
-          atomicMin(&S.segarg[S.lab[j]], j);
-      __syncthreads();
-      SEL_PROF(1);
-      const int perq0 = (w + blockDim.x - 1) / blockDim.x;
-      int cnt = 0;
-      for (int u = 0; u < perq0; ++u) {
-        int l = tid * perq0 + u;
-        if (l < w && S.segarg[l] != INT_MAX) ++cnt;
-      }
-      int P;
-      int pos = block_excl_scan(cnt, ws, P);
-      for (int u = 0; u < perq0; ++u) {
-        int l = tid * perq0 + u;
-        if (l < w && S.segarg[l] != INT_MAX) S.cand[pos++] = S.segarg[l];
-      }
-      __syncthreads();
-      SEL_PROF(2);
-      const int k = w - R.target;
-      if (P <= k) {
-        for (int q = tid; q < P; q += blockDim.x) S.sel[q] = S.cand[q];
-        b = P;
-      } else {  // keep the k cheapest by (cost, col) (batching.py:66-68)
-        const int perq = (P + blockDim.x - 1) / blockDim.x;
-        unsigned keep = 0;
-        for (int u = 0; u < perq; ++u) {
-          int q = tid * perq + u;
-          if (q < P) {
-            double cq = S.lce[S.cand[q]];
-            int rk = 0;
-            for (int o = 0; o < P; ++o) {
-              double co = S.lce[S.cand[o]];
-              rk += (co < cq) || (co == cq && o < q);
-            }
-            if (rk < k) keep |= 1u << u;
-          }
-        }
-        int tot;
-        int p2 = block_excl_scan(__popc(keep), ws, tot);
-        for (int u = 0; u < perq; ++u)
-          if (keep >> u & 1u) S.sel[p2++] = S.cand[tid * perq + u];
-        b = k;
-      }
-    }
-    __syncthreads();
-    SEL_PROF(3);
-    // trace (seams.py:68-81): walk each seam's block-end columns through the staged deltas,
-    // keeping those of this CTA's blocks (bl % CL == rank); then decode (seam, block) pairs
-    // in parallel into the removed-column log
-    int16_t* log = R.rem;  // rows x rem_cap, this batch's columns at [removed, removed + b)
-    for (int s = tid; s < b; s += blockDim.x) {
-      int c = S.sel[s];
-      int next_mine = (nblk - 1) - ((nblk - 1 - (int)rank) % CL + CL) % CL;  // highest block with bl % CL == rank
-      for (int bl = nblk - 1; bl >= 0; --bl) {
-        if (bl == next_mine) {
-          R.cend[(long)bl * pitch + s] = (int16_t)c;
-          next_mine -= CL;
-        }
-        c += stage_dtab ? lds_s8(smem_u32(S.dtab) + (uint32_t)bl * (uint32_t)pitch + (uint32_t)c)
-                        : (int)dsrc[(size_t)bl * pitch + c];
-      }
-      if (rank == 0) log[removed + s] = (int16_t)c;  // row 0 (== the seam's label)
-    }
-    __syncthreads();
-    const int myblk = nblk > (int)rank ? (nblk - 1 - (int)rank) / CL + 1 : 0;
-    // int passes: this CTA's blocks of choice words move into shared memory (the landing-
-    // delta table is no longer needed) with bulk copies, so the walk below reads smem
-    const bool stage_cw = !fp64 && stage_dtab && CL >= 4 && b > 0 && myblk > 0;
-    if (stage_cw) {
-      if (tid == 0) {
-        fence_proxy_async_global();
-        mbar_arrive_tx(&s_dbar, (uint32_t)(myblk * pitch * 8));
-        for (int m = 0; m < myblk; ++m)
-          bulk_g2s(S.dtab + (size_t)m * pitch * 8, R.pw + (long)((int)rank + m * CL) * pitch, (uint32_t)pitch * 8u,
-                   &s_dbar);
-      }
-      mbar_wait(&s_dbar, 1);
-    }
-    for (int q = tid; q < b * myblk; q += blockDim.x) {
-      int s = q / myblk, bl = (int)rank + (q - s * myblk) * CL;
-      int c = R.cend[(long)bl * pitch + s];
-      const uint64_t* pwb = R.pw + (long)bl * pitch;
-      const uint32_t cws = smem_u32(S.dtab) + (uint32_t)((q - s * myblk) * pitch) * 8u;
-      int i_start = 1 + bl * kBlockRows;
-      int i_end = min(i_start + kBlockRows, rows) - 1;
-      if (fp64) {  // path word of the seam's end column
-        uint64_t word = pwb[c];
-        for (int i = i_end; i >= i_start; --i) {
-          log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
-          c += (int)(word & 3u) - 1;
-          word >>= 2;
-        }
-      } else if (stage_cw) {  // choice words of the visited columns (shared memory)
-        for (int i = i_end, q = 0; i >= i_start; --i, ++q) {
-          log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
-          c += (int)((lds64_u(cws + 8u * (uint32_t)c) >> (2 * q)) & 3u) - 1;
-        }
-      } else {
-        for (int i = i_end, q = 0; i >= i_start; --i, ++q) {
-          log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
-          c += (int)((pwb[c] >> (2 * q)) & 3u) - 1;
-        }
-      }
-    }
-    SEL_PROF(4);
-    if (rank == 0 && R.cols != nullptr)
-      for (int s = tid; s < b; s += blockDim.x) {
-        R.cols[removed + s] = (int16_t)S.sel[s];
-        R.costs[removed + s] = S.lce[S.sel[s]];
-      }
-    if (rank == 0 && tid == 0) R.sizes[iters] = b;  // every CTA reads them in the final phase
+  // ---------------- 2. select + trace (redundant per CTA)
+  const int b = fp64 ? select_trace<true>(R, smem, ws, &s_dbar, w, iters, removed, rank, CL, nblk)
+                     : select_trace<false>(R, smem, ws, &s_dbar, w, iters, removed, rank, CL, nblk);
   cluster_sync();  // the batch's log is complete before the row kernels read it
   if (rank == 0 && tid == 0) {
     Rg.b = b;
@@ -1542,17 +1561,20 @@ int carve_cluster_size(int nruns, int width, int num_sms) {
 }
 
 
-constexpr size_t kSmemBudget = 220 * 1024;
+// Int-pass launches fit two pass CTAs on an SM (228 KB of shared memory, 1 KB reserved per
+// CTA, the static barriers); fp64 launches may take the whole opt-in.
+constexpr size_t kSmemBudgetInt = 111 * 1024;
+constexpr size_t kSmemBudgetF64 = 220 * 1024;
 
-size_t carve_smem_bytes(int rows, int pitch, bool stage, int cl, int dp_warps) {
+size_t dp_smem_bytes(int pitch, int dp_warps, bool f64) {
+  return 2 * (size_t)(f64 ? 8 : 4) * pitch +
+         (size_t)dp_warps * ((f64 ? dp_ring_bytes<true>() : dp_ring_bytes<false>()) + 8 * kPwStageWords);
+}
+
+size_t carve_smem_bytes(int rows, int pitch, bool stage, int dp_warps, bool f64) {
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
-  size_t dp = 2 * sizeof(double) * (size_t)pitch + (size_t)dp_warps * (dp_ring_bytes<true>() + 8 * kPwStageWords);
-  size_t sel = (size_t)pitch * (8 + 8 + 4 * 4) + 16;
-  if (stage) {  // delta table, later (clusters of >= 4) this CTA's blocks of 64-bit choice words
-    const size_t dtab = (size_t)(nblk + 3) * pitch;
-    const size_t cw = cl >= 4 ? (size_t)((nblk + cl - 1) / cl) * pitch * 8 : 0;
-    sel += dtab > cw ? dtab : cw;
-  }
+  const size_t dp = dp_smem_bytes(pitch, dp_warps, f64);
+  const size_t sel = (f64 ? sel_bytes<true>(pitch) : sel_bytes<false>(pitch)) + (stage ? (size_t)nblk * pitch : 0);
   return dp > sel ? dp : sel;
 }
 
@@ -1561,25 +1583,28 @@ int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
 // pass, compact, gradient, check (+ mean with reaverage_energy)
 int carve_kernels_per_iteration(bool reaverage) { return reaverage ? 5 : 4; }
 
+// the landing-delta table is staged in shared memory when the int layout still fits two CTAs
+// per SM with it (and the fp64 layout the opt-in)
 bool carve_stage_dtab(int rows, int pitch, int cl) {
-  return carve_smem_bytes(rows, pitch, true, cl, carve_dp_warps(pitch, cl)) <= kSmemBudget;
+  const int dpw = carve_dp_warps(pitch, cl);
+  return carve_smem_bytes(rows, pitch, true, dpw, false) <= kSmemBudgetInt &&
+         carve_smem_bytes(rows, pitch, true, dpw, true) <= kSmemBudgetF64;
 }
 
+// one carve iteration (pass, compaction, gradient [, mean]); f64 = the pass may be an fp64 one
+// (first pass of runs with a uniform map, or reaverage_energy): the larger shared-memory layout
 void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
-                            int max_fr, bool reaverage) {
+                            int max_fr, bool reaverage, bool f64) {
   if (nruns == 0) return;
   const int dpw = carve_dp_warps(width, cl);
   SCPL_ARG(dpw <= kMaxWarps, "carve width too large for the cluster size");
   const bool stage = carve_stage_dtab(rows, pitch, cl);
-  size_t smem = carve_smem_bytes(rows, pitch, stage, cl, dpw);
+  f64 = f64 || reaverage;
+  size_t smem = carve_smem_bytes(rows, pitch, stage, dpw, f64);
   SCPL_ARG(smem <= 227 * 1024, "carve plane too large for shared memory");
   smem_optin(reinterpret_cast<const void*>(carve_pass_kernel));
-  if (cl > 8) {
-    static bool nonportable = false;
-    if (!nonportable)
-      SCPL_CUDA(cudaFuncSetAttribute(carve_pass_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    nonportable = true;
-  }
+  if (cl > 8 && once_per_device(reinterpret_cast<const void*>(&launch_carve_iteration)))
+    SCPL_CUDA(cudaFuncSetAttribute(carve_pass_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nruns * cl);
   cfg.blockDim = dim3(kMaxWarps * 32);
@@ -1592,7 +1617,7 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl));
+  SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl, f64 ? 1 : 0));
   SCPL_CHECK_LAUNCH();
   const size_t csmem = carve_compact_smem(pitch);
   smem_optin(reinterpret_cast<const void*>(carve_compact_kernel));
@@ -1649,39 +1674,56 @@ __global__ void carve_check_kernel(const CarveRun* __restrict__ runs, int nruns,
   }
 }
 
-// carve every run to its target in ONE graph launch: while (any run above target)
-// { pass; compact; gradient } -- no host round trip per iteration.
+static void launch_carve_check(CarveRun* runs_d, int nruns, int max_iters, int* iters_d,
+                               cudaGraphConditionalHandle h, cudaStream_t cs) {
+  cudaLaunchAttribute pa[1];
+  pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pa[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cc = {};
+  cc.gridDim = dim3(1);
+  cc.blockDim = dim3(256);
+  cc.stream = cs;
+  cc.attrs = pa;
+  cc.numAttrs = 1;
+  SCPL_CUDA(cudaLaunchKernelEx(&cc, carve_check_kernel, (const CarveRun*)runs_d, nruns, max_iters, iters_d, h));
+}
+
+// carve every run to its target in ONE graph launch: [first iteration with the fp64-sized
+// pass, then] while (any run above target) { pass; compact; gradient } -- no host round trip
+// per iteration.  first_f64: the runs' first pass is an fp64 one (they carry a uniform map).
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
-                                 int* iters_d, int max_fr, bool reaverage) {
+                                 int* iters_d, int max_fr, bool reaverage, bool first_f64) {
   cudaGraph_t g;
   SCPL_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
   SCPL_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaStream_t cs;
+  SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  const long before = g_launches.load();
+  cudaGraphNode_t pro_last = nullptr;
+  if (first_f64 && !reaverage) {  // prologue: the fp64 pass, then the condition for the loop
+    SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, true);
+    launch_carve_check(runs_d, nruns, max_iters, iters_d, h, cs);
+    cudaStreamCaptureStatus cst;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    SCPL_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps));
+    SCPL_ARG(ndeps == 1, "internal: carve prologue must end in one node");
+    pro_last = deps[0];  // the check kernel
+    SCPL_CUDA(cudaStreamEndCapture(cs, &g));
+  }
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
   cudaGraphNode_t cond;
-  SCPL_CUDA(cudaGraphAddNode(&cond, g, nullptr, 0, &cp));
+  SCPL_CUDA(cudaGraphAddNode(&cond, g, pro_last ? &pro_last : nullptr, pro_last ? 1 : 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  cudaStream_t cs;
-  SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  const long before = g_launches.load();
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage);
-  {
-    cudaLaunchAttribute pa[1];
-    pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pa[0].val.programmaticStreamSerializationAllowed = 1;
-    cudaLaunchConfig_t cc = {};
-    cc.gridDim = dim3(1);
-    cc.blockDim = dim3(256);
-    cc.stream = cs;
-    cc.attrs = pa;
-    cc.numAttrs = 1;
-    SCPL_CUDA(cudaLaunchKernelEx(&cc, carve_check_kernel, (const CarveRun*)runs_d, nruns, max_iters, iters_d, h));
-  }
+  launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false);
+  launch_carve_check(runs_d, nruns, max_iters, iters_d, h, cs);
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
   g_launches.store(before);  // counted per executed iteration by the caller
   cudaGraphExec_t ex;

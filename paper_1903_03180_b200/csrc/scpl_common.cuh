@@ -37,6 +37,8 @@ static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 // Opt a kernel into the full 227 KB of dynamic shared memory, once per process: setting a
 // function attribute while that kernel runs on another stream can serialise the host.
 void smem_optin(const void* kernel);
+// true the first time (current device, key) is seen (per-device one-time attribute setup)
+bool once_per_device(const void* key);
 
 // ---------------------------------------------------------------- exact arithmetic
 // energy.py:35 -- luma = rint(fma(b,.114, fma(r,.299, g*.587))).  Outside the exact

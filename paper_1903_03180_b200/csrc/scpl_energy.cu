@@ -26,7 +26,6 @@ namespace scpl {
 constexpr int kCW = 128, kCH = 32;      // output tile
 constexpr int kCRows = kCH + 2;         // luma rows incl. halo
 constexpr int kRawPx = kCW + 32;        // raw columns: c0-16 .. c0+143 (16-aligned box start)
-constexpr int kLumW = kCW + 8;          // luma columns: c0-4 .. c0+131
 constexpr int kLumStride = 144;         // bytes per luma row in shared memory
 constexpr int kCodesThreads = 256;      // 8 warps: warp = 4 output rows, lane = 4 columns
 
@@ -314,11 +313,13 @@ static void launch_codes_c(const uint8_t* frames, const uint8_t* prev_frame, int
   const size_t smem = 2 * (size_t)G::kSlot + (size_t)kCRows * kLumStride + 16;
   const int tiles_x = cdiv(W, kCW), tiles = tiles_x * cdiv(H, kCH);
   const long units = (long)tiles * n;
-  static int per_sm = 0;  // resident CTAs per SM (queried once)
+  static std::atomic<int> per_sm_cache{0};  // resident CTAs per SM (same on every B200)
+  int per_sm = per_sm_cache.load();
+  smem_optin(reinterpret_cast<const void*>(codes_kernel<C>));  // (once per device)
   if (per_sm == 0) {
-    smem_optin(reinterpret_cast<const void*>(codes_kernel<C>));
     SCPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, codes_kernel<C>, kCodesThreads, smem));
     if (per_sm < 1) per_sm = 1;
+    per_sm_cache.store(per_sm);
   }
   const long grid = std::min<long>(units, (long)num_sms * per_sm);
   codes_kernel<C><<<(int)grid, kCodesThreads, smem, st>>>(tm, frames, prev_frame, t0, n, H, W, tiles_x, units,

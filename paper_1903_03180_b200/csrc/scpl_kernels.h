@@ -111,11 +111,11 @@ struct alignas(64) CarveRun {
   int carve_cluster_size(int nruns, int width, int num_sms); \
   void encode_carve_tensor_maps(CarveRun& R); \
   void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st, \
-                              int max_fr = 1, bool reaverage = false); \
+                              int max_fr = 1, bool reaverage = false, bool f64 = false); \
   void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st); \
   void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st); \
   cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters, \
-                                   int* iters_d, int max_fr = 1, bool reaverage = false); \
+                                   int* iters_d, int max_fr = 1, bool reaverage = false, bool first_f64 = false); \
   bool carve_stage_dtab(int rows, int pitch, int cl); \
   int carve_kernels_per_iteration(bool reaverage); \
   int carve_warps(int width, int cl); \

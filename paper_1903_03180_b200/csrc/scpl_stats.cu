@@ -335,11 +335,8 @@ __global__ void __launch_bounds__(256, 4) window_stats_scan_kernel(ScanState* S,
 }
 
 static void stats_smem_attr() {
-  static bool done = false;
-  if (done) return;
-  smem_optin(reinterpret_cast<const void*>(window_stats_kernel));
+  smem_optin(reinterpret_cast<const void*>(window_stats_kernel));  // (once per device)
   smem_optin(reinterpret_cast<const void*>(window_stats_scan_kernel));
-  done = true;
 }
 
 // ------------------------------------------------------------ device: tree fold
@@ -652,9 +649,70 @@ __global__ void uniform_kernel(const uint16_t* __restrict__ codes, int H, int W,
   }
 }
 
+// Width phases (the common case): each thread owns 8 consecutive pixels of a row, reads their
+// codes with one 16-byte load per frame (four frames in flight), keeps 8 sequential fp64 sums
+// (the reference's per-pixel order, buffering.py:71) and writes 8 means with 16-byte stores.
+// e is recomputed on the fp64 pipe (energy.py:86-87) instead of table loads.
+constexpr int kUniPx = 8;
+__device__ __forceinline__ double energy_fp64(uint32_t code, bool pure, double wm, double wg) {
+  const uint32_t g = code & 255u;
+  if (pure) return (double)g;
+  return fmin(__dadd_rn(__dmul_rn(wm, (double)(code >> 8)), __dmul_rn(wg, (double)g)), 255.0);
+}
+__global__ void __launch_bounds__(256) uniform_vec_kernel(const uint16_t* __restrict__ codes, int H, int W, int s,
+                                                          int n, int first_pure, double wm, double wg,
+                                                          double* __restrict__ out, int pitch) {
+  const long N = (long)H * W;
+  const long q = blockIdx.x * (long)blockDim.x + threadIdx.x;  // 8-pixel group
+  if (q * kUniPx >= N) return;
+  const long p = q * kUniPx;
+  const uint4* src = reinterpret_cast<const uint4*>(codes + (size_t)s * N + p);
+  const size_t fstride = (size_t)N / kUniPx;  // uint4 per frame
+  double acc[kUniPx];
+  {
+    const uint4 v = __ldcs(src);
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+    const bool pure = first_pure && s == 0;
+#pragma unroll
+    for (int k = 0; k < kUniPx; ++k) acc[k] = energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, pure, wm, wg);
+  }
+  int t = 1;
+  for (; t + 4 <= n; t += 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + (size_t)(t + u) * fstride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int k = 0; k < kUniPx; ++k)
+        acc[k] = __dadd_rn(acc[k], energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, false, wm, wg));
+    }
+  }
+  for (; t < n; ++t) {
+    const uint4 v = __ldcs(src + (size_t)t * fstride);
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < kUniPx; ++k)
+      acc[k] = __dadd_rn(acc[k], energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, false, wm, wg));
+  }
+  const double dn = (double)n;
+  const int i = (int)(p / W), j = (int)(p - (long)i * W);
+  double2* o = reinterpret_cast<double2*>(out + (long)i * pitch + j);
+#pragma unroll
+  for (int k = 0; k < kUniPx; k += 2) o[k / 2] = make_double2(__ddiv_rn(acc[k], dn), __ddiv_rn(acc[k + 1], dn));
+}
+
 void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
                     int transposed, double* out, cudaStream_t st, int pitch) {
   if (pitch <= 0) pitch = transposed ? H : W;
+  const long N = (long)H * W;
+  if (!transposed && W % kUniPx == 0 && pitch % 2 == 0 && (reinterpret_cast<uintptr_t>(codes) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    uniform_vec_kernel<<<cdiv(N / kUniPx, 256), 256, 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, out, pitch);
+    SCPL_CHECK_LAUNCH();
+    return;
+  }
   dim3 grid(cdiv(W, 32), cdiv(H, 32));
   uniform_kernel<<<grid, dim3(32, 8), 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, transposed, out, pitch);
   SCPL_CHECK_LAUNCH();

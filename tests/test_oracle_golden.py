@@ -85,9 +85,18 @@ def test_buffer_scan_golden(small):
         g = small["stream"][str(s)]
         assert [n for _, n in runs] == g["runs"]
         assert [fhex(a) for _, _, a, _ in tr.asde] == g["asde"]
-        # C restatement of the pairwise mean agrees push by push
-        for t, n, a, _ in tr.asde[:5]:
-            pass
+        # the C restatement of numpy's pairwise mean gives the same ASDE, push by push
+        S, Q, n_in = None, None, 0
+        for (t, n, a, ok), e in zip(tr.asde, maps[1:]):
+            if n_in == 0 or n == 2 and S is None:
+                S, Q, n_in = maps[t - 1].copy(), maps[t - 1] * maps[t - 1], 1
+            assert n == n_in + 1
+            cS, cQ = S + e, Q + e * e
+            assert fhex(O.asde_from_sums_c(cS, cQ, n)) == fhex(a)
+            if ok:
+                S, Q, n_in = cS, cQ, n
+            else:
+                S, Q, n_in = e.copy(), e * e, 1
 
 
 def test_asde_c_matches_numpy():
