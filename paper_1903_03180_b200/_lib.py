@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscpl.so")
+# SCPL_CHECKED=1 loads the checked build (device-side invariant checks, build_ext.py)
+LIB_PATH = os.path.join(_HERE, "libscpl_checked.so" if os.environ.get("SCPL_CHECKED") else "libscpl.so")
 
 _c_int_p = ctypes.POINTER(ctypes.c_int)
 _vp = ctypes.c_void_p

@@ -52,16 +52,28 @@ def _compile(entry, force: bool) -> str:
     return obj
 
 
-def build(force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
+LIB_CHECKED = os.path.join(HERE, "libscpl_checked.so")  # device invariant checks (SCPL_CHECKED=1)
+
+
+def _link(lib, objs, force):
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < _newest(objs):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-               "-o", LIB, *objs]
+               "-o", lib, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+
+
+def build(force: bool = False, checked: bool = True) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    entries = [(s, o, e) for s, o, e in SOURCES]
+    if checked:  # the same sources with -DSCPL_CHECKS into *_chk.o
+        entries += [(s, o.replace(".o", "_chk.o"), e + ["-DSCPL_CHECKS"]) for s, o, e in SOURCES]
+    with ThreadPoolExecutor(max_workers=len(entries)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, force), entries))
+    _link(LIB, objs[:len(SOURCES)], force)
+    if checked:
+        _link(LIB_CHECKED, objs[len(SOURCES):], force)
     return LIB
 
 

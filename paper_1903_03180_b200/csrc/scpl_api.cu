@@ -25,6 +25,7 @@
 #include <set>
 #include <tuple>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/scpl.h"
@@ -871,14 +872,20 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   const int prio_lo = ctx->prio_lo, prio_hi = ctx->prio_hi;
   for (cudaStream_t* x : {&ctx->s_h2d, &ctx->s_d2h})
     if (!*x) SCPL_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
-  while ((int)ctx->lanes.size() < njobs) {
+  // Clips in flight: a batch's clips take the lanes in turn (clip j on lane j % L), so the
+  // scans of later clips queue behind earlier ones on their lane while the earlier clips' runs
+  // carve -- scans and carves overlap instead of running as two phases.
+  int nlanes = njobs > 1 ? 12 : 1;
+  if (const char* e = getenv("SCPL_LANES")) nlanes = std::max(1, atoi(e));
+  nlanes = std::min(nlanes, njobs);
+  while ((int)ctx->lanes.size() < nlanes) {
     ScanLane l;
     SCPL_CUDA(cudaStreamCreateWithPriority(&l.s_codes, cudaStreamNonBlocking, prio_hi));
     SCPL_CUDA(cudaStreamCreateWithPriority(&l.s_scan, cudaStreamNonBlocking, prio_hi));
     ctx->lanes.push_back(l);
   }
   for (int j = 0; j < njobs; ++j) {
-    jobs[j].lane = &ctx->lanes[j];
+    jobs[j].lane = &ctx->lanes[j % nlanes];
     jobs[j].index = j;
   }
   const int carve_hi = prio_lo - prio_hi >= 2 ? prio_hi + 1 : prio_hi;
@@ -957,7 +964,6 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       J.scan.h_runs = reinterpret_cast<int*>(pin_take(sizeof(int) * 2 * (size_t)T));
       J.scan.h_state = reinterpret_cast<ScanState*>(pin_take(sizeof(ScanState)));
       J.scan.h_L = reinterpret_cast<int*>(pin_take(sizeof(int)));
-      scan_start(ctx, J.scan, *J.lane, J.codes.as<uint16_t>(), T, h, w, P, st);
     }
   }
   std::list<Group> groups;
@@ -999,12 +1005,14 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       SCPL_CUDA(cudaEventRecord(J.ev_chunk_codes[c], sc));
     }
   }
-  // 2. buffer scans, chunk by chunk (fixed one-frame runs for scpl / raw; given runs: none)
+  // 2. buffer scans, chunk by chunk (fixed one-frame runs for scpl / raw; given runs: none);
+  // a lane's scans run one clip after another (its scan state is reset in stream order)
   for (auto& J : jobs) {
     cudaStream_t ss = J.lane->s_scan;
     J.ev_codes = new_event(true);
     J.ev_scan = new_event(true);
     SCPL_CUDA(cudaStreamWaitEvent(ss, ev_alloc, 0));
+    if (buffered && !given) scan_start(ctx, J.scan, *J.lane, J.codes.as<uint16_t>(), T, h, w, P, ss);
     SCPL_CUDA(cudaStreamWaitEvent(ss, J.ev_chunk_codes[0], 0));
     SCPL_CUDA(cudaEventRecord(J.ev_codes, ss));  // (first chunk's codes)
     J.ev_chunk.assign(nchunk, nullptr);
@@ -1159,46 +1167,51 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
     if (const char* e = getenv("SCPL_GROUP_MIN")) min_group = std::max(1, atoi(e));
     // a batch's closed runs go out in groups of at most max_group (each group's carve loop is
     // one serial chain of pass / row kernels: more groups, more chains in flight)
-    int max_group = njobs > 1 ? 8 : 1 << 30;
+    int max_group = 1 << 30;
     if (const char* e = getenv("SCPL_GROUP_MAX")) max_group = std::max(1, atoi(e));
-    for (int c = 0; c < nchunk; ++c) {
-      const bool last_chunk = c + 1 == nchunk;
-      std::vector<RunRef> pending;
-      std::vector<cudaEvent_t> ready;
+    // event-driven: harvest every clip's chunks as they complete (any order), dispatch groups
+    std::vector<int> next(njobs, 0);
+    int remaining = njobs * nchunk;
+    std::vector<RunRef> pending;
+    std::vector<cudaEvent_t> ready;
+    while (remaining > 0) {
+      bool progress = false;
       for (auto& J : jobs) {
-        hmark("wait chunk " + std::to_string(c));
-        SCPL_CUDA(cudaEventSynchronize(J.ev_chunk[c]));
-        const int n = J.scan.h_n[c];
-        for (int r = (int)J.runs.size(); r < n; ++r) J.runs.push_back({J.scan.h_runs[2 * r], J.scan.h_runs[2 * r + 1]});
-      }
-      if (shards > 1) {  // this rank's runs, each as it closes
-        ClipJob& J = jobs[0];
-        for (int r = J.done; r < (int)J.runs.size(); ++r)
-          if (mine(J.runs[r])) dispatch({{&J, r}}, {J.ev_chunk[c]}, host_in && last_chunk);
-        J.done = (int)J.runs.size();
-        continue;
-      }
-      int npend = 0;
-      for (auto& J : jobs) npend += (int)J.runs.size() - J.done;
-      if (npend == 0 || (npend < min_group && !last_chunk)) continue;
-      for (auto& J : jobs) {
-        if ((int)J.runs.size() == J.done) continue;
-        for (int r = J.done; r < (int)J.runs.size(); ++r) {
-          pending.push_back({&J, r});
-          ready.push_back(J.ev_chunk[c]);
-          if ((int)pending.size() == max_group) {
-            dispatch(pending, ready, false);
-            pending.clear();
-            ready.clear();
+        while (next[J.index] < nchunk) {
+          const int c = next[J.index];
+          const cudaError_t q = cudaEventQuery(J.ev_chunk[c]);
+          if (q == cudaErrorNotReady) break;
+          SCPL_CUDA(q);
+          const int n = J.scan.h_n[c];
+          for (int r = (int)J.runs.size(); r < n; ++r)
+            J.runs.push_back({J.scan.h_runs[2 * r], J.scan.h_runs[2 * r + 1]});
+          ++next[J.index];
+          --remaining;
+          progress = true;
+          if (shards > 1) {  // this rank's runs (a single clip), each as it closes
+            for (int r = J.done; r < (int)J.runs.size(); ++r)
+              if (mine(J.runs[r])) dispatch({{&J, r}}, {J.ev_chunk[c]}, host_in && remaining == 0);
+            J.done = (int)J.runs.size();
+            continue;
           }
+          for (int r = J.done; r < (int)J.runs.size(); ++r) {
+            pending.push_back({&J, r});
+            ready.push_back(J.ev_chunk[c]);
+          }
+          J.done = (int)J.runs.size();
         }
-        J.done = (int)J.runs.size();
       }
       // (a device clip's scan ends long before its groups do: only a host clip's last group,
       // closed after the copies, carves with the GPU to itself)
-      std::sort(ready.begin(), ready.end());
-      ready.erase(std::unique(ready.begin(), ready.end()), ready.end());
-      dispatch(pending, ready, host_in && last_chunk && njobs == 1);
+      while ((int)pending.size() >= min_group || (remaining == 0 && !pending.empty())) {
+        const size_t k = std::min(pending.size(), (size_t)max_group);
+        std::vector<RunRef> grp(pending.begin(), pending.begin() + k);
+        std::vector<cudaEvent_t> ev(ready.begin(), ready.begin() + k);
+        pending.erase(pending.begin(), pending.begin() + k);
+        ready.erase(ready.begin(), ready.begin() + k);
+        dispatch(grp, ev, host_in && remaining == 0 && pending.empty() && njobs == 1);
+      }
+      if (!progress && remaining > 0) std::this_thread::yield();
     }
   } else {
     ClipJob& J = jobs[0];

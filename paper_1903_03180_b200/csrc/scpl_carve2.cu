@@ -878,6 +878,8 @@ __device__ __forceinline__ void compact_row(uint8_t* L, uint8_t* G, const int16_
   const bool f4 = b <= 255;
   for (int t = lane; t < b; t += 32) {
     const int16_t rv = rg[t];
+    // the batch's seams are pairwise disjoint (batching.py:104): strictly increasing per row
+    SCPL_DCHECK(rv >= t && rv < w0 && (t == 0 || rg[t - 1] < rv), "removed columns disjoint and in range");
     if (stage_list) rs[t] = rv;
     const int at = rv - t;  // >= 0
     if (f4) {
@@ -1176,12 +1178,14 @@ __device__ int select_trace(const CarveRun& R, uint8_t* smem, int* ws, uint64_t*
     if constexpr (F64) {  // path word of the seam's end column
       uint64_t word = pwb[c];
       for (int i = i_end; i >= i_start; --i) {
+        SCPL_DCHECK(c >= 0 && c < w, "trace column inside the row (fp64 pass)");
         log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
         c += (int)(word & 3u) - 1;
         word >>= 2;
       }
     } else {
       for (int i = i_end, qq = 0; i >= i_start; --i, ++qq) {
+        SCPL_DCHECK(c >= 0 && c < w, "trace column inside the row");
         log[(long)i * R.rem_cap + removed + s] = (int16_t)c;
         c += (int)((pwb[c] >> (2 * qq)) & 3u) - 1;
       }
@@ -1392,6 +1396,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) carve_index_kernel(CarveRun* _
       const int sidx = base - lane;
       int o = 0;
       if (sidx >= 0) o = alive_select(wv, pre, nw32, lg[off + sidx]);
+      SCPL_DCHECK(sidx < 0 || (o >= 0 && o < R.width0 && (wv[o >> 5] >> (o & 31) & 1u)),
+                  "index map: removed column is an alive original column");
       __syncwarp();
       if (sidx >= 0) atomicAnd(&wv[o >> 5], ~(1u << (o & 31)));
       __syncwarp();

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <atomic>
 #include <string>
@@ -33,6 +34,22 @@ struct Error {
   } while (0)
 
 static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
+
+// Device-side invariant checks of the checked build (libscpl_checked.so, -DSCPL_CHECKS; loaded
+// with SCPL_CHECKED=1): a violated invariant prints and traps, which fails the call with a
+// CUDA error.  Compiled out of the product build.
+#ifdef SCPL_CHECKS
+#define SCPL_DCHECK(cond, what)                                                                   \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("SCPL_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                  \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define SCPL_DCHECK(cond, what) ((void)0)
+#endif
 
 // Opt a kernel into the full 227 KB of dynamic shared memory, once per process: setting a
 // function attribute while that kernel runs on another stream can serialise the host.

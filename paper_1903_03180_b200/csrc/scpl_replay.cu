@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(256) replay_rows_kernel(const uint8_t* __restr
     const int16_t* ir = idx + (size_t)i * stride;
     for (int y = threadIdx.x; y < tw; y += blockDim.x) {
       int s = ir[y];
+      SCPL_DCHECK(s >= 0 && s < W, "replay index inside the row");
 #pragma unroll
       for (int c = 0; c < C; ++c) rout[y * C + c] = rin[s * C + c];
     }
@@ -92,6 +93,10 @@ __global__ void __launch_bounds__(128) replay_rows_vec_kernel(const uint8_t* __r
   int src[kRpPx];
 #pragma unroll
   for (int k = 0; k < kRpPx; ++k) src[k] = active && y0 + k < tw ? (int)idx[(size_t)i * stride + y0 + k] * C : 0;
+#pragma unroll
+  for (int k = 0; k < kRpPx; ++k)
+    SCPL_DCHECK(src[k] >= 0 && src[k] < W * C && (k == 0 || y0 + k >= tw || src[k] > src[k - 1]),
+                "replay index map strictly increasing inside the row");
   __syncthreads();
   for (int t = 0; t < T; ++t) {
     const int sl = t % kRing;

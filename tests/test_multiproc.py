@@ -80,8 +80,8 @@ def _shard_worker(rank, world, port, out):
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_clip_gather(world):
     """One clip split across ranks (sharding.py): every frame is owned by exactly
-    one rank (buffered: run r on rank r % world; scpl/raw: a contiguous frame block), and after
-    the per-span broadcasts every rank holds every frame."""
+    one rank (buffered: runs dealt to the least-loaded rank as they close; scpl/raw: a contiguous
+    frame block), and after the per-span broadcasts every rank holds every frame."""
     from paper_1903_03180_b200 import sharding
     runs = [(0, 5), (5, 3), (8, 4), (12, 1), (13, 6)]
     for mode in ("buffered", "scpl"):
@@ -96,3 +96,96 @@ def test_sharded_clip_gather(world):
     for r in range(world):
         for mode in ("buffered", "scpl"):
             assert res[r][mode] == [100 + t for t in range(19)]
+
+
+def _scan_once_worker(rank, world, port, out):
+    """scan_once mode's host plumbing: rank 0's run list reaches every rank (broadcast of host
+    objects), every rank computes the same LPT owners, and the spans gather back whole."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    from paper_1903_03180_b200 import sharding
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    runs = [(0, 62), (62, 38), (100, 3)] + [(103 + 4 * k, 4) for k in range(24)] + [(199, 2), (201, 52), (253, 47)]
+    got = sharding.broadcast_runs(runs if rank == 0 else None)
+    owners = sharding.lpt_owners(got, world)
+    T = 300
+    x = torch.full((T, 2), -1, dtype=torch.int32)
+    for s, n in sharding.owned_spans(got, rank, world, "buffered", T, owners):
+        x[s:s + n] = torch.arange(s, s + n, dtype=torch.int32)[:, None] + 1000
+    sharding.gather_runs(x, got, world, "buffered", owners=owners)
+    out[rank] = (got, owners, x[:, 0].tolist())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_scan_once_lpt_gather(world):
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_scan_once_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    runs0, owners0, _ = res[0]
+    for r in range(world):
+        runs, owners, x = res[r]
+        assert runs == runs0 and owners == owners0          # identical on every rank
+        assert x == [1000 + t for t in range(300)]          # every frame gathered
+    # LPT balance: no rank carries more than one run's cost above the least loaded one
+    load = [0.0] * world
+    for run, o in zip(runs0, owners0):
+        load[o] += 1000.0 + run[1]
+    assert max(load) - min(load) <= 1000.0 + max(n for _, n in runs0)
+
+
+def test_run_owner_assignments():
+    """libscpl's online assignment (runs in scan order to the least-loaded rank) and the LPT
+    deal: deterministic, every run owned once, loads balanced to within one run."""
+    from paper_1903_03180_b200 import sharding
+    runs = [(0, 62), (62, 38), (100, 3)] + [(103 + 4 * k, 4) for k in range(24)] + [(199, 2), (201, 52), (253, 47)]
+    for world in (1, 2, 4, 8):
+        for fn in (sharding.run_owners, sharding.lpt_owners):
+            owners = fn(runs, world)
+            assert owners == fn(runs, world) and len(owners) == len(runs)
+            assert set(owners) <= set(range(world))
+            load = [0.0] * world
+            for run, o in zip(runs, owners):
+                load[o] += 1000.0 + run[1]
+            assert max(load) - min(load) <= 1000.0 + 62
+    assert sharding.run_owners([(0, 5), (5, 3), (8, 4)], 2) == [0, 1, 1]  # least loaded (5 + 1000 > 3 + 1000)
+
+
+def _c4_worker(rank, world, port, out):
+    """BASELINE C4 across ranks: 64 clips, 64/world per rank (clip i's seed is i), no exchange
+    on the data path; the bench's max-over-ranks time reduction."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1903_03180_b200 import sharding
+    from paper_1903_03180_b200.synth import C4_CLIPS, config_clip
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = sharding.shard_clips(C4_CLIPS, rank, world)
+    digests = [int(config_clip("C4", frames=1, clip=i)[0][0, :8, :8].astype(np.int64).sum()) for i in mine[:2]]
+    worst = bench.reduce_max(float(len(mine)) + 0.5 * rank, world, "cpu")
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine)
+    out[rank] = (mine, digests, worst, gathered)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c4_clip_sharding(world):
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_c4_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    allc = sorted(c for r in range(world) for c in res[r][0])
+    assert allc == list(range(64))                           # every clip exactly once
+    assert all(len(res[r][0]) == 64 // world for r in range(world))
+    assert res[0][3] == res[world - 1][3]
+    assert res[0][2] == 64 // world + 0.5 * (world - 1)       # max over ranks
+    d = [x for r in range(world) for x in res[r][1]]
+    assert len(set(d)) == len(d)                             # different seeds, different clips
