@@ -1201,29 +1201,29 @@ __device__ int select_trace(const CarveRun& R, uint8_t* smem, int* ws, uint64_t*
   return b;
 }
 
-// One DP pass + select + trace for every active run (one cluster per run).  Per-run state
-// (width, iters, removed) is read at entry and written back at exit.
-// fp64_smem: this launch's dynamic shared memory holds the fp64 layouts (a buffered run's first
-// pass, every pass with reaverage_energy); int-pass launches get the smaller int layout, so two
-// pass CTAs fit on an SM.
-__global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun* __restrict__ runs, int CL,
-                                                                       int fp64_smem) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ int ws[32];
-  __shared__ __align__(8) uint64_t s_xbar[2];
-  __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
-  __shared__ __align__(8) uint64_t s_dbar;  // delta-table staging (select phase)
-  __shared__ __align__(8) uint64_t s_hbar[kMaxWarps * 4];  // DP warp -> helper warp staging
-  const uint32_t rank = cluster_rank();
-  CarveRun& Rg = runs[blockIdx.x / CL];
-  const CarveRun& R = Rg;  // fields read in place; the state fields are copied below
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Shared-memory barriers of a pass (static shared memory of the carve kernels)
+struct PassBars {
+  uint64_t* xbar;  // [2] neighbour exchange
+  uint64_t* rbar;  // [kMaxWarps * 6] DP energy rings
+  uint64_t* dbar;  // [1] delta-table staging
+  uint64_t* hbar;  // [kMaxWarps * 4] DP warp -> helper warp
+};
+
+// One DP pass + select + trace of run Rg on this CTA's cluster, at width w after `iters` passes
+// and `removed` seams: returns the batch size (every CTA computes the same).  The barriers are
+// initialised here (reinit: they held the previous pass's phases; every use of them is complete
+// -- the caller synchronised the cluster).  Ends with a cluster barrier: the batch's removed-
+// column log is complete.
+__device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iters, int removed, bool fp64,
+                            uint8_t* smem, int* ws, const PassBars& B, bool reinit, long long& t_dp,
+                            long long& t_sel) {
+  const CarveRun& R = Rg;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int w = R.width, iters = R.iters, removed = R.removed;
-  if (w <= R.target) {  // done: nothing this iteration
-    if (rank == 0 && tid == 0) Rg.b = 0;
-    return;
-  }
-  const int rows = R.rows, pitch = R.pitch;
+  const int rows = R.rows;
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
   const int plane = 0;  // planes are compacted in place
   long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1232,18 +1232,27 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
 
   const int per = ((w + CL - 1) / CL + 15) & ~15;
   const int ndp = min(kMaxWarps, (per + kOwn - 1) / kOwn);
-  const bool fp64 = R.U != nullptr && (iters == 0 || R.reaverage);  // reaverage: every pass on the mean
-  if (fp64 && !fp64_smem) __trap();  // (launcher bug: an int-sized launch reached an fp64 pass)
   if (tid == 0) {
-    mbar_init(&s_xbar[0], 1);
-    mbar_init(&s_xbar[1], 1);
-    mbar_init(&s_dbar, 1);
+    if (reinit) {
+      mbar_inval(&B.xbar[0]);
+      mbar_inval(&B.xbar[1]);
+      mbar_inval(B.dbar);
+    }
+    mbar_init(&B.xbar[0], 1);
+    mbar_init(&B.xbar[1], 1);
+    mbar_init(B.dbar, 1);
     if (rows > 1 && per >= kXRows)  // the pass's first exchange, announced before it can start
-      mbar_arrive_tx(&s_xbar[0], halo_bytes_for(w, CL, rank, fp64 ? 8 : 4));
+      mbar_arrive_tx(&B.xbar[0], halo_bytes_for(w, CL, rank, fp64 ? 8 : 4));
   }
   if (lane == 0) {
-    for (int k = 0; k < 6; ++k) mbar_init(&s_rbar[wid * 6 + k], 1);
-    for (int k = 0; k < 4; ++k) mbar_init(&s_hbar[wid * 4 + k], 32);
+    for (int k = 0; k < 6; ++k) {
+      if (reinit) mbar_inval(&B.rbar[wid * 6 + k]);
+      mbar_init(&B.rbar[wid * 6 + k], 1);
+    }
+    for (int k = 0; k < 4; ++k) {
+      if (reinit) mbar_inval(&B.hbar[wid * 4 + k]);
+      mbar_init(&B.hbar[wid * 4 + k], 32);
+    }
     fence_mbar_init();
   }
   uint32_t xc = 0, xm = 0, rph = 0;
@@ -1266,47 +1275,77 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
     const bool in_dp = wid < ndp || per < kXRows;
     // helper warps: the block-end global stores of DP warp (wid - ndp), off its critical path
     const bool helpers = per >= kXRows && 2 * ndp <= kMaxWarps;
+    const int pitch = R.pitch;
     uint8_t* ring = smem + 2 * (fp64 ? 8 : 4) * (size_t)pitch;
     uint32_t* pw_stage0 = reinterpret_cast<uint32_t*>(ring + (size_t)ndp * (fp64 ? dp_ring_bytes<true>()
                                                                                  : dp_ring_bytes<false>()));
     if (in_dp) {
       const Geo g = geo(wid);
       uint32_t* pw_stage = pw_stage0 + wid * 2 * kPwStageWords;
-      uint64_t* hb = helpers ? &s_hbar[wid * 4] : nullptr;
+      uint64_t* hb = helpers ? &B.hbar[wid * 4] : nullptr;
       if (fp64)
-        dp_pass<true>(R, Rg, g, plane, reinterpret_cast<double*>(smem), CL, rank, per, s_xbar, xc, xm,
-                      ring + (size_t)wid * dp_ring_bytes<true>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
+        dp_pass<true>(R, Rg, g, plane, reinterpret_cast<double*>(smem), CL, rank, per, B.xbar, xc, xm,
+                      ring + (size_t)wid * dp_ring_bytes<true>(), &B.rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
       else
-        dp_pass<false>(R, Rg, g, plane, reinterpret_cast<int*>(smem), CL, rank, per, s_xbar, xc, xm,
-                       ring + (size_t)wid * dp_ring_bytes<false>(), &s_rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
+        dp_pass<false>(R, Rg, g, plane, reinterpret_cast<int*>(smem), CL, rank, per, B.xbar, xc, xm,
+                       ring + (size_t)wid * dp_ring_bytes<false>(), &B.rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
     } else if (helpers && wid < 2 * ndp) {
       const int dw = wid - ndp;
       const uint32_t* stage = pw_stage0 + dw * 2 * kPwStageWords;
       if (fp64)
-        pw_helper<true>(R, geo(dw), stage, &s_hbar[dw * 4]);
+        pw_helper<true>(R, geo(dw), stage, &B.hbar[dw * 4]);
       else
-        pw_helper<false>(R, geo(dw), stage, &s_hbar[dw * 4]);
+        pw_helper<false>(R, geo(dw), stage, &B.hbar[dw * 4]);
     }
   }
   cluster_sync();  // lastce / pw / delta of all CTAs visible
-  long long t_dp = clock64() - tp;
+  t_dp += clock64() - tp;
   tp = clock64();
 
   // ---------------- 2. select + trace (redundant per CTA)
-  const int b = fp64 ? select_trace<true>(R, smem, ws, &s_dbar, w, iters, removed, rank, CL, nblk)
-                     : select_trace<false>(R, smem, ws, &s_dbar, w, iters, removed, rank, CL, nblk);
-  cluster_sync();  // the batch's log is complete before the row kernels read it
-  if (rank == 0 && tid == 0) {
+  const int b = fp64 ? select_trace<true>(R, smem, ws, B.dbar, w, iters, removed, rank, CL, nblk)
+                     : select_trace<false>(R, smem, ws, B.dbar, w, iters, removed, rank, CL, nblk);
+  cluster_sync();  // the batch's log is complete before the rows are compacted
+  t_sel += clock64() - tp;
+  if (rank == 0 && tid == 0 && R.prof) {
+    for (int k = 0; k < 8; ++k) R.prof[4 + k] += dprof[k];
+    if (iters < 500) R.prof[33 + 2 * iters] = (long long)globaltimer_ns();
+  }
+  return b;
+}
+
+// One DP pass + select + trace for every active run (one cluster per run).  Per-run state
+// (width, iters, removed) is read at entry and written back at exit.
+// fp64_smem: this launch's dynamic shared memory holds the fp64 layouts (a buffered run's first
+// pass, every pass with reaverage_energy); int-pass launches get the smaller int layout, so two
+// pass CTAs fit on an SM.
+__global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun* __restrict__ runs, int CL,
+                                                                       int fp64_smem) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ int ws[32];
+  __shared__ __align__(8) uint64_t s_xbar[2];
+  __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
+  __shared__ __align__(8) uint64_t s_dbar;  // delta-table staging (select phase)
+  __shared__ __align__(8) uint64_t s_hbar[kMaxWarps * 4];  // DP warp -> helper warp staging
+  const uint32_t rank = cluster_rank();
+  CarveRun& Rg = runs[blockIdx.x / CL];
+  const int w = Rg.width, iters = Rg.iters, removed = Rg.removed;
+  if (w <= Rg.target) {  // done: nothing this iteration
+    if (rank == 0 && threadIdx.x == 0) Rg.b = 0;
+    return;
+  }
+  const bool fp64 = Rg.U != nullptr && (iters == 0 || Rg.reaverage);  // reaverage: every pass on the mean
+  if (fp64 && !fp64_smem) __trap();  // (launcher bug: an int-sized launch reached an fp64 pass)
+  long long t_dp = 0, t_sel = 0;
+  const int b = cluster_pass(Rg, CL, rank, w, iters, removed, fp64, smem, ws,
+                             PassBars{s_xbar, s_rbar, &s_dbar, s_hbar}, false, t_dp, t_sel);
+  if (rank == 0 && threadIdx.x == 0) {
     Rg.b = b;
     Rg.width = w - b;
     Rg.iters = iters + 1;
     Rg.removed = removed + b;
     Rg.cyc_dp += t_dp;
-    Rg.cyc_sel += clock64() - tp;
-    if (R.prof) {
-      for (int k = 0; k < 8; ++k) R.prof[4 + k] += dprof[k];
-      if (iters < 500) R.prof[33 + 2 * iters] = (long long)globaltimer_ns();
-    }
+    Rg.cyc_sel += t_sel;
   }
 }
 
