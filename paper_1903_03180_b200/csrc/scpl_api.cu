@@ -93,7 +93,7 @@ struct scpl_ctx {
   std::map<std::tuple<long, int, const void*>, cudaGraphExec_t> scan_graphs;  // (N, spec, lane state)
   uint8_t* pin = nullptr;  // pinned scratch (pinned_scratch)
   size_t pin_cap = 0;
-  std::vector<cudaStream_t> s_carve;  // concurrent run groups
+  std::vector<std::vector<cudaStream_t>> s_carve;  // concurrent run groups, per priority level
   // Instantiated carve loops kept for reuse (instantiating / destroying a conditional graph
   // costs host time on every group): free entries by shape, each with its own run-state
   // memory that the graph's kernels point at.
@@ -315,7 +315,8 @@ struct CarveSet {
   int max_fr = 1;           // most frames carved together by one run (reaverage)
   bool reaverage = false;
   bool has_uniform = false;  // U holds a uniform map for the first pass (else the mean gradient)
-  int kc = 6;                // DP window variant (scpl_carve2.cu: kc6 / kc4)
+  int kc = 6;                // DP window variant (scpl_carve2.cu: kc6 / kc4 / kc3)
+  int kc_first = 6, cl_first = 1;  // variant + cluster of the fp64 first pass (uniform map)
   long long prof[4] = {0, 0, 0, 0};
   scpl_ctx* ctx = nullptr;
   std::array<int, 8> loop_key{};
@@ -411,6 +412,24 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   S.reaverage = reaverage;
   S.has_uniform = uniform_given;
   S.kc = kc;
+  // the fp64 first pass takes the first variant (the group's, then narrower ones) whose fp64
+  // layout still fits two pass CTAs per SM: otherwise it waits for a whole free SM while the
+  // other groups' int passes hold every SM (measured: the last run of C2 started ~7 ms late)
+  S.kc_first = kc;
+  S.cl_first = cl;
+  static const bool first_same = getenv("SCPL_FIRST_SAME") != nullptr;  // (experiments)
+  if (with_U && !reaverage && !first_same) {
+    const bool fit4 = cols <= 16 * 4 * 64, fit3 = cols <= 16 * 4 * 32;
+    for (int k : {kc, 4, 3}) {
+      if ((k == 4 && !fit4) || (k == 3 && !fit3)) continue;
+      const int c = carve_cluster(k, nruns, cols, 148);
+      if (SCPL_CARVE_FN(k, carve_f64_fits_pair)(cols, c)) {
+        S.kc_first = k;
+        S.cl_first = c;
+        break;
+      }
+    }
+  }
   S.runs.assign(nruns, CarveRun{});
   uint8_t* base = S.mem.as<uint8_t>();
   size_t plane_off = 0;
@@ -455,6 +474,7 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
       R.labs = reinterpret_cast<int16_t*>(take((size_t)rem_cap * cols * 2));  // passes <= seams removed
     }
     SCPL_CARVE_FN(kc, encode_carve_tensor_maps)(R);
+    if (S.kc_first != kc) SCPL_CARVE_FN(S.kc_first, encode_carve_tensor_map_U)(R);
   }
 }
 
@@ -476,7 +496,8 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   const bool graph = S.cols > S.target && !host_loops();
   S.ctx = ctx;
   S.loop_key = {nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
-                (int)S.reaverage + 2 * graph + 4 * S.kc + 64 * (int)S.has_uniform};
+                (int)S.reaverage + 2 * graph + 4 * S.kc + 64 * (int)S.has_uniform + 128 * S.kc_first +
+                    2048 * S.cl_first};
   auto it = ctx->loop_pool.find(S.loop_key);
   if (it != ctx->loop_pool.end()) {
     S.loop = it->second;
@@ -492,16 +513,20 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   CarveRun* runs_d = reinterpret_cast<CarveRun*>(S.loop.mem);
   int* iters_d = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(S.loop.mem) + sizeof(CarveRun) * nruns);
   std::memcpy(h_runs, S.runs.data(), sizeof(CarveRun) * nruns);
-  // run states and the zeroed counter from mapped pinned memory
-  kc6::launch_word_copy(runs_d, h_runs, sizeof(CarveRun) * nruns + sizeof(int), st);
+  // run states and the zeroed loop counters (iterations, CTAs done) from mapped pinned memory
+  S.h_iters[1] = 0;
+  kc6::launch_word_copy(runs_d, h_runs, sizeof(CarveRun) * nruns + 2 * sizeof(int), st);
   if (S.reaverage && !S.has_uniform)  // first pass on the mean gradient too (pipeline.py:289-290)
     kc6::launch_carve_mean(runs_d, nruns, S.rows, st);
   if (S.cols > S.target && host_loops()) {  // bursts of 8 iterations, host checks the widths
     int done_iters = 0;
     while (true) {
-      for (int k = 0; k < 8; ++k)  // (a uniform map's first pass is an fp64 one)
-        SCPL_CARVE_FN(S.kc, launch_carve_iteration)(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, st, S.max_fr,
-                                                    S.reaverage, done_iters + k == 0 && S.has_uniform);
+      for (int k = 0; k < 8; ++k) {  // (a uniform map's first pass is an fp64 one)
+        const bool first = done_iters + k == 0 && S.has_uniform && !S.reaverage;
+        SCPL_CARVE_FN(first ? S.kc_first : S.kc, launch_carve_iteration)(
+            runs_d, nruns, S.rows, S.pitch, S.cols, first ? S.cl_first : S.cl, st, S.max_fr, S.reaverage, first,
+            nullptr);
+      }
       done_iters += 8;
       kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns, st);
       SCPL_CUDA(cudaStreamSynchronize(st));
@@ -511,9 +536,9 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
     }
   } else if (graph) {
     if (!S.loop.ex)
-      S.loop.ex = SCPL_CARVE_FN(S.kc, build_carve_loop)(runs_d, nruns, S.rows, S.pitch, S.cols, S.cl,
-                                                        S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage,
-                                                        S.has_uniform);
+      S.loop.ex = SCPL_CARVE_FN(S.kc, build_carve_loop)(
+          runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage,
+          S.has_uniform, SCPL_CARVE_FN(S.kc_first, launch_carve_iteration), S.cl_first);
     SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
   kc6::launch_carve_index(runs_d, nruns, S.rows, st);
@@ -611,7 +636,8 @@ void scpl_destroy(scpl_ctx* ctx) {
     cudaFree(kv.second.vnodes);
   }
   if (ctx->pin) cudaFreeHost(ctx->pin);
-  for (cudaStream_t x : ctx->s_carve) cudaStreamDestroy(x);
+  for (auto& lv : ctx->s_carve)
+    for (cudaStream_t x : lv) cudaStreamDestroy(x);
   for (auto& kv : ctx->scan_graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : ctx->loop_pool) {
     if (kv.second.ex) cudaGraphExecDestroy(kv.second.ex);
@@ -864,7 +890,7 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   // Priorities: the scans feed everything (they release the runs), so codes and scans get the
   // highest; carve groups are ordered by position in the batch (see dispatch) -- the carve
   // passes compete for whole SMs.  Levels: prio_hi (scan) .. prio_lo; carve groups use
-  // prio_hi+1 .. prio_lo (or all if the range is tiny), kStreamsPerLevel streams each.
+  // prio_hi+1 .. prio_lo (or all if the range is tiny).
   if (!ctx->prio_known) {
     SCPL_CUDA(cudaDeviceGetStreamPriorityRange(&ctx->prio_lo, &ctx->prio_hi));
     ctx->prio_known = true;
@@ -890,13 +916,37 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   }
   const int carve_hi = prio_lo - prio_hi >= 2 ? prio_hi + 1 : prio_hi;
   const int nlevels = prio_lo - carve_hi + 1;  // levels carve_hi .. prio_lo
-  const int kStreamsPerLevel = njobs > 1 ? 8 : 4;
-  while ((int)ctx->s_carve.size() < nlevels * kStreamsPerLevel) {
-    const int level = (int)ctx->s_carve.size() / kStreamsPerLevel;  // 0 = lowest priority
-    cudaStream_t x;
-    SCPL_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_lo - level));
-    ctx->s_carve.push_back(x);
-  }
+  // Every group of a call gets a stream of its own (groups sharing a stream would carve one
+  // after the other: measured, C2's last run waited ~7 ms for an earlier group that way), up to
+  // kMaxStreamsPerLevel per priority level, created on demand.
+  const int kMaxStreamsPerLevel = 16;
+  if ((int)ctx->s_carve.size() < nlevels) ctx->s_carve.resize(nlevels);
+  std::vector<int> used_at(nlevels, 0);
+  // SCPL_CARVE_STREAMS=N (experiments): groups take N streams in turn instead (group g on stream
+  // g % N, all at the carve priority), bounding how many groups carve at once
+  static const int n_streams = getenv("SCPL_CARVE_STREAMS") ? std::max(1, atoi(getenv("SCPL_CARVE_STREAMS"))) : 0;
+  int group_count = 0;
+  auto carve_stream = [&](int level) {
+    if (n_streams > 0) level = nlevels - 1;
+    auto& v = ctx->s_carve[level];
+    if (n_streams > 0) {
+      const int k = group_count++ % n_streams;
+      while ((int)v.size() <= k) {
+        cudaStream_t x;
+        SCPL_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_lo - level));
+        v.push_back(x);
+      }
+      return v[k];
+    }
+    const int k = used_at[level]++;
+    if (k >= kMaxStreamsPerLevel) return v[k % kMaxStreamsPerLevel];
+    if ((int)v.size() <= k) {
+      cudaStream_t x;
+      SCPL_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_lo - level));  // 0 = lowest
+      v.push_back(x);
+    }
+    return v[k];
+  };
   std::vector<int> phases;  // 0 width, 1 height (pipeline.py:192-193, 246-277)
   if (!scan_only)
     for (int ax : (P.height_first ? std::vector<int>{1, 0} : std::vector<int>{0, 1})) {
@@ -1033,7 +1083,6 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
 
   // 3. carve + replay, one run group at a time as runs close
   const long total_frames = (long)T * njobs;
-  int next_stream = 0;
   auto dispatch = [&](std::vector<RunRef> rr, std::vector<cudaEvent_t> ready, bool final_group) {
     if (rr.empty()) return;
     std::sort(ready.begin(), ready.end());
@@ -1050,8 +1099,9 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       // groups go first (measured ~2% faster on C2 than the other order, and equal priorities
       // are ~30% slower); a host clip's last group closes alone after the copies and is the
       // critical path, so there the later groups go first
-      if (!host_in) level = nlevels - 1 - level;
-      G.st = ctx->s_carve[level * kStreamsPerLevel + (next_stream++ % kStreamsPerLevel)];
+      static const bool late_first = getenv("SCPL_PRIO_LATE") != nullptr;  // (experiments)
+      if (!host_in && !late_first) level = nlevels - 1 - level;
+      G.st = carve_stream(level);
     }
     cudaStream_t gs = G.st;
     SCPL_CUDA(cudaStreamWaitEvent(gs, ev_alloc, 0));

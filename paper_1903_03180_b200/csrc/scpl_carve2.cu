@@ -1029,7 +1029,9 @@ __device__ int select_trace(const CarveRun& R, uint8_t* smem, int* ws, uint64_t*
   using Bits = typename Sel::Bits;
   const int tid = threadIdx.x;
   const int rows = R.rows, pitch = R.pitch;
-  const bool stage_dtab = R.stage_dtab != 0;
+  // (the fp64 pass chains the deltas in global memory: its shared memory stays small enough for
+  // two pass CTAs per SM; it is one pass per run)
+  const bool stage_dtab = R.stage_dtab != 0 && !F64;
   Sel S;
   S.carve(smem, pitch, stage_dtab);
   const int8_t* dsrc = R.delta;
@@ -1581,6 +1583,12 @@ void encode_carve_tensor_maps(CarveRun& R) {
   for (int p = 0; p < 2; ++p)
     encode_plane(&R.tm_grad[p], R.grad[p], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, R.width0, R.rows, R.pitch,
                  DpCfg<false>::kStageRows);
+  encode_carve_tensor_map_U(R);
+}
+
+// the fp64 plane's map alone (box = this variant's ring row): the fp64 first pass may run with
+// another variant than the int passes
+void encode_carve_tensor_map_U(CarveRun& R) {
   if (R.U)
     encode_plane(&R.tm_U, R.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, R.width0, R.rows, R.pitch,
                  DpCfg<true>::kStageRows);
@@ -1619,9 +1627,15 @@ size_t dp_smem_bytes(int pitch, int dp_warps, bool f64) {
 size_t carve_smem_bytes(int rows, int pitch, bool stage, int dp_warps, bool f64) {
   const int nblk = (rows - 1 + kBlockRows - 1) / kBlockRows;
   const size_t dp = dp_smem_bytes(pitch, dp_warps, f64);
-  const size_t sel = (f64 ? sel_bytes<true>(pitch) : sel_bytes<false>(pitch)) + (stage ? (size_t)nblk * pitch : 0);
+  // (the fp64 pass never stages the delta table: select_trace)
+  const size_t sel = f64 ? sel_bytes<true>(pitch) : sel_bytes<false>(pitch) + (stage ? (size_t)nblk * pitch : 0);
   return dp > sel ? dp : sel;
 }
+
+// shared memory of this variant's fp64 pass (the first pass of a run with a uniform map): the
+// launcher runs that pass with the narrowest variant that keeps it within the two-CTA budget
+size_t carve_f64_smem(int width, int cl) { return carve_smem_bytes(2, (width + 15) & ~15, false, carve_dp_warps(width, cl), true); }
+bool carve_f64_fits_pair(int width, int cl) { return carve_f64_smem(width, cl) <= kSmemBudgetInt; }
 
 int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
 
@@ -1631,15 +1645,44 @@ int carve_kernels_per_iteration(bool reaverage) { return reaverage ? 5 : 4; }
 // the landing-delta table is staged in shared memory when the int layout still fits two CTAs
 // per SM with it (and the fp64 layout the opt-in)
 bool carve_stage_dtab(int rows, int pitch, int cl) {
-  const int dpw = carve_dp_warps(pitch, cl);
-  return carve_smem_bytes(rows, pitch, true, dpw, false) <= kSmemBudgetInt &&
-         carve_smem_bytes(rows, pitch, true, dpw, true) <= kSmemBudgetF64;
+  return carve_smem_bytes(rows, pitch, true, carve_dp_warps(pitch, cl), false) <= kSmemBudgetInt;
 }
 
 // one carve iteration (pass, compaction, gradient [, mean]); f64 = the pass may be an fp64 one
 // (first pass of runs with a uniform map, or reaverage_energy): the larger shared-memory layout
+// Loop condition of the device-side carve loop: another iteration while any run is above its
+// target (bounded by max_iters: every pass removes at least one seam).
+__global__ void carve_check_kernel(const CarveRun* __restrict__ runs, int nruns, int max_iters, int* iters,
+                                   cudaGraphConditionalHandle loop) {
+  pdl_wait();
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < nruns; r += blockDim.x)
+    if (runs[r].width > runs[r].target) any = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int n = ++*iters;
+    cudaGraphSetConditional(loop, (any && n < max_iters) ? 1u : 0u);
+  }
+}
+
+static void launch_carve_check(CarveRun* runs_d, int nruns, int max_iters, int* iters_d,
+                               cudaGraphConditionalHandle h, cudaStream_t cs) {
+  cudaLaunchAttribute pa[1];
+  pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pa[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cc = {};
+  cc.gridDim = dim3(1);
+  cc.blockDim = dim3(256);
+  cc.stream = cs;
+  cc.attrs = pa;
+  cc.numAttrs = 1;
+  SCPL_CUDA(cudaLaunchKernelEx(&cc, carve_check_kernel, (const CarveRun*)runs_d, nruns, max_iters, iters_d, h));
+}
+
 void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
-                            int max_fr, bool reaverage, bool f64) {
+                            int max_fr, bool reaverage, bool f64, const RowsLoop* loop) {
   if (nruns == 0) return;
   const int dpw = carve_dp_warps(width, cl);
   SCPL_ARG(dpw <= kMaxWarps, "carve width too large for the cluster size");
@@ -1684,6 +1727,7 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   SCPL_CUDA(cudaLaunchKernelEx(&rc, carve_dirty_kernel, runs_d));
   SCPL_CHECK_LAUNCH();
   if (reaverage) launch_carve_mean(runs_d, nruns, rows, st);
+  if (loop) launch_carve_check(runs_d, nruns, loop->max_iters, loop->counters, loop->handle, st);
 }
 
 // Word copy by the SMs.  Small control transfers between device memory and mapped pinned
@@ -1702,42 +1746,12 @@ void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st)
   SCPL_CHECK_LAUNCH();
 }
 
-// Loop condition of the device-side carve loop: another iteration while any run is above its
-// target (bounded by max_iters: every pass removes at least one seam).
-__global__ void carve_check_kernel(const CarveRun* __restrict__ runs, int nruns, int max_iters, int* iters,
-                                   cudaGraphConditionalHandle loop) {
-  pdl_wait();
-  __shared__ int any;
-  if (threadIdx.x == 0) any = 0;
-  __syncthreads();
-  for (int r = threadIdx.x; r < nruns; r += blockDim.x)
-    if (runs[r].width > runs[r].target) any = 1;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int n = ++*iters;
-    cudaGraphSetConditional(loop, (any && n < max_iters) ? 1u : 0u);
-  }
-}
-
-static void launch_carve_check(CarveRun* runs_d, int nruns, int max_iters, int* iters_d,
-                               cudaGraphConditionalHandle h, cudaStream_t cs) {
-  cudaLaunchAttribute pa[1];
-  pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  pa[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t cc = {};
-  cc.gridDim = dim3(1);
-  cc.blockDim = dim3(256);
-  cc.stream = cs;
-  cc.attrs = pa;
-  cc.numAttrs = 1;
-  SCPL_CUDA(cudaLaunchKernelEx(&cc, carve_check_kernel, (const CarveRun*)runs_d, nruns, max_iters, iters_d, h));
-}
-
 // carve every run to its target in ONE graph launch: [first iteration with the fp64-sized
 // pass, then] while (any run above target) { pass; compact; gradient } -- no host round trip
 // per iteration.  first_f64: the runs' first pass is an fp64 one (they carry a uniform map).
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
-                                 int* iters_d, int max_fr, bool reaverage, bool first_f64) {
+                                 int* iters_d, int max_fr, bool reaverage, bool first_f64, FirstIter first,
+                                 int first_cl) {
   cudaGraph_t g;
   SCPL_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -1748,14 +1762,15 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
   cudaGraphNode_t pro_last = nullptr;
   if (first_f64 && !reaverage) {  // prologue: the fp64 pass, then the condition for the loop
     SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, true);
-    launch_carve_check(runs_d, nruns, max_iters, iters_d, h, cs);
+    const RowsLoop lp{max_iters, iters_d, h};
+    (first ? first : launch_carve_iteration)(runs_d, nruns, rows, pitch, width, first ? first_cl : cl, cs, max_fr,
+                                             reaverage, true, &lp);
     cudaStreamCaptureStatus cst;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
     SCPL_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps));
     SCPL_ARG(ndeps == 1, "internal: carve prologue must end in one node");
-    pro_last = deps[0];  // the check kernel
+    pro_last = deps[0];  // the kernel that sets the condition
     SCPL_CUDA(cudaStreamEndCapture(cs, &g));
   }
   cudaGraphNodeParams cp = {};
@@ -1767,8 +1782,10 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
   SCPL_CUDA(cudaGraphAddNode(&cond, g, pro_last ? &pro_last : nullptr, pro_last ? 1 : 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false);
-  launch_carve_check(runs_d, nruns, max_iters, iters_d, h, cs);
+  {
+    const RowsLoop lp{max_iters, iters_d, h};
+    launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false, &lp);
+  }
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
   g_launches.store(before);  // counted per executed iteration by the caller
   cudaGraphExec_t ex;

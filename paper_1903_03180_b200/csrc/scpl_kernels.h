@@ -103,6 +103,16 @@ struct alignas(64) CarveRun {
   int b;                // size of the batch selected by the latest pass (0: none)
   long long cyc_dp, cyc_sel;  // SM cycles of the DP and select/trace phases, summed over passes
 };
+// Device-side carve loop plumbing: the iteration's last kernel sets the loop's condition
+// (counters[0]: iterations executed)
+struct RowsLoop {
+  int max_iters;
+  int* counters;
+  cudaGraphConditionalHandle handle;
+};
+// one carve iteration of some DP window variant (the fp64 first pass may use another variant)
+using FirstIter = void (*)(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
+                           int max_fr, bool reaverage, bool f64, const RowsLoop* loop);
 // carve launchers (scpl_carve2.cu), compiled once per DP window width: kc6 (default) and kc4
 #define SCPL_CARVE_DECLS \
   void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes, \
@@ -111,11 +121,15 @@ struct alignas(64) CarveRun {
   int carve_cluster_size(int nruns, int width, int num_sms); \
   void encode_carve_tensor_maps(CarveRun& R); \
   void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st, \
-                              int max_fr = 1, bool reaverage = false, bool f64 = false); \
+                              int max_fr = 1, bool reaverage = false, bool f64 = false, \
+                              const RowsLoop* loop = nullptr); \
   void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st); \
   void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st); \
   cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters, \
-                                   int* iters_d, int max_fr = 1, bool reaverage = false, bool first_f64 = false); \
+                                   int* iters_d, int max_fr = 1, bool reaverage = false, bool first_f64 = false, \
+                                   FirstIter first = nullptr, int first_cl = 0); \
+  void encode_carve_tensor_map_U(CarveRun& R); \
+  bool carve_f64_fits_pair(int width, int cl); \
   bool carve_stage_dtab(int rows, int pitch, int cl); \
   int carve_kernels_per_iteration(bool reaverage); \
   int carve_warps(int width, int cl); \
