@@ -1101,6 +1101,7 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       // critical path, so there the later groups go first
       static const bool late_first = getenv("SCPL_PRIO_LATE") != nullptr;  // (experiments)
       if (!host_in && !late_first) level = nlevels - 1 - level;
+      if (final_group) level = nlevels - 1;  // (the critical path: top carve priority)
       G.st = carve_stream(level);
     }
     cudaStream_t gs = G.st;
@@ -1213,8 +1214,13 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   } else if (buffered) {
     // host clips: every closed run goes out at once (the copies are the bottleneck); device
     // clips: groups of >= 4 runs (fewer, larger carve sets), >= 8 across a batch of clips
-    int min_group = host_in ? 1 : (njobs > 1 ? 8 : 4);
-    if (const char* e = getenv("SCPL_GROUP_MIN")) min_group = std::max(1, atoi(e));
+    // device clips: pairs of runs, but a run of >= 48 frames at once and short runs (< 8 frames
+    // on average, e.g. a panning segment's 4-frame runs) as they close -- a group carves until its
+    // slowest run is done (measured: C2 13.8 ms with singles vs 14.9 with groups of 4; C5 16.9 ms
+    // with pairs vs 19.2 singles / 17.7 fours)
+    int min_group = host_in ? 1 : (njobs > 1 ? 8 : 2);
+    const bool fixed_min = getenv("SCPL_GROUP_MIN") != nullptr;
+    if (fixed_min) min_group = std::max(1, atoi(getenv("SCPL_GROUP_MIN")));
     // a batch's closed runs go out in groups of at most max_group (each group's carve loop is
     // one serial chain of pass / row kernels: more groups, more chains in flight)
     int max_group = 1 << 30;
@@ -1253,13 +1259,28 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       }
       // (a device clip's scan ends long before its groups do: only a host clip's last group,
       // closed after the copies, carves with the GPU to itself)
-      while ((int)pending.size() >= min_group || (remaining == 0 && !pending.empty())) {
+      int want = min_group;
+      if (!fixed_min && !host_in && njobs == 1 && !pending.empty()) {
+        long fr = 0;
+        int longest = 0;
+        for (auto& x : pending) {
+          fr += x.job->runs[x.r].second;
+          longest = std::max(longest, x.job->runs[x.r].second);
+        }
+        // a long run goes at once (the clip's critical paths), so do bursts of short runs
+        if (longest >= 48 || fr < 8L * (long)pending.size()) want = 1;
+      }
+      while ((int)pending.size() >= want || (remaining == 0 && !pending.empty())) {
         const size_t k = std::min(pending.size(), (size_t)max_group);
         std::vector<RunRef> grp(pending.begin(), pending.begin() + k);
         std::vector<cudaEvent_t> ev(ready.begin(), ready.begin() + k);
         pending.erase(pending.begin(), pending.begin() + k);
         ready.erase(ready.begin(), ready.begin() + k);
-        dispatch(grp, ev, host_in && remaining == 0 && pending.empty() && njobs == 1);
+        // the clip's last group (closed by the end of the scan) is the critical path of a single
+        // clip: SCPL_LAST_WIDE=1 carves it with the narrowest window at the top carve priority
+        static const bool last_wide = getenv("SCPL_LAST_WIDE") != nullptr;
+        const bool last = remaining == 0 && pending.empty() && njobs == 1;
+        dispatch(grp, ev, last && (host_in || last_wide));
       }
       if (!progress && remaining > 0) std::this_thread::yield();
     }
