@@ -239,29 +239,6 @@ def rank_workload(name: str, rank: int, frames=None):
 
 
 # ------------------------------------------------------------------ CPU legs (oracle port)
-def _oracle_window(args):
-    """Retarget one bounded window of the config clip with the oracle port (worker process)."""
-    name, start, n = args
-    sys.path.insert(0, ROOT)
-    from oracle import scpl_oracle as O
-    from paper_1903_03180_b200.synth import generate_clip
-    spec, tw, th = CONFIGS[name]
-    clip = generate_clip(spec, frames=n, threads=1, start=start)
-    t0 = time.perf_counter()
-    O.retarget_video(list(clip), target_width=tw, target_height=th, literal_replay=True)
-    return time.perf_counter() - t0
-
-
-def cpu_sample(name: str, workers: int, frames_per_worker: int, pool=None):
-    """Time of `workers` concurrent oracle windows of `frames_per_worker` frames each: the
-    slowest window's compute time (clip generation and process start-up excluded)."""
-    jobs = [(name, (w * frames_per_worker) % max(1, CONFIGS[name][0].frames - frames_per_worker),
-             frames_per_worker) for w in range(workers)]
-    if workers == 1 or pool is None:
-        return max(_oracle_window(j) for j in jobs[:1]) if workers == 1 else None
-    return max(pool.map(_oracle_window, jobs))
-
-
 def workload(name: str) -> str:
     """The config's workload name, identical on both arms."""
     spec, tw, th = CONFIGS[name]
@@ -269,30 +246,96 @@ def workload(name: str) -> str:
             f"buffered SCPL, alpha 0.2, max_len 64, wm/wg 0.6/0.4")
 
 
+def _golden_runs(name: str):
+    """The config clip's real run list (tests/golden, produced by the reference itself)."""
+    path = os.path.join(ROOT, "tests", "golden", f"{name}{'_clip0' if name == 'C4' else ''}.json")
+    with open(path) as f:
+        g = json.load(f)
+    return [tuple(r) for r in g["runs"]], int(g["dp_passes"]), float(g.get("reference_wall_s") or 0.0)
+
+
+def _oracle_run(args):
+    """One real run of the config clip through the oracle port (worker process): the energy and
+    buffer pushes of its first k_e frames, the carve of its representative frame (batch_carve on
+    the run's mean energy) and the literal replay of one frame (remove_batch per batch,
+    pipeline.py:140-154).  Returns (run length, its single-core time: per-frame costs x length +
+    the carve)."""
+    name, start, n, k_e = args
+    sys.path.insert(0, ROOT)
+    from oracle import scpl_oracle as O
+    from paper_1903_03180_b200.synth import generate_clip
+    spec, tw, th = CONFIGS[name]
+    lo = max(0, start - 1)
+    k_e = min(n, k_e)
+    fr = generate_clip(spec, frames=k_e + (start - lo), threads=1, start=lo)
+    prev = fr[0] if start > 0 else None
+    fr = fr[start - lo:]
+    t0 = time.perf_counter()
+    maps = [O.motion_energy(fr[0], prev)] + [O.motion_energy(f, p) for p, f in zip(fr[:k_e - 1], fr[1:k_e])]
+    O.buffer_scan(maps, O.BufferPolicy())  # (the pushes of these frames)
+    u = maps[0] if k_e == 1 else O.uniform_energy(maps)
+    t1 = time.perf_counter()
+    if tw is not None and tw < fr[0].shape[1]:
+        work, target, pe = fr[0], tw, u
+    else:  # height carve: the reference transposes frames and energy (pipeline.py:263-265)
+        work, target, pe = O._transpose(fr[0]), th, O._transpose(u)
+    _, batches = O.batch_carve(work, target, energy=pe)
+    t2 = time.perf_counter()
+    O.replay_batches([work], batches)
+    t3 = time.perf_counter()
+    return n, (t1 - t0) / k_e * n + (t2 - t1) + (t3 - t2) * n
+
+
 def run_reference(a, world, rank):
-    """--impl reference: the oracle port on the host cores, rank 0 only."""
+    """--impl reference: the oracle port (numpy restatement of vidcarve's path) on the host
+    cores, rank 0 only.  Each step, every core takes one REAL run of the config clip (the
+    reference's own run list, cycled so the run-length mix is the clip's) and times its energy +
+    pushes, its carve and the literal replay of its frames (measured on its first frames,
+    extrapolated to the run's length: the per-frame costs are per-frame work); the step's value is
+    the runs' frames over their summed single-core time divided by the cores."""
     if rank != 0:
         return
     from concurrent.futures import ProcessPoolExecutor
     spec, tw, th = CONFIGS[a.config]
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    workers = max(1, cores)  # every host thread: one oracle window per core, one BLAS thread each
-    fpw = 2
+    workers = max(1, cores)  # every host thread: one oracle run per core, one BLAS thread each
+    runs, dp, ref_wall = _golden_runs(a.config)
+    k_e = 2
+    nxt = 0
+
+    def step(pool):
+        nonlocal nxt
+        jobs = [(a.config, runs[(nxt + w) % len(runs)][0], runs[(nxt + w) % len(runs)][1], k_e)
+                for w in range(workers)]
+        nxt += workers
+        res = list(pool.map(_oracle_run, jobs))
+        frames = sum(n for n, _ in res)
+        core_s = sum(t for _, t in res)
+        return frames, core_s
+
     with ProcessPoolExecutor(max_workers=workers) as pool:
-        for _ in range(a.warmup):
-            cpu_sample(a.config, workers, fpw, pool)
-        times = [cpu_sample(a.config, workers, fpw, pool) for _ in range(a.steps)]
-    per_step = sum(times) / len(times)
-    value = workers * fpw / per_step
-    sample = (f"{workers} concurrent oracle windows x {fpw} frames of {a.config} "
-              f"({spec.height}x{spec.width} -> {th or spec.height}x{tw or spec.width}), buffered, literal replay; "
-              f"step time = slowest window's compute time")
+        for _ in range(min(a.warmup, 1)):  # (CPU code: one warm-up step loads the modules)
+            step(pool)
+        samples = [step(pool) for _ in range(a.steps)]
+    frames = sum(f for f, _ in samples)
+    core_s = sum(t for _, t in samples)
+    per_frame_core = core_s / frames            # single-core seconds per output frame
+    value = workers / per_frame_core            # frames/s on `workers` cores
+    clip_frames = sum(n for _, n in runs)
+    per_step = clip_frames * per_frame_core / workers
+    sample = (f"per step {workers} real runs of {a.config} (the reference's run list, cycled: mix "
+              f"{clip_frames} frames / {len(runs)} runs), each through the oracle port: energy + pushes of its "
+              f"first {k_e} frames, the carve of its representative frame, the literal replay (remove_batch "
+              f"per batch) of a frame; per-frame costs x run length; {workers} cores; the reference itself "
+              f"took {ref_wall:.0f} s for the clip on one core of the build host "
+              f"({clip_frames / ref_wall if ref_wall else 0:.3f} frames/s)")
     line = {
-        "metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8/f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": workload(a.config), "frames_per_step": workers * fpw,
-                   "sample": f"{workers} windows x {fpw} frames of the clip per step"},
+        "metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8/f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": workload(a.config), "frames_per_step": clip_frames,
+                   "sample": f"{workers} real runs per step, per-frame costs extrapolated to the run lengths",
+                   "single_core_s_per_frame": per_frame_core},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -466,11 +509,19 @@ def main():
 
     cpu = None
     if not a.no_cpu_baseline and world == 1:
-        n_cpu = 2
-        secs = cpu_sample(name, 1, n_cpu)
-        cpu = {"value": n_cpu / secs, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"first {n_cpu} frames of {name} through the oracle port (numpy restatement of "
-                         f"vidcarve.retarget_video, buffered, literal replay), {secs:.1f}s"}
+        # one core, the clip's real runs in order (the reference's run list) until ~20 s of work
+        runs, _, ref_wall = _golden_runs(name)
+        fr_done, core_s, k, t_start = 0, 0.0, 0, time.perf_counter()
+        while time.perf_counter() - t_start < 20.0 and k < len(runs):
+            n_, t_ = _oracle_run((name, runs[k][0], runs[k][1], 2))
+            fr_done += n_
+            core_s += t_
+            k += 1
+        cpu = {"value": fr_done / core_s, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"the first {k} real runs of {name} ({fr_done} frames) through the oracle port on one "
+                         f"core: energy + pushes, carve, literal replay (per-frame costs x run length); the "
+                         f"reference itself: {ref_wall:.0f} s for the {sum(n for _, n in runs)}-frame clip on one "
+                         f"build-host core"}
 
     line = {
         "metric": metric_for(name), "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
