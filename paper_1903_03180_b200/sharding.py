@@ -22,6 +22,8 @@ collective at all).  There is no collective on the compute path.
 
 from __future__ import annotations
 
+import os
+
 RUN_COST0 = 1000.0  # a run's carve, in frames of replay
 
 
@@ -112,6 +114,62 @@ def retarget_clip_sharded(clip, config, group=None, out=None, scan_once=False, g
         dist.all_reduce(dp, group=group)
         m.dp_passes = int(dp.item())
     return res, m
+
+
+def shared_host_buffer(name: str, shape, pin: bool = True):
+    """A host uint8 buffer every process of the node maps (/dev/shm/<name>): the ranks of a split
+    clip write their runs' output frames straight into it (their D2H copies land there), so the
+    outputs are gathered on the host with no collective.  Pinned (cudaHostRegister) when CUDA is
+    up, so the copies run asynchronously.  The creator (rank 0) sizes it; the others attach."""
+    import math
+    import torch
+    nbytes = int(math.prod(shape))
+    path = os.path.join("/dev/shm", name)
+    t = torch.from_file(path, shared=True, size=nbytes, dtype=torch.uint8).view(*shape)
+    if pin and torch.cuda.is_available():
+        rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), nbytes, 0)
+        if int(rc) != 0:
+            raise RuntimeError(f"cudaHostRegister failed ({int(rc)}) for the shared output buffer")
+    return t
+
+
+def release_host_buffer(t, name: str) -> None:
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
+    try:
+        os.unlink(os.path.join("/dev/shm", name))
+    except FileNotFoundError:
+        pass
+
+
+def retarget_clip_sharded_host(clip, config, out, group=None):
+    """One HOST clip split across the ranks of `group`, outputs gathered on the host: rank 0 scans
+    (scan_runs), the run list goes to every rank, runs are dealt longest-processing-time first,
+    and every rank's host-buffer call (chunked H2D, per-run D2H) writes its runs' frames into
+    `out` -- a shared_host_buffer all ranks map.  After the barrier every rank sees the whole
+    output.  Returns RunMetrics with dp_passes summed over the ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from .pipeline import RunMetrics, _run_device, _targets, scan_runs
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    tw, th = _targets(clip, config)
+    if config.mode == "buffered":
+        runs = scan_runs(clip, config) if rank == 0 else None
+        runs = broadcast_runs(runs, group) if world > 1 else runs
+        owners = lpt_owners(runs, world)
+        mine = [r for r, o in zip(runs, owners) if o == rank]
+        _, dp, _, _ = _run_device(clip.contiguous(), config, tw, th, out=out, runs_in=mine)
+    else:  # scpl / raw: a contiguous block of frames per rank
+        _, dp, runs, _ = _run_device(clip.contiguous(), config, tw, th, out=out, shard=(rank, world))
+    if world > 1:
+        t = torch.tensor([dp], dtype=torch.int64)
+        dist.all_reduce(t, group=group)
+        dp = int(t.item())
+        dist.barrier(group=group)
+    return out, RunMetrics(dp_passes=dp, frames_out=clip.shape[0], runs=runs)
 
 
 def shard_clips(n_clips: int, rank: int, world: int) -> list[int]:

@@ -346,3 +346,40 @@ def test_two_devices_one_process(P):
         assert o.device.index == d and m.dp_passes == g["dp_passes"]
         o = o.cpu().numpy()
         assert [sha(o[t]) for t in range(o.shape[0])] == g["frames_sha"]
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_host_split_into_shared_buffer(P, world):
+    """One HOST clip split by runs, outputs gathered on the host (sharding.py): each rank's
+    host-buffer call carves its LPT share of the runs (scanned once) and its per-run D2H copies
+    land in one shared, pinned /dev/shm buffer.  The ranks run one after another here (they never
+    wait on each other); the merged buffer is the reference's clip."""
+    import uuid
+    import torch
+    from paper_1903_03180_b200 import sharding
+    from paper_1903_03180_b200.pipeline import _run_device
+    from paper_1903_03180_b200.synth import config_clip
+    g = json.load(open(_c4_goldens()[1]))
+    clip, tw, th = config_clip("C4", clip=g["clip"])
+    host = torch.from_numpy(clip).pin_memory()
+    cfg = P.RetargetConfig(target_width=tw, mode="buffered")
+    name = f"scpl_gpu_test_{uuid.uuid4().hex[:8]}"
+    out = sharding.shared_host_buffer(name, (clip.shape[0],) + tuple(g["out_shape"]))
+    try:
+        if world == 1:
+            res, m = sharding.retarget_clip_sharded_host(host, cfg, out)
+            assert m.dp_passes == g["dp_passes"] and [list(r) for r in m.runs] == g["runs"]
+        else:
+            runs = P.scan_runs(host, cfg)
+            owners = sharding.lpt_owners(runs, world)
+            dp = 0
+            for rank in range(world):
+                mine = [r for r, o in zip(runs, owners) if o == rank]
+                _, d, _, _ = _run_device(host, cfg, tw, clip.shape[1], out=out, runs_in=mine)
+                dp += d
+            assert dp == g["dp_passes"]
+        o = out.numpy()
+        bad = [t for t in range(o.shape[0]) if sha(o[t]) != g["frames_sha"][t]]
+        assert not bad, f"{len(bad)} frames differ"
+    finally:
+        sharding.release_host_buffer(out, name)

@@ -189,3 +189,46 @@ def test_c4_clip_sharding(world):
     assert res[0][2] == 64 // world + 0.5 * (world - 1)       # max over ranks
     d = [x for r in range(world) for x in res[r][1]]
     assert len(set(d)) == len(d)                             # different seeds, different clips
+
+
+def _shared_buf_worker(rank, world, port, name, out):
+    """Host gather through one shared buffer (sharding.shared_host_buffer): every rank writes its
+    runs' frames (LPT owners) straight into the mapping, and after a barrier every rank reads the
+    whole clip -- no collective carries frames."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    from paper_1903_03180_b200 import sharding
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    runs = [(0, 7), (7, 3), (10, 12), (22, 2), (24, 9)]
+    owners = sharding.lpt_owners(runs, world)
+    buf = sharding.shared_host_buffer(name, (33, 4, 5, 3), pin=False)
+    for (s, n), o in zip(runs, owners):
+        if o == rank:
+            buf[s:s + n] = torch.arange(s, s + n, dtype=torch.uint8)[:, None, None, None] + 100
+    dist.barrier()
+    out[rank] = buf[:, 0, 0, 0].tolist()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shared_host_buffer_gather(world):
+    import uuid
+    from paper_1903_03180_b200 import sharding
+    name = f"scpl_test_{uuid.uuid4().hex[:8]}"
+    port = _free_port()
+    try:
+        with mp.Manager() as mgr:
+            out = mgr.dict()
+            mp.spawn(_shared_buf_worker, args=(world, port, name, out), nprocs=world, join=True)
+            res = dict(out)
+    finally:
+        try:
+            os.unlink(os.path.join("/dev/shm", name))
+        except FileNotFoundError:
+            pass
+    for r in range(world):
+        assert res[r] == [100 + t for t in range(33)]
+    assert sharding is not None
