@@ -214,8 +214,10 @@ __global__ void __launch_bounds__(kCodesThreads, 4) codes_kernel(const __grid_co
   using G = RawGeo<C>;
   extern __shared__ __align__(128) uint8_t smem[];
   auto raw = [&](uint32_t s) { return smem + (s & 1u) * G::kSlot; };
-  uint8_t* lum = smem + 2 * G::kSlot;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(lum + kCRows * kLumStride);
+  // two luma buffers: frame q's luma pass writes one while frame q-1's tile pass may still read
+  // the other, so one block barrier per frame suffices
+  auto lum = [&](uint32_t s) { return smem + 2 * G::kSlot + (s & 1u) * (kCRows * kLumStride); };
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * G::kSlot + 2 * kCRows * kLumStride);
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -261,21 +263,23 @@ __global__ void __launch_bounds__(kCodesThreads, 4) codes_kernel(const __grid_co
     };
     auto tma_slot = [&](int q) { return use_tma && !(q == 0 && !prev_in_clip); };
     uint32_t prev[4] = {0, 0, 0, 0};
+    // One barrier per frame (B_q, after the luma pass): the raw slot of frame q+1 was last read by
+    // frame q-1's luma pass and the luma buffer of frame q by frame q-2's tile pass, both before
+    // B_{q-1}; a plain (cooperative) fill of frame q+1 is made visible by B_q.
     fill(q0, seq);
+    if (!tma_slot(q0)) __syncthreads();
     for (int q = q0; q <= q1; ++q, ++seq) {
-      if (q + 1 <= q1) fill(q + 1, seq + 1);  // the slot was released by the sync ending frame q-1
+      if (q + 1 <= q1) fill(q + 1, seq + 1);
       if (tma_slot(q)) {
         mbar_wait(&bar[seq & 1], (phase >> (seq & 1)) & 1u);
         phase ^= 1u << (seq & 1);
       }
-      __syncthreads();  // plain fills visible
-      codes_luma<C>(smem_u32(raw(seq)), src_lane + (seq & 1u) * G::kSlot, smem_u32(lum), r0, c0, H, W);
-      __syncthreads();
+      codes_luma<C>(smem_u32(raw(seq)), src_lane + (seq & 1u) * G::kSlot, smem_u32(lum(seq)), r0, c0, H, W);
+      __syncthreads();  // B_q
       const int t = tb + q - 1;
-      codes_tile(smem_u32(lum), prev, q >= 1, q > 1 || have_prev0, r0, c0, H, W,
+      codes_tile(smem_u32(lum(seq)), prev, q >= 1, q > 1 || have_prev0, r0, c0, H, W,
                  codes + (size_t)t * fpx + (size_t)(r0 + 4 * (threadIdx.x >> 5)) * W + c0 + 4 * (threadIdx.x & 31),
                  vec_out);
-      __syncthreads();  // lum and raw(seq) free
     }
   }
 }
@@ -310,7 +314,7 @@ static void launch_codes_c(const uint8_t* frames, const uint8_t* prev_frame, int
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     SCPL_ARG(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed for the clip");
   }
-  const size_t smem = 2 * (size_t)G::kSlot + (size_t)kCRows * kLumStride + 16;
+  const size_t smem = 2 * (size_t)G::kSlot + 2 * (size_t)kCRows * kLumStride + 16;
   const int tiles_x = cdiv(W, kCW), tiles = tiles_x * cdiv(H, kCH);
   const long units = (long)tiles * n;
   static std::atomic<int> per_sm_cache{0};  // resident CTAs per SM (same on every B200)

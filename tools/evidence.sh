@@ -1,0 +1,25 @@
+#!/bin/bash
+# Round evidence on one B200 (outputs in gpurun_out/, summarised into profiles/ by hand):
+# benches, every config, launch lists and full ncu captures of the main kernels.
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+R=${ROUND:-r2}
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/${R}_bench_C2.log 2>&1
+timeout 900 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${R}_bench_C4.log 2>&1
+timeout 1200 bash tools/probe/all_configs.sh > gpurun_out/${R}_configs.txt 2>&1
+# the driver-style launch list of the bench command itself (graph loops: pass / row kernels inside
+# conditional graphs do not appear), then the host-loop variant that shows every kernel
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/${R}_launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
+  > gpurun_out/${R}_ncu_bench.log 2>&1
+SCPL_HOST_LOOPS=1 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${R}_launches_C2_hostloops.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e \
+  > gpurun_out/${R}_ncu_hl.log 2>&1
+SCPL_HOST_LOOPS=1 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${R}_launches_C4x8_hostloops.csv python tools/probe/c4_batch.py --child --clips 8 --steps 1 --warmup 0 \
+  > gpurun_out/${R}_ncu_c4.log 2>&1
+for k in carve_pass_kernel carve_compact_kernel carve_dirty_kernel codes_kernel window_stats_scan replay_rows_vec uniform_vec; do
+  SCPL_HOST_LOOPS=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -s 12 -c 1 \
+    -o gpurun_out/${R}_full_$k python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/${R}_full_$k.log 2>&1
+done
+echo done > gpurun_out/${R}_evidence.done
