@@ -315,6 +315,7 @@ struct CarveSet {
   int max_fr = 1;           // most frames carved together by one run (reaverage)
   bool reaverage = false;
   bool has_uniform = false;  // U holds a uniform map for the first pass (else the mean gradient)
+  bool bucket = false;       // pad the run count to carve_bucket (batches: many group sizes)
   int kc = 6;                // DP window variant (scpl_carve2.cu: kc6 / kc4 / kc3)
   int kc_first = 6, cl_first = 1;  // variant + cluster of the fp64 first pass (uniform map)
   long long prof[4] = {0, 0, 0, 0};
@@ -329,7 +330,7 @@ struct CarveSet {
   CarveSet& operator=(const CarveSet&) = delete;
   ~CarveSet() {
     if (!loop.mem) return;
-    constexpr size_t kPoolCap = 64;
+    constexpr size_t kPoolCap = 256;
     ctx->loop_pool.emplace(loop_key, loop);
     ctx->loop_order.push_back(loop_key);
     while (ctx->loop_order.size() > kPoolCap) {
@@ -478,24 +479,36 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
   }
 }
 
+// run-count bucket of the pooled carve loops: the next power of two (multiples of 64 above)
+int carve_bucket(int nruns) {
+  if (nruns > 64) return (nruns + 63) / 64 * 64;
+  int b = 1;
+  while (b < nruns) b <<= 1;
+  return b;
+}
+
 // Carve every run of a set to its target, asynchronously on st: one graph launch runs the
 // iteration loop on the device (pass, compaction, gradient until every run is done), then
 // the index kernel; the final run states and the iteration count land in pinned memory
 // (h_state: nruns CarveRuns + 16 bytes; read by carve_finish once the stream is done).
 void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   const int nruns = (int)S.runs.size();
+  const bool graph = S.cols > S.target && !host_loops();
+  // graph loops are instantiated for a bucketed run count (padding runs are already "done", so
+  // every kernel skips them): the pooled graphs then serve any group size up to the bucket
+  // instead of instantiating a conditional graph (~1 ms of host time) per new group size
+  const int nb = graph && S.bucket ? carve_bucket(nruns) : nruns;
   CarveRun* h_runs = reinterpret_cast<CarveRun*>(h_state);
   S.h_runs = h_runs;
-  S.h_iters = reinterpret_cast<int*>(h_runs + nruns);
+  S.h_iters = reinterpret_cast<int*>(h_runs + nb);
   *S.h_iters = 0;
   if (nruns == 0) return;
   for (auto& R : S.runs) {
     R.cyc_dp = R.cyc_sel = 0;
     if (R.prof) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, kProfBytes, st));
   }
-  const bool graph = S.cols > S.target && !host_loops();
   S.ctx = ctx;
-  S.loop_key = {nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
+  S.loop_key = {nb, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
                 (int)S.reaverage + 2 * graph + 4 * S.kc + 64 * (int)S.has_uniform + 128 * S.kc_first +
                     2048 * S.cl_first};
   auto it = ctx->loop_pool.find(S.loop_key);
@@ -508,14 +521,15 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
         break;
       }
   } else {
-    SCPL_CUDA(cudaMalloc(&S.loop.mem, sizeof(CarveRun) * nruns + 16));
+    SCPL_CUDA(cudaMalloc(&S.loop.mem, sizeof(CarveRun) * nb + 16));
   }
   CarveRun* runs_d = reinterpret_cast<CarveRun*>(S.loop.mem);
-  int* iters_d = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(S.loop.mem) + sizeof(CarveRun) * nruns);
+  int* iters_d = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(S.loop.mem) + sizeof(CarveRun) * nb);
   std::memcpy(h_runs, S.runs.data(), sizeof(CarveRun) * nruns);
+  for (int r = nruns; r < nb; ++r) h_runs[r] = CarveRun{};  // padding: width == target == 0
   // run states and the zeroed loop counters (iterations, CTAs done) from mapped pinned memory
   S.h_iters[1] = 0;
-  kc6::launch_word_copy(runs_d, h_runs, sizeof(CarveRun) * nruns + 2 * sizeof(int), st);
+  kc6::launch_word_copy(runs_d, h_runs, sizeof(CarveRun) * nb + 2 * sizeof(int), st);
   if (S.reaverage && !S.has_uniform)  // first pass on the mean gradient too (pipeline.py:289-290)
     kc6::launch_carve_mean(runs_d, nruns, S.rows, st);
   if (S.cols > S.target && host_loops()) {  // bursts of 8 iterations, host checks the widths
@@ -537,12 +551,12 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   } else if (graph) {
     if (!S.loop.ex)
       S.loop.ex = SCPL_CARVE_FN(S.kc, build_carve_loop)(
-          runs_d, nruns, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage,
+          runs_d, nb, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage,
           S.has_uniform, SCPL_CARVE_FN(S.kc_first, launch_carve_iteration), S.cl_first);
     SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
   kc6::launch_carve_index(runs_d, nruns, S.rows, st);
-  kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns + sizeof(int), st);  // states + counter
+  kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nb + sizeof(int), st);  // states + counter
 }
 
 // after the stream is done: run states back into S.runs, launch accounting, profile
@@ -593,7 +607,7 @@ void carve_finish(CarveSet& S) {
 
 void carve_run_all(scpl_ctx* ctx, CarveSet& S, cudaStream_t st) {
   const int nruns = (int)S.runs.size();
-  uint8_t* pin = pinned_scratch(ctx, sizeof(CarveRun) * (size_t)std::max(nruns, 1) + 64);
+  uint8_t* pin = pinned_scratch(ctx, sizeof(CarveRun) * (size_t)carve_bucket(std::max(nruns, 1)) + 64);
   carve_launch(ctx, S, pin, st);
   SCPL_CUDA(cudaStreamSynchronize(st));
   carve_finish(S);
@@ -901,7 +915,7 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   // Clips in flight: a batch's clips take the lanes in turn (clip j on lane j % L), so the
   // scans of later clips queue behind earlier ones on their lane while the earlier clips' runs
   // carve -- scans and carves overlap instead of running as two phases.
-  int nlanes = njobs > 1 ? 12 : 1;
+  int nlanes = njobs > 1 ? 8 : 1;
   if (const char* e = getenv("SCPL_LANES")) nlanes = std::max(1, atoi(e));
   nlanes = std::min(nlanes, njobs);
   while ((int)ctx->lanes.size() < nlanes) {
@@ -953,14 +967,18 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       if (ax == 0 && tw < w) phases.push_back(0);
       if (ax == 1 && th < h) phases.push_back(1);
     }
-  const int chunk = 16;
+  // chunks of 16 frames: a host clip's copies overlap its codes and scan, and a single clip's
+  // runs reach the carve while its scan goes on; a batch of device clips is scanned clip by clip
+  // in one piece (other clips' runs keep the carve busy; a chunk costs host API calls per clip)
+  const int chunk = (njobs > 1 && !host_in) ? std::max(T, 1) : 16;
   const int nchunk = (T + chunk - 1) / chunk;
   if (buffered && !given) upload_phi(ctx, P);
 
   // pinned scratch: scan readbacks, then per group and phase the carve-run states
   const size_t scan_pin = 64 + ((sizeof(int) * (nchunk + 2 * (size_t)T) + 63) & ~(size_t)63) + sizeof(ScanState) + 64;
-  const size_t need =
-      njobs * scan_pin + (phases.size() + 1) * (size_t)T * njobs * (sizeof(CarveRun) + 64) + 4096 * (size_t)njobs;
+  // (carve states: at most twice the runs per phase with the bucket padding, + 64 B per group)
+  const size_t need = njobs * scan_pin + (2 * phases.size() + 1) * (size_t)T * njobs * (sizeof(CarveRun) + 64) +
+                      4096 * (size_t)njobs;
   uint8_t* pin = pinned_scratch(ctx, need);
   size_t pin_used = 0;
   auto pin_take = [&](size_t bytes) {
@@ -1033,31 +1051,39 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   cudaEvent_t ev_alloc = new_event(false);
   SCPL_CUDA(cudaEventRecord(ev_alloc, st));
 
-  // 1. frames in (host) and energy codes, chunk by chunk (each scan starts on its first chunk);
-  // clip by clip on the copy stream, so the first clips' scans start first
-  if (host_in) SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
-  for (auto& J : jobs) {
-    cudaStream_t sc = J.lane->s_codes;
-    SCPL_CUDA(cudaStreamWaitEvent(sc, ev_alloc, 0));
-    J.ev_chunk_codes.assign(nchunk, nullptr);
-    for (int c = 0; c < nchunk; ++c) {
-      const int t0 = c * chunk, n = std::min(chunk, T - t0);
-      if (host_in) {
+  // 1. frames in (host): every clip's chunks on the copy stream, clip by clip, so the first
+  // clips' scans start first
+  std::vector<std::vector<cudaEvent_t>> ev_h2d(njobs);
+  if (host_in) {
+    SCPL_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ev_alloc, 0));
+    for (auto& J : jobs)
+      for (int c = 0; c < nchunk; ++c) {
+        const int t0 = c * chunk, n = std::min(chunk, T - t0);
         SCPL_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(J.frames) + fbytes0 * t0, J.frames_host + fbytes0 * t0,
                                   fbytes0 * n, cudaMemcpyHostToDevice, ctx->s_h2d));
         if (njobs == 1) mark("h2d " + std::to_string(c), ctx->s_h2d);
         cudaEvent_t e = new_event(false);
         SCPL_CUDA(cudaEventRecord(e, ctx->s_h2d));
-        SCPL_CUDA(cudaStreamWaitEvent(sc, e, 0));
+        ev_h2d[J.index].push_back(e);
       }
+  }
+  // 2. per clip, on its lane: energy codes chunk by chunk, then the buffer scan chunk by chunk
+  // (each scan chunk waits for its codes; fixed one-frame runs for scpl / raw; given runs: no
+  // scan).  A lane's scans run one clip after another (its scan state is reset in stream order).
+  // A batch's clips are started lazily (at most two per lane ahead of the harvested ones): the
+  // host's API calls for later clips then overlap the GPU work instead of delaying the first
+  // dispatch.
+  auto start_job = [&](ClipJob& J) {
+    cudaStream_t sc = J.lane->s_codes;
+    SCPL_CUDA(cudaStreamWaitEvent(sc, ev_alloc, 0));
+    J.ev_chunk_codes.assign(nchunk, nullptr);
+    for (int c = 0; c < nchunk; ++c) {
+      const int t0 = c * chunk, n = std::min(chunk, T - t0);
+      if (host_in) SCPL_CUDA(cudaStreamWaitEvent(sc, ev_h2d[J.index][c], 0));
       if (P.mode != 0) launch_codes(J.frames, nullptr, t0, n, h, w, C, J.codes.as<uint16_t>(), ctx->num_sms, sc);
       J.ev_chunk_codes[c] = new_event(false);
       SCPL_CUDA(cudaEventRecord(J.ev_chunk_codes[c], sc));
     }
-  }
-  // 2. buffer scans, chunk by chunk (fixed one-frame runs for scpl / raw; given runs: none);
-  // a lane's scans run one clip after another (its scan state is reset in stream order)
-  for (auto& J : jobs) {
     cudaStream_t ss = J.lane->s_scan;
     J.ev_codes = new_event(true);
     J.ev_scan = new_event(true);
@@ -1079,7 +1105,11 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       SCPL_CUDA(cudaStreamWaitEvent(ss, J.ev_chunk_codes[nchunk - 1], 0));
     }
     SCPL_CUDA(cudaEventRecord(J.ev_scan, ss));
-  }
+  };
+  const bool polled = buffered && !given && !scan_only;
+  const int ahead = 2 * nlanes;
+  int started = 0;
+  for (; started < njobs && (!polled || started < ahead); ++started) start_job(jobs[started]);
 
   // 3. carve + replay, one run group at a time as runs close
   const long total_frames = (long)T * njobs;
@@ -1166,7 +1196,10 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
       }
       mark("group " + std::to_string(gi) + " setup done", gs);
       hmark("group carve_launch");
-      carve_launch(ctx, S, pin_take(sizeof(CarveRun) * nr + 16), gs);
+      // (a batch's groups come in many sizes: their pooled graphs are shared per bucket; the
+      // padding clusters cost a single clip's few group sizes more than they save)
+      S.bucket = njobs > 1;
+      carve_launch(ctx, S, pin_take(sizeof(CarveRun) * (S.bucket ? carve_bucket(nr) : nr) + 16), gs);
       hmark("group replay");
       mark("group " + std::to_string(gi) + " carve done", gs);
       const int nH = height ? th : curH, nW = height ? curW : tw;
@@ -1227,12 +1260,13 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
     if (const char* e = getenv("SCPL_GROUP_MAX")) max_group = std::max(1, atoi(e));
     // event-driven: harvest every clip's chunks as they complete (any order), dispatch groups
     std::vector<int> next(njobs, 0);
-    int remaining = njobs * nchunk;
+    int remaining = njobs * nchunk, harvested_jobs = 0;
     std::vector<RunRef> pending;
     std::vector<cudaEvent_t> ready;
     while (remaining > 0) {
       bool progress = false;
-      for (auto& J : jobs) {
+      for (int ji = 0; ji < started; ++ji) {
+        ClipJob& J = jobs[ji];
         while (next[J.index] < nchunk) {
           const int c = next[J.index];
           const cudaError_t q = cudaEventQuery(J.ev_chunk[c]);
@@ -1244,6 +1278,7 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
           ++next[J.index];
           --remaining;
           progress = true;
+          if (next[J.index] == nchunk) ++harvested_jobs;
           if (shards > 1) {  // this rank's runs (a single clip), each as it closes
             for (int r = J.done; r < (int)J.runs.size(); ++r)
               if (mine(J.runs[r])) dispatch({{&J, r}}, {J.ev_chunk[c]}, host_in && remaining == 0);
@@ -1282,6 +1317,7 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
         const bool last = remaining == 0 && pending.empty() && njobs == 1;
         dispatch(grp, ev, last && (host_in || last_wide));
       }
+      while (started < njobs && started < harvested_jobs + ahead) start_job(jobs[started++]);
       if (!progress && remaining > 0) std::this_thread::yield();
     }
   } else {
