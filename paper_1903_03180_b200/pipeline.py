@@ -11,6 +11,7 @@ the result is then a CUDA tensor (T, H', W'[, C]) and nothing touches the host.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Iterable
@@ -344,11 +345,20 @@ def _stack_pinned(arrs):
     h, w = arrs[0].shape[:2]
     host = torch.empty((T, h, w, C), dtype=torch.uint8, pin_memory=True)
     hv = host.numpy()
-    for t, a in enumerate(arrs):
-        a8 = _as_u8_frame(a, t)
+
+    def put(t):
+        a8 = _as_u8_frame(arrs[t], t)
         if a8.ndim == 2:
             a8 = a8[:, :, None]
         hv[t] = a8  # (broadcasts a gray frame over three channels when mixed)
+
+    if T * h * w * C >= (64 << 20):  # large clips: the host copy in parallel (numpy releases the GIL)
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+            list(ex.map(put, range(T)))
+    else:
+        for t in range(T):
+            put(t)
     return host
 
 
