@@ -318,6 +318,7 @@ struct CarveSet {
   bool bucket = false;       // pad the run count to carve_bucket (batches: many group sizes)
   int kc = 6;                // DP window variant (scpl_carve2.cu: kc6 / kc4 / kc3)
   int kc_first = 6, cl_first = 1;  // variant + cluster of the fp64 first pass (uniform map)
+  bool fused = false;        // fused int passes (no compaction / gradient kernels)
   long long prof[4] = {0, 0, 0, 0};
   scpl_ctx* ctx = nullptr;
   std::array<int, 8> loop_key{};
@@ -432,6 +433,10 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     }
   }
   S.runs.assign(nruns, CarveRun{});
+  // fused int passes (one frame per run): the pass kernel removes the previous batch and computes
+  // the energy itself; the gradient plane's memory becomes the second luma plane
+  S.fused = !reaverage && max_fr == 1 && rows >= 2 && SCPL_CARVE_FN(kc, carve_fused_ok)(cols, target, cl);
+  const int ring_w = S.fused ? SCPL_CARVE_FN(kc, carve_fused_ring_w)(cols, target, cl) : 0;
   uint8_t* base = S.mem.as<uint8_t>();
   size_t plane_off = 0;
   const int stage = SCPL_CARVE_FN(kc, carve_stage_dtab)(rows, pitch, cl) ? 1 : 0;
@@ -454,6 +459,11 @@ void carve_alloc(CarveSet& S, int nruns, int rows, int cols, int target, int kma
     R.fstride = (long long)plane_al;
     R.luma[0] = R.luma[1] = base + plane_off;
     R.grad[0] = R.grad[1] = base + plane_off + (size_t)R.nfr * plane_al;
+    R.fused = S.fused ? 1 : 0;
+    R.ring_w = ring_w;
+    R.lsel = 0;
+    R.fdbg = getenv("SCPL_FDBG") ? atoi(getenv("SCPL_FDBG")) : 0;
+    if (S.fused) R.luma[1] = R.grad[0];
     plane_off += (size_t)R.nfr * 2 * plane_al;
     R.width = cols;
     R.idx = reinterpret_cast<int16_t*>(take(plane * 2));
@@ -510,7 +520,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   S.ctx = ctx;
   S.loop_key = {nb, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
                 (int)S.reaverage + 2 * graph + 4 * S.kc + 64 * (int)S.has_uniform + 128 * S.kc_first +
-                    2048 * S.cl_first};
+                    2048 * S.cl_first + 65536 * (int)S.fused};
   auto it = ctx->loop_pool.find(S.loop_key);
   if (it != ctx->loop_pool.end()) {
     S.loop = it->second;
@@ -539,7 +549,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
         const bool first = done_iters + k == 0 && S.has_uniform && !S.reaverage;
         SCPL_CARVE_FN(first ? S.kc_first : S.kc, launch_carve_iteration)(
             runs_d, nruns, S.rows, S.pitch, S.cols, first ? S.cl_first : S.cl, st, S.max_fr, S.reaverage, first,
-            nullptr);
+            nullptr, S.fused);
       }
       done_iters += 8;
       kc6::launch_word_copy(h_runs, runs_d, sizeof(CarveRun) * nruns, st);
@@ -552,7 +562,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
     if (!S.loop.ex)
       S.loop.ex = SCPL_CARVE_FN(S.kc, build_carve_loop)(
           runs_d, nb, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage,
-          S.has_uniform, SCPL_CARVE_FN(S.kc_first, launch_carve_iteration), S.cl_first);
+          S.has_uniform, SCPL_CARVE_FN(S.kc_first, launch_carve_iteration), S.cl_first, S.fused);
     SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
   kc6::launch_carve_index(runs_d, nruns, S.rows, st);
@@ -564,12 +574,13 @@ void carve_finish(CarveSet& S) {
   const int nruns = (int)S.runs.size();
   if (nruns == 0) return;
   std::memcpy(S.runs.data(), S.h_runs, sizeof(CarveRun) * nruns);
-  g_launches.fetch_add((long)kc6::carve_kernels_per_iteration(S.reaverage) * *S.h_iters, std::memory_order_relaxed);
+  g_launches.fetch_add((long)(S.fused ? 2 : kc6::carve_kernels_per_iteration(S.reaverage)) * *S.h_iters,
+                       std::memory_order_relaxed);
   for (auto& R : S.runs)
     if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;
   for (auto& R : S.runs) {
-    long long c[17] = {};
+    long long c[31] = {};
     if (R.prof) {
       SCPL_CUDA(cudaMemcpy(c, R.prof, sizeof(c), cudaMemcpyDeviceToHost));
       c[0] = R.cyc_dp;
@@ -580,6 +591,11 @@ void carve_finish(CarveSet& S) {
               " trace %lld (x CTAs)\n",
               R.iters, R.rows, c[0], c[1], c[4], c[5], c[6], c[7], c[8], c[9], c[10], c[11], c[12], c[13], c[14],
               c[15], c[16]);
+      if (R.fused)
+        fprintf(stderr,
+                "carve prod (rank 0 thread 0, cycles): stagewait %lld issue %lld A0 %lld A1 %lld A2 %lld empty %lld"
+                " B %lld full %lld svc %lld | dp ringwait %lld | A1 setup %lld words %lld edge %lld own %lld\n",
+                c[17], c[18], c[19], c[20], c[21], c[22], c[23], c[24], c[25], c[26], c[27], c[28], c[29], c[30]);
       // pass timestamps (globaltimer ns at entry / exit of each pass): time inside passes vs gaps
       const int n = std::min(R.iters, (int)(kProfBytes / 16) - 16);
       std::vector<long long> ts(2 * (size_t)n);

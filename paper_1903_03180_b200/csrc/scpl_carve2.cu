@@ -426,22 +426,410 @@ __device__ __forceinline__ void store_block_end(const CarveRun& R, const Geo& g,
 // staging buffer and moves on).  hbar: full[2] (32 DP-lane arrivals), empty[2] (32 helper-
 // lane arrivals); a header of ~0 ends the pass.
 template <bool F64>
+__device__ __forceinline__ bool pw_service(const CarveRun& R, const Geo& g, const uint32_t* stage, uint64_t* hbar,
+                                           uint32_t& n) {
+  mbar_wait_sleep(&hbar[n & 1], (n >> 1) & 1);
+  const uint32_t* stg = stage + (n & 1) * kPwStageWords;
+  const uint32_t hdr = stg[3 * kWin];
+  if (hdr == 0xffffffffu) return false;
+  store_block_end<F64>(R, g, stg, (int)hdr, (int)stg[3 * kWin + 1]);
+  mbar_arrive(&hbar[2 + (n & 1)]);
+  ++n;
+  return true;
+}
+template <bool F64>
 __device__ void pw_helper(const CarveRun& R, const Geo& g, const uint32_t* stage, uint64_t* hbar) {
-  for (uint32_t n = 0;; ++n) {
-    mbar_wait(&hbar[n & 1], (n >> 1) & 1);
-    const uint32_t* stg = stage + (n & 1) * kPwStageWords;
-    const uint32_t hdr = stg[3 * kWin];
-    if (hdr == 0xffffffffu) break;
-    store_block_end<F64>(R, g, stg, (int)hdr, (int)stg[3 * kWin + 1]);
-    mbar_arrive(&hbar[2 + (n & 1)]);
+  uint32_t n = 0;
+  while (pw_service<F64>(R, g, stage, hbar, n)) {
   }
 }
+
+// ------------------------------------------------------------------ fused producer (int passes)
+// default_energy (batching.py:110-115) of the carved frame without compaction / gradient
+// kernels: while the DP warps work on block k, the producer warps build block k+1's energy rows
+// for this CTA's windows.  Per row: the previous batch (remove_batch, batching.py:76-107) is
+// removed from the source luma plane row (only the columns the CTA's windows need, +-1), the
+// compacted row goes to a luma ring in shared memory (and the CTA's own columns to the other
+// luma plane, for the next pass), then the Sobel energy (energy.py:40-59, edge replication)
+// of the ring rows goes into the DP's energy ring.  Luma of a pixel commutes with compaction,
+// so this is default_energy of the carved RGB frame.
+// The fused pass kernel has kFusedWarps warps: warpgroup 0 = the DP warps (setmaxnreg: 128
+// registers), warpgroups 1-2 = kProdWarps producer warps (56 registers); producer q < 4 also
+// stores DP warp q's block ends (helper duty).  Launch allocation: 80 registers per thread.
+constexpr int kFusedWarps = 12;
+constexpr int kProdWarps = 8;
+constexpr int kProdFirst = 4;   // first producer warp
+constexpr int kRegDp = 128, kRegProd = 56, kRegFused = 80;
+constexpr int kLumRing = 34;    // luma ring rows: block k's Sobel needs rows 32k .. 32k+33
+constexpr int kProdBar = 3;     // named barrier of the producer warps
+// Every input of a producer (the source luma rows, the previous batch's removed columns) exists
+// when the pass starts, so the producers stage block k+1's inputs with cp.async while they
+// work on block k: per compaction row the source columns the CTA needs (a superset fixed per
+// pass: the new columns [d0, d1) come from [d0, d1 + b)) and the row's removed-column list.
+// Batches larger than kProdBcap read global memory directly (slower, same results).
+constexpr int kProdBcap = 64;
+constexpr int kStageRows = 34;  // compaction rows per block (block 0: rows 0 .. 33)
+__host__ __device__ inline int fused_stage_sw(int rw) { return (rw + 48 + kProdBcap + 15) & ~15; }
+__host__ __device__ inline int fused_stage_slot(int rw) { return fused_stage_sw(rw) + 2 * kProdBcap + 32; }
+
+struct ProdGeo {
+  int g_lo;   // image column of energy-ring column 0 (16-aligned, may be negative)
+  int rw;     // energy-ring row stride; luma-ring row stride rw + 32 (column c <-> image c + g_lo - 16)
+  int cta_lo, cta_hi;
+};
+
+// the CTA's energy columns [g_lo, g_hi) at width w: the union of its active DP warps' windows
+__host__ __device__ inline bool fused_cta_range(int w, int CL, int rank, int& g_lo, int& g_hi) {
+  const int per = ((w + CL - 1) / CL + 15) & ~15;
+  const int cta_lo = w < rank * per ? w : rank * per;
+  const int cta_hi = w < cta_lo + per ? w : cta_lo + per;
+  bool any = false;
+  for (int dw = 0; dw < kMaxWarps; ++dw) {
+    const int own_lo = cta_lo + dw * kOwn;
+    const int own_hi = cta_hi < own_lo + kOwn ? cta_hi : own_lo + kOwn;
+    if (own_lo >= own_hi) break;
+    int wl = own_lo - kXRows;
+    if (w >= kWin) wl = wl < 0 ? 0 : (wl > w - kWin ? w - kWin : wl);
+    const int lo = wl & ~15, hi = wl + kWin;
+    if (!any || lo < g_lo) g_lo = lo;
+    if (!any || hi > g_hi) g_hi = hi;
+    any = true;
+  }
+  return any;
+}
+
+// DP-phase shared memory of a fused int pass: exchange rows (2 x 4 B x pitch), the helper
+// staging of kProdWarps DP warps, the energy ring (1 + 2 x 32 rows of rw), the luma ring
+// (kLumRing rows of rw + 32), the per-row breakpoint table, two blocks of staged inputs
+__host__ __device__ inline size_t fused_off_stage(int pitch) { return 8 * (size_t)pitch; }
+__host__ __device__ inline size_t fused_off_ering(int pitch) {
+  return fused_off_stage(pitch) + (size_t)kDpWarps * 2 * kPwStageWords * 4;
+}
+__host__ __device__ inline size_t fused_off_lring(int pitch, int rw) {
+  return fused_off_ering(pitch) + (size_t)(1 + 2 * kXRows) * rw;
+}
+__host__ __device__ inline size_t fused_off_rowtab(int pitch, int rw) {
+  return fused_off_lring(pitch, rw) + (size_t)kLumRing * (rw + 32);
+}
+__host__ __device__ inline size_t fused_off_pstage(int pitch, int rw) {
+  return fused_off_rowtab(pitch, rw) + ((kStageRows * 8 + 15) & ~15);
+}
+__host__ __device__ inline size_t fused_dp_bytes(int pitch, int rw) {
+  return fused_off_pstage(pitch, rw) + (size_t)2 * kStageRows * fused_stage_slot(rw);
+}
+
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds32p(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// (no "memory" clobber: the producers' shared-memory phases are ordered by prod_bar, whose asm
+// is a compiler barrier; a clobber here would force every CarveRun field to be re-read)
+__device__ __forceinline__ uint32_t lds16p(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32p(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void prod_bar() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kProdBar), "n"(kProdWarps * 32) : "memory");
+}
+
+// One luma row's horizontal Sobel terms around 4 columns (even / odd columns in 16-bit lanes):
+// S = l + 2m + r and D = r - l + 256, from the luma-ring words at a - 4, a, a + 4.
+__device__ __forceinline__ void sobel_prep(uint32_t a, uint32_t& se, uint32_t& so, uint32_t& de, uint32_t& dO) {
+  const uint32_t lo = lds32p(a - 4), mid = lds32p(a), hi = lds32p(a + 4);
+  const uint32_t wl = __byte_perm(lo, mid, 0x6543);  // columns -1 .. 2
+  const uint32_t wr = __byte_perm(mid, hi, 0x4321);  // columns 1 .. 4
+  const uint32_t le = __byte_perm(wl, 0, 0x4240), lo_ = __byte_perm(wl, 0, 0x4341);
+  const uint32_t me = __byte_perm(mid, 0, 0x4240), mo = __byte_perm(mid, 0, 0x4341);
+  const uint32_t re = __byte_perm(wr, 0, 0x4240), ro = __byte_perm(wr, 0, 0x4341);
+  se = le + 2u * me + re;
+  so = lo_ + 2u * mo + ro;
+  de = re + 0x01000100u - le;
+  dO = ro + 0x01000100u - lo_;
+}
+
+// The producer warps of a fused int pass (tp = 0 .. 255 over kProdWarps warps).  Per block k
+// (DP rows 1+32k .. 32k+32), all producer threads share every phase:
+//   wait for block k's staged inputs, stage block k+1 (cp.async: the source columns the CTA
+//   needs, [d0, d1 + b), and the removed-column lists of compaction rows a0(k) .. a1(k));
+//   A1 warp per row: the previous batch's breakpoints a_t = rr[t] - t below / inside [d0, d1)
+//      by ballots, then lane per 4-column word: source shift s(y) = #{a_t <= y}, one funnel
+//      shift of two staged words (byte-wise where s changes inside the word) into the luma ring;
+//   A2 edge replication (np.pad "edge"), the CTA's own columns to the next plane;
+//   wait until the DP is done with the slot's previous block; B Sobel (8-row streams, lane per
+//   4-column word) from the luma ring into the energy ring; full[slot]; helper duty.
+// Compaction rows: block 0 rows 0 .. 33, block k rows 32k+2 .. 32k+33 (block k's Sobel needs
+// luma rows 32k .. 32k+33; the luma ring holds kLumRing = 34 rows).
+__device__ void produce_pass(const CarveRun& R, int w, int b, int off, const ProdGeo& P, uint8_t* ering,
+                             uint8_t* lring, uint8_t* pstage, uint64_t* full, uint64_t* empty, int tp, bool helper,
+                             const Geo& hg, const uint32_t* hstage, uint64_t* hbar, bool active_cta,
+                             long long* prof) {
+  constexpr int NT = kProdWarps * 32;
+  // (SCPL_PROF: producer thread 0 of rank 0 times its phases into prof[17..25])
+  long long pt = prof ? clock64() : 0;
+  auto ph = [&](int i) {
+    if (prof) {
+      const long long u = clock64();
+      prof[17 + i] += u - pt;
+      pt = u;
+    }
+  };
+  // every CarveRun field in registers (the cp.async / barrier asm are compiler barriers)
+  const int rows = R.rows, pitch = R.pitch, rw = P.rw, lw = P.rw + 32, lo = P.g_lo - 16;
+  const int g_lo = P.g_lo, cta_lo = P.cta_lo, cta_hi = P.cta_hi;
+  const int16_t* const rem = R.rem;
+  const long rem_cap = R.rem_cap;
+  const uint8_t* src = R.luma[R.lsel];
+  uint8_t* dst = R.luma[R.lsel ^ 1];
+  const int nstage = active_cta ? (rows - 1 + kXRows - 1) / kXRows : 0;
+  const int d0 = max(g_lo - 1, 0), d1 = min(g_lo + rw + 1, w);
+  const int y0 = d0 & ~3;
+  const bool staged = b <= kProdBcap;
+  const int X0 = d0 & ~15, X1 = min((d1 + b + 15) & ~15, pitch);
+  const int nch = (X1 - X0) >> 4;                 // staged 16-byte source chunks per row
+  const int ncr = b > 0 ? (b + 14) / 8 + 1 : 0;   // staged 16-byte removed-list chunks per row
+  const int per_row = nch + ncr;
+  const int sw = fused_stage_sw(rw), slot = fused_stage_slot(rw);
+  const bool tiny = rows < 3 || w < 3;  // zero energy below the 3x3 Sobel domain
+  const int lane = tp & 31, pw = tp >> 5;  // producer warp 0 .. kProdWarps-1
+  const int fdbg = R.fdbg;
+  auto a0f = [&](int k) { return k == 0 ? 0 : kXRows * k + 2; };
+  auto a1f = [&](int k) { return min(kXRows * k + 34, rows); };
+  auto erow = [&](int r) -> uint8_t* {
+    return ering + (size_t)(r == 0 ? 0 : 1 + kXRows * (((r - 1) / kXRows) & 1) + (r - 1) % kXRows) * rw;
+  };
+  auto stage_block = [&](int k) {
+    if (staged && k < nstage) {
+      uint8_t* buf = pstage + (size_t)(k & 1) * kStageRows * slot;
+      const int r0 = a0f(k), nr = a1f(k) - r0;
+      for (int p = tp; p < nr * per_row; p += NT) {
+        const int j = p / per_row, c = p - j * per_row;
+        uint8_t* sl = buf + (size_t)j * slot;
+        if (c < nch)
+          cp_async16(sl + 16 * c, src + (size_t)(r0 + j) * pitch + X0 + 16 * c);
+        else
+          cp_async16(sl + sw + 16 * (c - nch), rem + (((long)(r0 + j) * rem_cap + off) & ~7L) + 8 * (c - nch));
+      }
+    }
+    cp_async_commit();
+  };
+  uint32_t hn = 0;
+  bool hdone = !helper;
+  const uint32_t lsm = smem_u32(lring);
+  stage_block(0);
+  for (int k = 0; k < nstage; ++k) {
+    cp_async_wait<0>();
+    prod_bar();  // block k's staged rows (every thread's copies) are visible
+    ph(0);
+    if (!(fdbg & 4)) stage_block(k + 1);
+    ph(1);
+    const uint8_t* buf = pstage + (size_t)(k & 1) * kStageRows * slot;
+    const int r0 = a0f(k), nr = a1f(k) - r0;
+    // A1: warp per row
+    for (int j = pw; j < nr && !(fdbg & 8); j += kProdWarps) {
+      long long tq0 = prof ? clock64() : 0;
+      const long e = (long)(r0 + j) * rem_cap + off;
+      const int16_t* rr = staged ? reinterpret_cast<const int16_t*>(buf + (size_t)j * slot + sw) + (e & 7L) : rem + e;
+      // breakpoints: lane t holds a_t (t < 64 in registers; larger batches walk rr)
+      const uint32_t rrs = smem_u32(rr);
+      int alo = INT_MAX, ahi = INT_MAX;
+      if (staged) {
+        if (lane < b) alo = (int)(int16_t)lds16p(rrs + 2 * lane) - lane;
+        if (lane + 32 < b) ahi = (int)(int16_t)lds16p(rrs + 2 * (lane + 32)) - (lane + 32);
+      } else {
+        if (lane < b) alo = (int)rr[lane] - lane;
+        if (lane + 32 < b) ahi = (int)rr[lane + 32] - (lane + 32);
+      }
+      SCPL_DCHECK(lane >= b || ((int)rr[lane] >= lane && (int)rr[lane] < w + b && (lane == 0 || rr[lane - 1] < rr[lane])),
+                  "removed columns disjoint and in range (fused)");
+      int n_lt, m;
+      if (b <= 32) {
+        n_lt = __popc(__ballot_sync(0xffffffffu, alo < d0));
+        m = __popc(__ballot_sync(0xffffffffu, alo < d1)) - n_lt;
+      } else if (b <= 64) {
+        n_lt = __popc(__ballot_sync(0xffffffffu, alo < d0)) + __popc(__ballot_sync(0xffffffffu, ahi < d0));
+        m = __popc(__ballot_sync(0xffffffffu, alo < d1)) + __popc(__ballot_sync(0xffffffffu, ahi < d1)) - n_lt;
+      } else {
+        n_lt = 0;
+        m = 0;
+        for (int t = lane; t < b; t += 32) {
+          const int a = (int)rr[t] - t;
+          n_lt += a < d0;
+          m += a >= d0 && a < d1;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          n_lt += __shfl_xor_sync(0xffffffffu, n_lt, o);
+          m += __shfl_xor_sync(0xffffffffu, m, o);
+        }
+      }
+      // the first (up to) 2 in-range breakpoints in warp-uniform registers; more: walk rr
+      const bool few = m <= 2 && b <= 64;
+      int bp0 = INT_MAX, bp1 = INT_MAX;
+      if (few && m >= 1) {
+        const int t = n_lt;
+        bp0 = t < 32 ? __shfl_sync(0xffffffffu, alo, t & 31) : __shfl_sync(0xffffffffu, ahi, t & 31);
+        if (m >= 2) {
+          const int t1 = n_lt + 1;
+          bp1 = t1 < 32 ? __shfl_sync(0xffffffffu, alo, t1 & 31) : __shfl_sync(0xffffffffu, ahi, t1 & 31);
+        }
+      }
+      const uint8_t* sr = buf + (size_t)j * slot;  // staged: source column x at sr[x - X0]
+      const uint8_t* gsr = src + (size_t)(r0 + j) * pitch;
+      const uint32_t srs = smem_u32(sr), lrs = lsm + (uint32_t)(((r0 + j) % kLumRing) * lw - lo);
+      if (prof) {
+        const long long u = clock64();
+        prof[27] += u - tq0;
+        tq0 = u;
+      }
+      auto shift_at = [&](int y) {  // s(y) = #{a_t <= y}
+        if (few) return n_lt + (bp0 <= y) + (bp1 <= y);
+        int sy = n_lt;
+        for (int t = n_lt; t < n_lt + m; ++t) sy += (int)rr[t] - t <= y;
+        return sy;
+      };
+      for (int y4 = y0 + 4 * lane; y4 < d1 && !(fdbg & 1); y4 += 128) {
+        int s0 = n_lt, s3 = n_lt;
+        if (m > 0) {
+          s0 = shift_at(y4);
+          s3 = shift_at(y4 + 3);
+        }
+        uint32_t v;
+        if (staged && s0 == s3) {
+          const int x = y4 + s0 - X0;
+          const uint32_t a = srs + (uint32_t)(x & ~3);
+          v = __funnelshift_r(lds32p(a), lds32p(a + 4), (uint32_t)(x & 3) * 8u);
+        } else {  // the shift changes inside the word (or an unstaged row): byte by byte
+          const int xs[4] = {y4 + s0, y4 + 1 + shift_at(y4 + 1), y4 + 2 + shift_at(y4 + 2), y4 + 3 + s3};
+          v = 0u;
+          if (staged) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v |= (uint32_t)sr[xs[u] - X0] << (8 * u);
+          } else {
+            const int w0 = w + b;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v |= (xs[u] < w0 ? (uint32_t)gsr[xs[u]] : 0u) << (8 * u);
+          }
+        }
+        sts32p(lrs + (uint32_t)y4, v);
+      }
+      __syncwarp();
+      if (prof) {
+        const long long u = clock64();
+        prof[28] += u - tq0;
+        tq0 = u;
+      }
+      // edge replication (np.pad "edge") of this row: the same warp wrote it
+      if (d0 == 0 || d1 == w) {
+        uint8_t* lrow = lring + (size_t)((r0 + j) % kLumRing) * lw;
+        if (d0 == 0) {
+          const uint8_t v = lrow[-lo];
+          for (int c = lane; c < -lo; c += 32) lrow[c] = v;
+        }
+        if (d1 == w) {
+          const uint8_t v = lrow[w - 1 - lo];
+          for (int c = w - lo + lane; c < lw; c += 32) lrow[c] = v;
+        }
+      }
+      if (prof) prof[29] += clock64() - tq0;
+    }
+    if (prof) prof[30] += clock64() - pt;
+    prod_bar();
+    ph(3);
+    if (fdbg & 4) stage_block(k + 1);
+    // A2: the CTA's own columns to the next plane in 16-byte chunks (cta_lo and its ring column
+    // are 16-aligned; the last CTA may write up to 15 bytes past w -- never read)
+    {
+      const int nco = (cta_hi - cta_lo + 15) >> 4, c0 = cta_lo - lo;
+      for (int p = tp; p < nr * nco; p += NT) {
+        const int j = p / nco, c = p - j * nco;
+        *reinterpret_cast<uint4*>(dst + (size_t)(r0 + j) * pitch + cta_lo + 16 * c) =
+            *reinterpret_cast<const uint4*>(lring + (size_t)((r0 + j) % kLumRing) * lw + c0 + 16 * c);
+      }
+    }
+    ph(4);
+    if (k >= 2) mbar_wait_sleep(&empty[k & 1], ((k >> 1) - 1) & 1);
+    ph(5);
+    // B: Sobel of the block's rows (block 0 also row 0): groups of 8 rows, each shared by two
+    // warps (interleaved 4-column words), rows streamed
+    {
+      const int s0 = k == 0 ? 0 : 1 + kXRows * k, s1 = min(1 + kXRows * (k + 1), rows);
+      const int ngr = (s1 - s0 + 7) >> 3;
+      for (int g = pw >> 1; g < ngr; g += kProdWarps / 2) {
+        const int ra = s0 + 8 * g, rb = min(ra + 8, s1);
+        for (int c = 4 * (lane + 32 * (pw & 1)); c < rw; c += 256) {
+          if (tiny) {
+            for (int r = ra; r < rb; ++r) *reinterpret_cast<uint32_t*>(erow(r) + c) = 0u;
+            continue;
+          }
+          auto la = [&](int r) { return lsm + (uint32_t)((r % kLumRing) * lw + c + 16); };
+          uint32_t SEa, SOa, DEa, DOa, SEb, SOb, DEb, DOb;
+          sobel_prep(la(max(ra - 1, 0)), SEa, SOa, DEa, DOa);
+          sobel_prep(la(ra), SEb, SOb, DEb, DOb);
+          auto one = [&](int r) {
+            uint32_t SEc, SOc, DEc, DOc;
+            sobel_prep(la(min(r + 1, rows - 1)), SEc, SOc, DEc, DOc);
+            const uint32_t gxe = DEa + 2u * DEb + DEc, gxo = DOa + 2u * DOb + DOc;
+            const uint32_t gye = SEc + 0x04000400u - SEa, gyo = SOc + 0x04000400u - SOa;
+            const uint32_t ae = __vmaxu2(gxe, 0x08000800u - gxe) + __vmaxu2(gye, 0x08000800u - gye) - 0x08000800u;
+            const uint32_t ao = __vmaxu2(gxo, 0x08000800u - gxo) + __vmaxu2(gyo, 0x08000800u - gyo) - 0x08000800u;
+            *reinterpret_cast<uint32_t*>(erow(r) + c) =
+                __byte_perm(__vminu2(ae, 0x00FF00FFu), __vminu2(ao, 0x00FF00FFu), 0x6240);
+            SEa = SEb; SOa = SOb; DEa = DEb; DOa = DOb;
+            SEb = SEc; SOb = SOc; DEb = DEc; DOb = DOc;
+          };
+          if (rb - ra == 8) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) one(ra + r);
+          } else {
+            for (int r = ra; r < rb; ++r) one(r);
+          }
+        }
+      }
+    }
+    ph(6);
+    mbar_arrive(&full[k & 1]);
+    prod_bar();  // (the next block's A1 overwrites luma-ring rows this Sobel read)
+    ph(7);
+    if (!hdone && k >= 1) hdone = !pw_service<false>(R, hg, hstage, hbar, hn);
+    ph(8);
+  }
+  while (!hdone) hdone = !pw_service<false>(R, hg, hstage, hbar, hn);
+  ph(8);
+  cp_async_wait<0>();  // (only empty groups can remain: the select phase reuses the staging)
+}
+
+// Fused int passes: the DP warps read their energy rows from the CTA's shared ring, which the
+// producer warps fill (ring row 0 = image row 0, then two slots of 32 rows: block k in slot
+// k & 1, full[slot] completing once per use, empty[slot] when every active DP warp is done).
+struct FusedRing {
+  const uint8_t* ring;  // nullptr: per-warp TMA rings
+  int rw;               // ring row stride
+  int off;              // ring column of this warp's window start (win_lo - g_lo)
+  uint64_t* full;       // [2] producer -> DP
+  uint64_t* empty;      // [2] DP -> producer
+  long long* prof;      // (SCPL_PROF, one DP warp of rank 0) ring waits into prof[26]
+};
 
 template <bool F64, bool EDGE>
 __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
                         uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
                         uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage,
-                        uint64_t* hbar) {
+                        uint64_t* hbar, const FusedRing& F) {
   using V = Val<F64>;
   using T = typename V::T;
   constexpr int RS = DpCfg<F64>::kStageRows, S = DpCfg<F64>::kStages;
@@ -466,17 +854,24 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   const bool send_lo = nb_mode && active && rank > 0 && g.own_lo < g.cta_lo + kXRows;
   const bool send_hi = nb_mode && active && (int)rank + 1 < CL && g.own_hi > g.cta_hi - kXRows;
   const int nstage = (rows - 1 + RS - 1) / RS;
+  const bool fused = !F64 && F.ring != nullptr;
+  const int rsw = fused ? F.rw : kRingW;  // energy ring row stride
   if (active) {
+    if (fused) {  // row 0 comes with the first block
+      mbar_wait_sleep(&F.full[0], 0);
+      __syncwarp();
+    }
 #pragma unroll
     for (int k = 0; k < kC; ++k) {
       T v;
       if constexpr (F64)
         v = in[k] ? R.U[j0 + k] : 0.0;
       else
-        v = in[k] ? (int)R.grad[plane][j0 + k] << kKeyShift : 0;  // key of row 0
+        v = in[k] ? (int)(fused ? F.ring[F.off + lane * kC + k] : R.grad[plane][j0 + k]) << kKeyShift
+                  : 0;  // key of row 0
       ce[k] = in[k] ? v : V::inf();
     }
-    if (lane == 0)
+    if (lane == 0 && !fused)
       for (int st = 0; st < S - 1 && st < nstage; ++st) dp_issue_stage<F64>(Rg, plane, rows, st, g.win_lo, ring, bars);
   }
   // Exchange protocol (nb_mode): exchange e alternates between two mbarriers (e & 1); a
@@ -485,6 +880,13 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
   const uint32_t halo_bytes = nb_mode ? halo_bytes_for(w, CL, rank, (int)sizeof(T)) : 0u;
   // wait for stage st (issuing the one S-1 ahead first) and return its ring rows
   auto stage_rows = [&](int st) -> const uint8_t* {
+    if (fused) {
+      const long long tq = F.prof ? clock64() : 0;
+      mbar_wait_sleep(&F.full[st & 1], (st >> 1) & 1);
+      __syncwarp();
+      if (F.prof && lane == 0) F.prof[26] += clock64() - tq;
+      return F.ring + (size_t)(1 + kXRows * (st & 1)) * F.rw + F.off;
+    }
     __syncwarp();
     if (lane == 0 && st + S - 1 < nstage) dp_issue_stage<F64>(Rg, plane, rows, st + S - 1, g.win_lo, ring, bars);
     const int slot = st % S;
@@ -586,13 +988,13 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
           for (int r4 = 0; r4 < kSubRows; r4 += 4) {
             const uint8_t* ebase;
             if constexpr (RS == kXRows) {
-              ebase = stage + (size_t)(sb * kSubRows + r4) * kRingW * sz;
+              ebase = stage + (size_t)(sb * kSubRows + r4) * rsw * sz;
             } else {
               static_assert(RS == 4, "fp64 stages hold 4 rows");
               ebase = stage_rows((s0 - 1 + r4) / RS);
             }
 #pragma unroll
-            for (int r = 0; r < 4; ++r) dp_step<F64, EDGE>(ce, pw, ebase + (size_t)r * kRingW * sz, in, lane);
+            for (int r = 0; r < 4; ++r) dp_step<F64, EDGE>(ce, pw, ebase + (size_t)r * rsw * sz, in, lane);
           }
         } else {
 #pragma unroll 1
@@ -600,7 +1002,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
             const int i = s0 + r;
             const uint8_t* erow;
             if constexpr (RS == kXRows) {
-              erow = stage + (size_t)(sb * kSubRows + r) * kRingW * sz;
+              erow = stage + (size_t)(sb * kSubRows + r) * rsw * sz;
             } else {
               if ((i - 1) % RS == 0) stage = stage_rows((i - 1) / RS);
               erow = stage + (size_t)((i - 1) % RS) * kRingW * sz;
@@ -615,6 +1017,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
           for (int k = 0; k < kC; ++k) cwh[k] = 0u;
         }
       }
+      if (fused) mbar_arrive(&F.empty[xb & 1]);  // this block's energy rows are consumed
       // block end: owned words and landing deltas (read after the pass), stored after the
       // exchange below
       last_pbi = xb;
@@ -712,14 +1115,14 @@ template <bool F64>
 __device__ void dp_pass(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
                         uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
                         uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage,
-                        uint64_t* hbar) {
+                        uint64_t* hbar, const FusedRing& F) {
   // windows lie inside [0, w) unless the plane is narrower than one window
   if (g.w < kWin)
     dp_rows<F64, true>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
-                       pw_stage, hbar);
+                       pw_stage, hbar, F);
   else
     dp_rows<F64, false>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
-                        pw_stage, hbar);
+                        pw_stage, hbar, F);
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -1220,6 +1623,9 @@ struct PassBars {
 // initialised here (reinit: they held the previous pass's phases; every use of them is complete
 // -- the caller synchronised the cluster).  Ends with a cluster barrier: the batch's removed-
 // column log is complete.
+// FK: the fused kernel (kFusedWarps warps, fused int passes only); else the plain kernel
+// (kMaxWarps warps: fp64 passes and unfused int passes).
+template <bool FK>
 __device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iters, int removed, bool fp64,
                             uint8_t* smem, int* ws, const PassBars& B, bool reinit, long long& t_dp,
                             long long& t_sel) {
@@ -1234,6 +1640,15 @@ __device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iter
 
   const int per = ((w + CL - 1) / CL + 15) & ~15;
   const int ndp = min(kMaxWarps, (per + kOwn - 1) / kOwn);
+  // fused int pass: the host guarantees per >= kXRows and ndp <= kDpWarps at every width, and
+  // launches the fused kernel for exactly these passes
+  constexpr bool fused = FK;
+  if (FK != (!fp64 && R.fused != 0) || (FK && (per < kXRows || ndp > kDpWarps))) __trap();
+  int n_act = 0;  // DP warps with columns (they arrive on the ring's empty barriers)
+  {
+    const int clo = min(w, (int)rank * per), chi = min(w, clo + per);
+    for (int q = 0; q < ndp; ++q) n_act += clo + q * kOwn < chi;
+  }
   if (tid == 0) {
     if (reinit) {
       mbar_inval(&B.xbar[0]);
@@ -1246,11 +1661,19 @@ __device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iter
     if (rows > 1 && per >= kXRows)  // the pass's first exchange, announced before it can start
       mbar_arrive_tx(&B.xbar[0], halo_bytes_for(w, CL, rank, fp64 ? 8 : 4));
   }
-  if (lane == 0) {
+  if (fused) {  // rbar[0..1]: ring full (producer threads), rbar[2..3]: ring empty (DP lanes)
+    if (tid == 0)
+      for (int k = 0; k < 4; ++k) {
+        if (reinit) mbar_inval(&B.rbar[k]);
+        mbar_init(&B.rbar[k], k < 2 ? kProdWarps * 32 : max(n_act, 1) * 32);
+      }
+  } else if (lane == 0) {
     for (int k = 0; k < 6; ++k) {
       if (reinit) mbar_inval(&B.rbar[wid * 6 + k]);
       mbar_init(&B.rbar[wid * 6 + k], 1);
     }
+  }
+  if (lane == 0 && wid < kMaxWarps) {
     for (int k = 0; k < 4; ++k) {
       if (reinit) mbar_inval(&B.hbar[wid * 4 + k]);
       mbar_init(&B.hbar[wid * 4 + k], 32);
@@ -1278,6 +1701,44 @@ __device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iter
     // helper warps: the block-end global stores of DP warp (wid - ndp), off its critical path
     const bool helpers = per >= kXRows && 2 * ndp <= kMaxWarps;
     const int pitch = R.pitch;
+    if constexpr (FK) {
+      ProdGeo P;
+      P.rw = R.ring_w;
+      int g_hi = 0;
+      P.g_lo = 0;
+      const bool act = fused_cta_range(w, CL, (int)rank, P.g_lo, g_hi);
+      if (act && g_hi - P.g_lo > P.rw) __trap();  // (host bug: ring_w below the CTA's range)
+      P.cta_lo = min(w, (int)rank * per);
+      P.cta_hi = min(w, P.cta_lo + per);
+      uint32_t* stage0 = reinterpret_cast<uint32_t*>(smem + fused_off_stage(pitch));
+      uint8_t* ering = smem + fused_off_ering(pitch);
+      // register split (setmaxnreg, warpgroup-uniform): DP warpgroup up, producers down, then
+      // both back to the launch allocation for the select phase
+      if (wid < kProdFirst) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegDp));
+        if (wid < ndp) {
+          const Geo g = geo(wid);
+          const FusedRing F{ering, P.rw, g.win_lo - P.g_lo, &B.rbar[0], &B.rbar[2],
+                            R.prof && rank == 0 && wid == 0 ? R.prof : nullptr};
+          // (a DP warp without columns gets no helper: it would only send the end marker, after
+          // the other DP warps' blocks -- which its producer, blocked on that marker, must build)
+          dp_pass<false>(R, Rg, g, plane, reinterpret_cast<int*>(smem), CL, rank, per, B.xbar, xc, xm, nullptr,
+                         nullptr, rph, ndp, dprof, stage0 + wid * 2 * kPwStageWords,
+                         wid < n_act ? &B.hbar[wid * 4] : nullptr, F);
+        }
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegFused));
+      } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
+        const int q = wid - kProdFirst;
+        produce_pass(R, w, R.b, removed - R.b, P, ering, smem + fused_off_lring(pitch, P.rw),
+                     smem + fused_off_pstage(pitch, P.rw), &B.rbar[0], &B.rbar[2], tid - kProdFirst * 32,
+                     q < n_act, geo(min(q, ndp - 1)), stage0 + min(q, kDpWarps - 1) * 2 * kPwStageWords,
+                     &B.hbar[min(q, kDpWarps - 1) * 4], act,
+                     R.prof && rank == 0 && tid == kProdFirst * 32 ? R.prof : nullptr);
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegFused));
+      }
+    } else {
+    if (fused) __trap();
     uint8_t* ring = smem + 2 * (fp64 ? 8 : 4) * (size_t)pitch;
     uint32_t* pw_stage0 = reinterpret_cast<uint32_t*>(ring + (size_t)ndp * (fp64 ? dp_ring_bytes<true>()
                                                                                  : dp_ring_bytes<false>()));
@@ -1287,10 +1748,12 @@ __device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iter
       uint64_t* hb = helpers ? &B.hbar[wid * 4] : nullptr;
       if (fp64)
         dp_pass<true>(R, Rg, g, plane, reinterpret_cast<double*>(smem), CL, rank, per, B.xbar, xc, xm,
-                      ring + (size_t)wid * dp_ring_bytes<true>(), &B.rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
+                      ring + (size_t)wid * dp_ring_bytes<true>(), &B.rbar[wid * 6], rph, ndp, dprof, pw_stage, hb,
+                      FusedRing{});
       else
         dp_pass<false>(R, Rg, g, plane, reinterpret_cast<int*>(smem), CL, rank, per, B.xbar, xc, xm,
-                       ring + (size_t)wid * dp_ring_bytes<false>(), &B.rbar[wid * 6], rph, ndp, dprof, pw_stage, hb);
+                       ring + (size_t)wid * dp_ring_bytes<false>(), &B.rbar[wid * 6], rph, ndp, dprof, pw_stage, hb,
+                       FusedRing{});
     } else if (helpers && wid < 2 * ndp) {
       const int dw = wid - ndp;
       const uint32_t* stage = pw_stage0 + dw * 2 * kPwStageWords;
@@ -1298,6 +1761,7 @@ __device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iter
         pw_helper<true>(R, geo(dw), stage, &B.hbar[dw * 4]);
       else
         pw_helper<false>(R, geo(dw), stage, &B.hbar[dw * 4]);
+    }
     }
   }
   cluster_sync();  // lastce / pw / delta of all CTAs visible
@@ -1321,14 +1785,9 @@ __device__ int cluster_pass(CarveRun& Rg, int CL, uint32_t rank, int w, int iter
 // fp64_smem: this launch's dynamic shared memory holds the fp64 layouts (a buffered run's first
 // pass, every pass with reaverage_energy); int-pass launches get the smaller int layout, so two
 // pass CTAs fit on an SM.
-__global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun* __restrict__ runs, int CL,
-                                                                       int fp64_smem) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ int ws[32];
-  __shared__ __align__(8) uint64_t s_xbar[2];
-  __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
-  __shared__ __align__(8) uint64_t s_dbar;  // delta-table staging (select phase)
-  __shared__ __align__(8) uint64_t s_hbar[kMaxWarps * 4];  // DP warp -> helper warp staging
+template <bool FK>
+__device__ __forceinline__ void pass_body(CarveRun* __restrict__ runs, int CL, int fp64_smem, uint8_t* smem,
+                                          const PassBars& B, int* ws) {
   const uint32_t rank = cluster_rank();
   CarveRun& Rg = runs[blockIdx.x / CL];
   const int w = Rg.width, iters = Rg.iters, removed = Rg.removed;
@@ -1339,9 +1798,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
   const bool fp64 = Rg.U != nullptr && (iters == 0 || Rg.reaverage);  // reaverage: every pass on the mean
   if (fp64 && !fp64_smem) __trap();  // (launcher bug: an int-sized launch reached an fp64 pass)
   long long t_dp = 0, t_sel = 0;
-  const int b = cluster_pass(Rg, CL, rank, w, iters, removed, fp64, smem, ws,
-                             PassBars{s_xbar, s_rbar, &s_dbar, s_hbar}, false, t_dp, t_sel);
+  const int b = cluster_pass<FK>(Rg, CL, rank, w, iters, removed, fp64, smem, ws, B, false, t_dp, t_sel);
   if (rank == 0 && threadIdx.x == 0) {
+    if (FK) Rg.lsel ^= 1;  // the compacted luma went to the other plane
     Rg.b = b;
     Rg.width = w - b;
     Rg.iters = iters + 1;
@@ -1349,6 +1808,30 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun*
     Rg.cyc_dp += t_dp;
     Rg.cyc_sel += t_sel;
   }
+}
+
+__global__ void __launch_bounds__(kMaxWarps * 32, 2) carve_pass_kernel(CarveRun* __restrict__ runs, int CL,
+                                                                       int fp64_smem) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ int ws[32];
+  __shared__ __align__(8) uint64_t s_xbar[2];
+  __shared__ __align__(8) uint64_t s_rbar[kMaxWarps * 6];
+  __shared__ __align__(8) uint64_t s_dbar;  // delta-table staging (select phase)
+  __shared__ __align__(8) uint64_t s_hbar[kMaxWarps * 4];  // DP warp -> helper warp staging
+  pass_body<false>(runs, CL, fp64_smem, smem, PassBars{s_xbar, s_rbar, &s_dbar, s_hbar}, ws);
+}
+
+// Fused int passes: 4 DP warps + kProdWarps producer warps; launched at kRegFused registers per
+// thread (two CTAs per SM), split by setmaxnreg inside the DP phase.
+__global__ void __launch_bounds__(kFusedWarps * 32, 2) carve_pass_fused_kernel(CarveRun* __restrict__ runs,
+                                                                               int CL) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ int ws[32];
+  __shared__ __align__(8) uint64_t s_xbar[2];
+  __shared__ __align__(8) uint64_t s_rbar[4];
+  __shared__ __align__(8) uint64_t s_dbar;
+  __shared__ __align__(8) uint64_t s_hbar[kMaxWarps * 4];
+  pass_body<true>(runs, CL, 0, smem, PassBars{s_xbar, s_rbar, &s_dbar, s_hbar}, ws);
 }
 
 // Programmatic dependent launch: the row kernels and the loop check are launched while the
@@ -1639,6 +2122,39 @@ bool carve_f64_fits_pair(int width, int cl) { return carve_f64_smem(width, cl) <
 
 int carve_warps(int width, int cl) { return carve_dp_warps(width, cl); }
 
+// Fused int passes need, at every width the run's int passes see (target < w <= width0): at
+// least kXRows columns per CTA (neighbour exchanges) and at most kProdWarps DP warps.
+static int fused_ring_cap(int width0, int cl);
+// Opt-in (SCPL_FUSED=1): bit-exact, but measured slower than the separate row kernels -- the
+// producer warps are latency-bound next to the DP warps.
+bool carve_fused_ok(int width0, int target, int cl) {
+  if (!getenv("SCPL_FUSED")) return false;
+  const int per_min = ((target + 1 + cl - 1) / cl + 15) & ~15;
+  return per_min >= kXRows && carve_dp_warps(width0, cl) <= kDpWarps &&
+         fused_dp_bytes((width0 + 15) & ~15, fused_ring_cap(width0, cl)) <= kSmemBudgetInt;
+}
+
+// energy-ring row stride: the widest CTA range over every width up to width0 (a function of the
+// initial width and cluster size only, so launchers size the shared memory from them)
+static int fused_ring_cap(int width0, int cl) {
+  thread_local int c_w = -1, c_cl = -1, c_rw = 0;  // (launchers ask per iteration in host loops)
+  if (width0 == c_w && cl == c_cl) return c_rw;
+  int rw = 16;
+  for (int w = 1; w <= width0; ++w)
+    for (int r = 0; r < cl; ++r) {
+      int lo = 0, hi = 0;
+      if (fused_cta_range(w, cl, r, lo, hi)) rw = std::max(rw, (hi - lo + 15) & ~15);
+    }
+  c_w = width0;
+  c_cl = cl;
+  c_rw = rw;
+  return rw;
+}
+int carve_fused_ring_w(int width0, int target, int cl) {
+  (void)target;
+  return fused_ring_cap(width0, cl);
+}
+
 // pass, compact, gradient, check (+ mean with reaverage_energy)
 int carve_kernels_per_iteration(bool reaverage) { return reaverage ? 5 : 4; }
 
@@ -1682,20 +2198,25 @@ static void launch_carve_check(CarveRun* runs_d, int nruns, int max_iters, int* 
 }
 
 void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
-                            int max_fr, bool reaverage, bool f64, const RowsLoop* loop) {
+                            int max_fr, bool reaverage, bool f64, const RowsLoop* loop, bool fused) {
   if (nruns == 0) return;
   const int dpw = carve_dp_warps(width, cl);
   SCPL_ARG(dpw <= kMaxWarps, "carve width too large for the cluster size");
   const bool stage = carve_stage_dtab(rows, pitch, cl);
   f64 = f64 || reaverage;
   size_t smem = carve_smem_bytes(rows, pitch, stage, dpw, f64);
+  const bool fk = fused && !f64;  // the fused kernel: its DP phase holds the producer rings
+  if (fk) smem = std::max(carve_smem_bytes(rows, pitch, stage, dpw, false), fused_dp_bytes(pitch, fused_ring_cap(width, cl)));
   SCPL_ARG(smem <= 227 * 1024, "carve plane too large for shared memory");
   smem_optin(reinterpret_cast<const void*>(carve_pass_kernel));
-  if (cl > 8 && once_per_device(reinterpret_cast<const void*>(&launch_carve_iteration)))
+  smem_optin(reinterpret_cast<const void*>(carve_pass_fused_kernel));
+  if (cl > 8 && once_per_device(reinterpret_cast<const void*>(&launch_carve_iteration))) {
     SCPL_CUDA(cudaFuncSetAttribute(carve_pass_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SCPL_CUDA(cudaFuncSetAttribute(carve_pass_fused_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nruns * cl);
-  cfg.blockDim = dim3(kMaxWarps * 32);
+  cfg.blockDim = dim3((fk ? kFusedWarps : kMaxWarps) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1705,8 +2226,16 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl, f64 ? 1 : 0));
+  if (fk)
+    SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_fused_kernel, runs_d, cl));
+  else
+    SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl, f64 ? 1 : 0));
   SCPL_CHECK_LAUNCH();
+  if (fused) {  // the next pass's producers remove this batch: no row kernels
+    if (reaverage) launch_carve_mean(runs_d, nruns, rows, st);
+    if (loop) launch_carve_check(runs_d, nruns, loop->max_iters, loop->counters, loop->handle, st);
+    return;
+  }
   const size_t csmem = carve_compact_smem(pitch);
   smem_optin(reinterpret_cast<const void*>(carve_compact_kernel));
   cudaLaunchAttribute pa[1];
@@ -1751,7 +2280,7 @@ void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st)
 // per iteration.  first_f64: the runs' first pass is an fp64 one (they carry a uniform map).
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
                                  int* iters_d, int max_fr, bool reaverage, bool first_f64, FirstIter first,
-                                 int first_cl) {
+                                 int first_cl, bool fused) {
   cudaGraph_t g;
   SCPL_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -1764,7 +2293,7 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
     SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     const RowsLoop lp{max_iters, iters_d, h};
     (first ? first : launch_carve_iteration)(runs_d, nruns, rows, pitch, width, first ? first_cl : cl, cs, max_fr,
-                                             reaverage, true, &lp);
+                                             reaverage, true, &lp, fused);
     cudaStreamCaptureStatus cst;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
@@ -1784,7 +2313,7 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   {
     const RowsLoop lp{max_iters, iters_d, h};
-    launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false, &lp);
+    launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false, &lp, fused);
   }
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
   g_launches.store(before);  // counted per executed iteration by the caller

@@ -96,6 +96,14 @@ struct alignas(64) CarveRun {
   int16_t* cols;        // optional per-seam last-row column (capacity width0)
   double* costs;        // optional per-seam cost
   int16_t* labs;        // optional (seam dump): parent labels of every pass, passes x width0
+  // Fused int passes (fused != 0): the pass kernel's producer warps remove the previous batch
+  // from the luma plane luma[lsel] while the DP runs, write the compacted rows to luma[lsel ^ 1]
+  // and compute their Sobel energy straight into the DP's shared-memory ring (row stride
+  // ring_w) -- no compaction / gradient kernels, no gradient plane.
+  int fused;
+  int ring_w;
+  int lsel;
+  int fdbg;             // (experiments: SCPL_FDBG timing variants of the producer; results invalid)
   // state (read at every kernel entry, advanced by the pass kernel)
   int width;            // current width
   int iters;            // DP passes done
@@ -112,7 +120,7 @@ struct RowsLoop {
 };
 // one carve iteration of some DP window variant (the fp64 first pass may use another variant)
 using FirstIter = void (*)(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
-                           int max_fr, bool reaverage, bool f64, const RowsLoop* loop);
+                           int max_fr, bool reaverage, bool f64, const RowsLoop* loop, bool fused);
 // carve launchers (scpl_carve2.cu), compiled once per DP window width: kc6 (default) and kc4
 #define SCPL_CARVE_DECLS \
   void launch_run_setup(const uint8_t* frame, int H, int W, int C, int transposed, const uint16_t* codes, \
@@ -122,12 +130,14 @@ using FirstIter = void (*)(CarveRun* runs_d, int nruns, int rows, int pitch, int
   void encode_carve_tensor_maps(CarveRun& R); \
   void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st, \
                               int max_fr = 1, bool reaverage = false, bool f64 = false, \
-                              const RowsLoop* loop = nullptr); \
+                              const RowsLoop* loop = nullptr, bool fused = false); \
   void launch_carve_index(CarveRun* runs_d, int nruns, int rows, cudaStream_t st); \
   void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st); \
   cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters, \
                                    int* iters_d, int max_fr = 1, bool reaverage = false, bool first_f64 = false, \
-                                   FirstIter first = nullptr, int first_cl = 0); \
+                                   FirstIter first = nullptr, int first_cl = 0, bool fused = false); \
+  bool carve_fused_ok(int width0, int target, int cl); \
+  int carve_fused_ring_w(int width0, int target, int cl); \
   void encode_carve_tensor_map_U(CarveRun& R); \
   bool carve_f64_fits_pair(int width, int cl); \
   bool carve_stage_dtab(int rows, int pitch, int cl); \

@@ -457,3 +457,30 @@ def test_sharded_clip_matches_reference(P, world):
         assert dp == g["dp_passes"]
         bad = [t for t in range(merged.shape[0]) if sha(merged[t]) != g["frames_sha"][t]]
         assert not bad, f"{name} (scan once): {len(bad)} frames differ"
+
+
+@pytest.mark.parametrize("host_loops", [False, True])
+def test_fused_passes_match(P, host_loops, monkeypatch):
+    """SCPL_FUSED=1 (experimental fused int passes: the pass kernel's producer warps remove the
+    previous batch and compute the Sobel energy into the DP's ring) gives the reference's runs,
+    passes and frames -- a C4 clip against its golden, random single frames against the oracle."""
+    from oracle import scpl_oracle as O
+    from paper_1903_03180_b200.synth import config_clip
+    import torch
+    monkeypatch.setenv("SCPL_FUSED", "1")
+    if host_loops:
+        monkeypatch.setenv("SCPL_HOST_LOOPS", "1")
+    path = _config_golden("C4_clip0")[0]
+    g = json.load(open(path))
+    clip, tw, th = config_clip(g["config"], frames=g["frames"], clip=g["clip"])
+    out, m = P.retarget_video_tensor(torch.from_numpy(clip).cuda(),
+                                     P.RetargetConfig(target_width=tw, target_height=th, mode="buffered"))
+    assert [list(r) for r in m.runs] == g["runs"] and m.dp_passes == g["dp_passes"]
+    host_out = out.cpu().numpy()
+    assert all(sha(host_out[i]) == g["frames_sha"][i] for i in range(host_out.shape[0]))
+    rng = np.random.default_rng(21)
+    for h, w, t in [(100, 300, 250), (34, 520, 400), (200, 100, 60), (65, 1100, 1000)]:
+        frame = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+        c1, b1 = P.batch_carve(frame, t)
+        c2, b2 = O.batch_carve(frame, t)
+        assert np.array_equal(c1, c2) and [len(x) for x in b1] == [len(x) for x in b2]
