@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) replay_rows_kernel(const uint8_t* __restr
 // consecutive output pixels, keeps their 16 source columns in registers, and per frame gathers
 // 16*C bytes from the staged input row into registers and writes them with 16-byte stores.
 // Input rows arrive by 1-D bulk copies (TMA) into a kRing-slot ring, kRing-1 frames ahead.
-constexpr int kRing = 3;
+constexpr int kRing = 4;  // 3 frames ahead: a short run's rows are all in flight at once
 constexpr int kRpPx = 16;  // output pixels per thread
 
 template <int C>
@@ -91,8 +91,16 @@ __global__ void __launch_bounds__(128) replay_rows_vec_kernel(const uint8_t* __r
   const int y0 = tid * kRpPx;
   const bool active = y0 < tw;
   int src[kRpPx];
+  if (active && y0 + kRpPx <= tw && (stride & 7) == 0) {  // two 16-byte loads of the index row
+    const uint4* ip = reinterpret_cast<const uint4*>(idx + (size_t)i * stride + y0);
+    const uint4 a = __ldg(ip), b = __ldg(ip + 1);
+    const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int k = 0; k < kRpPx; ++k) src[k] = active && y0 + k < tw ? (int)idx[(size_t)i * stride + y0 + k] * C : 0;
+    for (int k = 0; k < kRpPx; ++k) src[k] = (int)(int16_t)(wv[k >> 1] >> (16 * (k & 1))) * C;
+  } else {
+#pragma unroll
+    for (int k = 0; k < kRpPx; ++k) src[k] = active && y0 + k < tw ? (int)idx[(size_t)i * stride + y0 + k] * C : 0;
+  }
 #pragma unroll
   for (int k = 0; k < kRpPx; ++k)
     SCPL_DCHECK(src[k] >= 0 && src[k] < W * C && (k == 0 || y0 + k >= tw || src[k] > src[k - 1]),

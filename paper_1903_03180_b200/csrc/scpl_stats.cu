@@ -669,32 +669,25 @@ __global__ void __launch_bounds__(256) uniform_vec_kernel(const uint16_t* __rest
   const uint4* src = reinterpret_cast<const uint4*>(codes + (size_t)s * N + p);
   const size_t fstride = (size_t)N / kUniPx;  // uint4 per frame
   double acc[kUniPx];
-  {
-    const uint4 v = __ldcs(src);
-    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-    const bool pure = first_pure && s == 0;
+  // frames in chunks of 8 with every load of a chunk in flight (short runs -- 2 to 8 frames --
+  // are one round trip), then the sequential fp64 sum in frame order (buffering.py:69-71)
+  const bool pure0 = first_pure && s == 0;
+  for (int t0 = 0; t0 < n; t0 += 8) {
+    uint4 v[8];
 #pragma unroll
-    for (int k = 0; k < kUniPx; ++k) acc[k] = energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, pure, wm, wg);
-  }
-  int t = 1;
-  for (; t + 4 <= n; t += 4) {
-    uint4 v[4];
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < n) v[u] = __ldcs(src + (size_t)(t0 + u) * fstride);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + (size_t)(t + u) * fstride);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
+      if (t0 + u >= n) break;
       const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+      const bool pure = pure0 && t0 + u == 0;
 #pragma unroll
-      for (int k = 0; k < kUniPx; ++k)
-        acc[k] = __dadd_rn(acc[k], energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, false, wm, wg));
+      for (int k = 0; k < kUniPx; ++k) {
+        const double e = energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, pure, wm, wg);
+        acc[k] = t0 + u == 0 ? e : __dadd_rn(acc[k], e);
+      }
     }
-  }
-  for (; t < n; ++t) {
-    const uint4 v = __ldcs(src + (size_t)t * fstride);
-    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int k = 0; k < kUniPx; ++k)
-      acc[k] = __dadd_rn(acc[k], energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, false, wm, wg));
   }
   const double dn = (double)n;
   const int i = (int)(p / W), j = (int)(p - (long)i * W);
