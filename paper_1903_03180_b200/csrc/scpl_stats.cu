@@ -659,7 +659,7 @@ __device__ __forceinline__ double energy_fp64(uint32_t code, bool pure, double w
   if (pure) return (double)g;
   return fmin(__dadd_rn(__dmul_rn(wm, (double)(code >> 8)), __dmul_rn(wg, (double)g)), 255.0);
 }
-__global__ void __launch_bounds__(256) uniform_vec_kernel(const uint16_t* __restrict__ codes, int H, int W, int s,
+__global__ void __launch_bounds__(256, 4) uniform_vec_kernel(const uint16_t* __restrict__ codes, int H, int W, int s,
                                                           int n, int first_pure, double wm, double wg,
                                                           double* __restrict__ out, int pitch) {
   const long N = (long)H * W;
@@ -669,16 +669,16 @@ __global__ void __launch_bounds__(256) uniform_vec_kernel(const uint16_t* __rest
   const uint4* src = reinterpret_cast<const uint4*>(codes + (size_t)s * N + p);
   const size_t fstride = (size_t)N / kUniPx;  // uint4 per frame
   double acc[kUniPx];
-  // frames in chunks of 8 with every load of a chunk in flight (short runs -- 2 to 8 frames --
-  // are one round trip), then the sequential fp64 sum in frame order (buffering.py:69-71)
+  // frames in chunks of 4 with every load of a chunk in flight (a short run is one or two round
+  // trips), then the sequential fp64 sum in frame order (buffering.py:69-71)
   const bool pure0 = first_pure && s == 0;
-  for (int t0 = 0; t0 < n; t0 += 8) {
-    uint4 v[8];
+  for (int t0 = 0; t0 < n; t0 += 4) {
+    uint4 v[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 4; ++u)
       if (t0 + u < n) v[u] = __ldcs(src + (size_t)(t0 + u) * fstride);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       if (t0 + u >= n) break;
       const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
       const bool pure = pure0 && t0 + u == 0;
