@@ -234,7 +234,9 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, ScanLane& lane, const uint16_t* co
                 const scpl_video_params& P, cudaStream_t st) {
   const long N = (long)H * W;
   const PwPlan& plan = plan_for(ctx, N);
-  const int spec = P.spec_len > 0 ? P.spec_len : 8;
+  // candidates per scan window (speculation length): params, else SCPL_SPEC (experiments), else 8
+  static const int spec_env = getenv("SCPL_SPEC") ? atoi(getenv("SCPL_SPEC")) : 0;
+  const int spec = P.spec_len > 0 ? P.spec_len : (spec_env > 0 ? spec_env : 8);
   SCPL_ARG(spec <= 64, "spec_len must be <= 64");
   if (!lane.scan) SCPL_CUDA(cudaMalloc(&lane.scan, sizeof(ScanState)));
   auto key = std::make_tuple(N, spec, (const void*)lane.scan);

@@ -334,7 +334,13 @@ __device__ __forceinline__ void dp_row(typename Val<F64>::T (&ce)[kC], uint64_t 
 // dirs within the current 32-row block, so the block's landing delta (sumdir - rows) needs
 // no path word.  cw collects this column's own dir per row (the choice word, latest row in
 // the low bits); the trace walks the choice words of the columns a seam visits.
-template <bool EDGE>
+// MASK (bit 0: left, bit 1: right): the window's left / right end is an image border (always
+// both with the EDGE layout): the lane at that end sees +inf beyond it.  Any other window end
+// is a decaying halo -- whatever value enters there reaches at most column r of the window after
+// r rows, never the owned columns (kXRows in from each end) within a 32-row block -- so it takes
+// the shuffled key unmasked, and the neighbour keys enter the minimum last (one dependent op
+// per row after the shuffle).
+template <bool EDGE, int MASK>
 __device__ __forceinline__ void dp_row_key(int (&K)[kC], uint32_t (&cw)[kC], const uint8_t* erow,
                                            const bool (&in)[kC], int lane) {
   int e[kC];
@@ -343,18 +349,26 @@ __device__ __forceinline__ void dp_row_key(int (&K)[kC], uint32_t (&cw)[kC], con
   for (int k = 0; k < kC; ++k) e[k] = (int)p[k];
   int left = __shfl_up_sync(0xffffffffu, K[kC - 1], 1);
   int right = __shfl_down_sync(0xffffffffu, K[0], 1);
-  if (lane == 0) left = kIntInf;
-  if (lane == 31) right = kIntInf;
+  if ((MASK & 1) && lane == 0) left = kIntInf;
+  if ((MASK & 2) && lane == 31) right = kIntInf;
   int n[kC];
 #pragma unroll
   for (int k = 0; k < kC; ++k) {
     // the candidates' biases add dir to the dir field and to the dir sum at once (sumdir + dir
     // <= 64 + 2 never carries into the dir field, so ties still go to the lower dir); the new
-    // key is the minimum with its dir field cleared plus the energy
-    const int l = k > 0 ? K[k - 1] : left;
-    const int c = K[k] + ((1 << kDirShift) + 1);
-    const int r = (k + 1 < kC ? K[k + 1] : right) + ((2 << kDirShift) + 2);
-    const int m = min(min(l, c), r);
+    // key is the minimum with its dir field cleared plus the energy.  The lane's own candidates
+    // are combined first, the shuffled neighbour last (integer min: the order does not matter)
+    constexpr int kBc = (1 << kDirShift) + 1, kBr = (2 << kDirShift) + 2;
+    int m;
+    if (kC == 1) {
+      m = min(min(K[0] + kBc, right + kBr), left);
+    } else if (k == 0) {
+      m = min(min(K[0] + kBc, K[1] + kBr), left);
+    } else if (k == kC - 1) {
+      m = min(min(K[k - 1], K[k] + kBc), right + kBr);
+    } else {
+      m = min(min(K[k - 1], K[k] + kBc), K[k + 1] + kBr);
+    }
     const int d = m & (3 << kDirShift);
     int v;  // m - d + e * 512 as two multiply-adds (FMA pipe; the ALU pipe is the DP's bottleneck)
     asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(v) : "r"(e[k]), "r"(1 << kKeyShift), "r"(m));
@@ -366,14 +380,14 @@ __device__ __forceinline__ void dp_row_key(int (&K)[kC], uint32_t (&cw)[kC], con
   for (int k = 0; k < kC; ++k) K[k] = n[k];
 }
 
-// one row of either pass
-template <bool F64, bool EDGE, class PW>
+// one row of either pass (the fp64 pass always masks)
+template <bool F64, bool EDGE, int MASK, class PW>
 __device__ __forceinline__ void dp_step(typename Val<F64>::T (&ce)[kC], PW (&pw)[kC], const uint8_t* erow,
                                         const bool (&in)[kC], int lane) {
   if constexpr (F64)
     dp_row<true, EDGE>(ce, pw, erow, in, lane);
   else
-    dp_row_key<EDGE>(ce, pw, erow, in, lane);
+    dp_row_key<EDGE, MASK>(ce, pw, erow, in, lane);
 }
 
 // One DP pass for this warp's window.  ceX: smem exchange rows [2][pitch]; ring: this
@@ -825,7 +839,7 @@ struct FusedRing {
   long long* prof;      // (SCPL_PROF, one DP warp of rank 0) ring waits into prof[26]
 };
 
-template <bool F64, bool EDGE>
+template <bool F64, bool EDGE, int MASK>
 __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int plane, typename Val<F64>::T* ceX, int CL,
                         uint32_t rank, int per_cta, uint64_t* xbar, uint32_t& xc, uint32_t& xm, uint8_t* ring,
                         uint64_t* bars, uint32_t& rph, int ndp, long long* dprof, uint32_t* pw_stage,
@@ -994,7 +1008,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
               ebase = stage_rows((s0 - 1 + r4) / RS);
             }
 #pragma unroll
-            for (int r = 0; r < 4; ++r) dp_step<F64, EDGE>(ce, pw, ebase + (size_t)r * rsw * sz, in, lane);
+            for (int r = 0; r < 4; ++r) dp_step<F64, EDGE, MASK>(ce, pw, ebase + (size_t)r * rsw * sz, in, lane);
           }
         } else {
 #pragma unroll 1
@@ -1007,7 +1021,7 @@ __device__ void dp_rows(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
               if ((i - 1) % RS == 0) stage = stage_rows((i - 1) / RS);
               erow = stage + (size_t)((i - 1) % RS) * kRingW * sz;
             }
-            dp_step<F64, EDGE>(ce, pw, erow, in, lane);
+            dp_step<F64, EDGE, MASK>(ce, pw, erow, in, lane);
           }
         }
       }
@@ -1118,11 +1132,27 @@ __device__ void dp_pass(const CarveRun& R, const CarveRun& Rg, const Geo& g, int
                         uint64_t* hbar, const FusedRing& F) {
   // windows lie inside [0, w) unless the plane is narrower than one window
   if (g.w < kWin)
-    dp_rows<F64, true>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+    dp_rows<F64, true, 3>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
                        pw_stage, hbar, F);
-  else
-    dp_rows<F64, false>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
-                        pw_stage, hbar, F);
+  else if constexpr (F64)  // (the fp64 pass always masks both ends)
+    dp_rows<true, false, 3>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+                            pw_stage, hbar, F);
+  else {
+    // which window ends are image borders
+    const int mask = (g.win_lo <= 0 ? 1 : 0) | (g.win_lo + kWin >= g.w ? 2 : 0);
+    if (mask == 0)
+      dp_rows<false, false, 0>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+                               pw_stage, hbar, F);
+    else if (mask == 1)
+      dp_rows<false, false, 1>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+                               pw_stage, hbar, F);
+    else if (mask == 2)
+      dp_rows<false, false, 2>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+                               pw_stage, hbar, F);
+    else
+      dp_rows<false, false, 3>(R, Rg, g, plane, ceX, CL, rank, per_cta, xbar, xc, xm, ring, bars, rph, ndp, dprof,
+                               pw_stage, hbar, F);
+  }
 }
 
 // ------------------------------------------------------------------ block helpers
