@@ -62,6 +62,47 @@ void smem_optin(const void* kernel) {
                                  optin - (int)fa.sharedSizeBytes));
   done.insert({dev, kernel});
 }
+static bool graph_prio_on() {
+  static const bool on = !(getenv("SCPL_GRAPH_PRIO") && atoi(getenv("SCPL_GRAPH_PRIO")) == 0);
+  return on;
+}
+void graph_set_priority(cudaGraph_t g, int prio) {
+  if (!graph_prio_on()) return;
+  static const bool dbg = getenv("SCPL_DEBUG_PRIO") != nullptr;
+  size_t n = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n && cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  for (cudaGraphNode_t nd : nodes) {
+    // (not every node type answers the attribute calls: those are skipped)
+    cudaKernelNodeAttrValue v = {};
+    const cudaError_t e0 = cudaGraphKernelNodeGetAttribute(nd, cudaKernelNodeAttributePriority, &v);
+    const int had = v.priority;
+    if (e0 != cudaSuccess) {
+      cudaGetLastError();
+      if (dbg) fprintf(stderr, "scpl prio: node skipped (%s)\n", cudaGetErrorString(e0));
+      continue;
+    }
+    v.priority = prio;
+    const cudaError_t e1 = cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributePriority, &v);
+    if (e1 != cudaSuccess) cudaGetLastError();
+    if (dbg) fprintf(stderr, "scpl prio: kernel node %d -> %d (%s)\n", had, prio, cudaGetErrorString(e1));
+  }
+}
+cudaStream_t capture_stream(int prio) {
+  cudaStream_t cs;
+  if (graph_prio_on())
+    SCPL_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio));
+  else
+    SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  return cs;
+}
 std::atomic<long> g_launches{0};
 }  // namespace scpl
 
@@ -206,6 +247,7 @@ uint8_t* pinned_scratch(scpl_ctx* ctx, size_t bytes) {
 // closed runs to the carve while the scan goes on -- it never waits on an ASDE.
 struct ScanStream {
   DBuf ck, leafsum, partial, runs_d;
+  long N = 0;
   cudaGraphExec_t graph = nullptr;
   const PwPlan* plan = nullptr;
   ScanState* state = nullptr;  // the lane's device state
@@ -242,10 +284,12 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, ScanLane& lane, const uint16_t* co
   auto key = std::make_tuple(N, spec, (const void*)lane.scan);
   auto it = ctx->scan_graphs.find(key);
   if (it == ctx->scan_graphs.end())
-    it = ctx->scan_graphs.emplace(key, build_scan_graph(lane.scan, plan.leaves, plan.nleaves, plan.vnodes, spec))
+    it = ctx->scan_graphs.emplace(key, build_scan_graph(lane.scan, N, plan.leaves, plan.nleaves, plan.vnodes, spec,
+                                                         ctx->prio_known ? ctx->prio_hi : 0))
              .first;
   S.graph = it->second;
   S.plan = &plan;
+  S.N = N;
   S.state = lane.scan;
   S.spec = spec;
   S.T = T;
@@ -284,7 +328,7 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, ScanLane& lane, const uint16_t* co
 void scan_chunk(ScanStream& S, int c, int avail, cudaStream_t st) {
   launch_scan_avail(S.state, avail, st);
   if (host_loops())
-    run_scan_host(S.state, S.plan->leaves, S.plan->nleaves, S.plan->vnodes, S.spec, S.h_L, st);
+    run_scan_host(S.state, S.N, S.plan->leaves, S.plan->nleaves, S.plan->vnodes, S.spec, S.h_L, st);
   else
     SCPL_CUDA(cudaGraphLaunch(S.graph, st));
   // (SM copies into mapped pinned memory: no copy-engine queueing behind the clip's copies)
@@ -298,7 +342,7 @@ void scan_end(ScanStream& S, cudaStream_t st) { kc6::launch_word_copy(S.h_state,
 void scan_finish(ScanStream& S, int chunks, scpl_video_result* result) {
   const ScanState& R = *S.h_state;
   if (!(R.done == 1 && R.nruns >= 1 && R.nruns <= S.T)) throw Error{2, "buffer scan did not finish"};
-  g_launches.fetch_add((long)chunks + 3L * R.steps, std::memory_order_relaxed);
+  g_launches.fetch_add((long)chunks + (long)R.steps, std::memory_order_relaxed);
   result->scan_windows = R.steps;
   result->scan_fallbacks = R.fallbacks;
 }
@@ -520,9 +564,11 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
     if (R.prof) SCPL_CUDA(cudaMemsetAsync(R.prof, 0, kProfBytes, st));
   }
   S.ctx = ctx;
+  int prio = 0;  // the loop's kernel nodes carry the group stream's priority (part of the pool key)
+  SCPL_CUDA(cudaStreamGetPriority(st, &prio));
   S.loop_key = {nb, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
                 (int)S.reaverage + 2 * graph + 4 * S.kc + 64 * (int)S.has_uniform + 128 * S.kc_first +
-                    2048 * S.cl_first + 65536 * (int)S.fused};
+                    2048 * S.cl_first + 65536 * (int)S.fused + (1 << 20) * (prio & 15)};
   auto it = ctx->loop_pool.find(S.loop_key);
   if (it != ctx->loop_pool.end()) {
     S.loop = it->second;
@@ -564,7 +610,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
     if (!S.loop.ex)
       S.loop.ex = SCPL_CARVE_FN(S.kc, build_carve_loop)(
           runs_d, nb, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, iters_d, S.max_fr, S.reaverage,
-          S.has_uniform, SCPL_CARVE_FN(S.kc_first, launch_carve_iteration), S.cl_first, S.fused);
+          S.has_uniform, SCPL_CARVE_FN(S.kc_first, launch_carve_iteration), S.cl_first, S.fused, prio);
     SCPL_CUDA(cudaGraphLaunch(S.loop.ex, st));
   }
   kc6::launch_carve_index(runs_d, nruns, S.rows, st);

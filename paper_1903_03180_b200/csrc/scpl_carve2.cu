@@ -2310,13 +2310,12 @@ void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st)
 // per iteration.  first_f64: the runs' first pass is an fp64 one (they carry a uniform map).
 cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters,
                                  int* iters_d, int max_fr, bool reaverage, bool first_f64, FirstIter first,
-                                 int first_cl, bool fused) {
+                                 int first_cl, bool fused, int prio) {
   cudaGraph_t g;
   SCPL_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
   SCPL_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-  cudaStream_t cs;
-  SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaStream_t cs = capture_stream(prio);
   const long before = g_launches.load();
   cudaGraphNode_t pro_last = nullptr;
   if (first_f64 && !reaverage) {  // prologue: the fp64 pass, then the condition for the loop
@@ -2346,6 +2345,8 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
     launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false, &lp, fused);
   }
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
+  graph_set_priority(g, prio);
+  graph_set_priority(body, prio);
   g_launches.store(before);  // counted per executed iteration by the caller
   cudaGraphExec_t ex;
   SCPL_CUDA(cudaGraphInstantiate(&ex, g, 0));

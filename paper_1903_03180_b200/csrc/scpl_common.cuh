@@ -56,6 +56,11 @@ static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 void smem_optin(const void* kernel);
 // true the first time (current device, key) is seen (per-device one-time attribute setup)
 bool once_per_device(const void* key);
+// Kernel nodes of a captured graph run at the priority recorded in the node, not at the
+// priority of the stream the graph is launched into: give every kernel node of g this one.
+void graph_set_priority(cudaGraph_t g, int prio);
+// the capture stream for a graph whose kernels should run at prio (SCPL_GRAPH_PRIO=0: default)
+cudaStream_t capture_stream(int prio);
 
 // ---------------------------------------------------------------- exact arithmetic
 // energy.py:35 -- luma = rint(fma(b,.114, fma(r,.299, g*.587))).  Outside the exact

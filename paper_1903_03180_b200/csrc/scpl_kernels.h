@@ -50,7 +50,7 @@ struct ScanState {
   double wm, wg;
   int T, max_len, spec, avail;
   int s, n_acc, init, L, done, nruns;
-  int steps;      // loop-body executions (3 kernels each)
+  int steps;      // loop-body executions (one window kernel each; its last CTA decides and plans)
   // Screened windows: a window is first evaluated by the cheap bounded kernel (approximate
   // ASDE + a rigorous bound on its distance to the reference's value); only a window with a
   // candidate whose threshold test the bound cannot settle is re-run exactly.
@@ -59,11 +59,13 @@ struct ScanState {
   int force_fallback;  // testing: treat every screened window as inconclusive
   int fallbacks;  // windows re-run exactly
   double asum[kScanMaxL], bsum[kScanMaxL];  // per candidate: sum of approximate std, of bounds
+  unsigned int ticket;  // CTAs of the current window launch that are done (the last one decides)
 };
-cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec);
+cudaGraphExec_t build_scan_graph(ScanState* S, long N, const int2* leaves, int nleaves, const PwVnode* vnodes,
+                                 int spec, int prio = 0);
 void launch_scan_reset(ScanState* S, const ScanState& init, cudaStream_t st);
 void launch_scan_avail(ScanState* S, int avail, cudaStream_t st);
-void run_scan_host(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec, int* h_L,
+void run_scan_host(ScanState* S, long N, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec, int* h_L,
                    cudaStream_t st);
 void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
                     int transposed, double* out, cudaStream_t st, int pitch = 0);
@@ -135,7 +137,8 @@ using FirstIter = void (*)(CarveRun* runs_d, int nruns, int rows, int pitch, int
   void launch_word_copy(void* dst, const void* src, size_t bytes, cudaStream_t st); \
   cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, int max_iters, \
                                    int* iters_d, int max_fr = 1, bool reaverage = false, bool first_f64 = false, \
-                                   FirstIter first = nullptr, int first_cl = 0, bool fused = false); \
+                                   FirstIter first = nullptr, int first_cl = 0, bool fused = false, \
+                                   int prio = 0); \
   bool carve_fused_ok(int width0, int target, int cl); \
   int carve_fused_ring_w(int width0, int target, int cl); \
   void encode_carve_tensor_map_U(CarveRun& R); \

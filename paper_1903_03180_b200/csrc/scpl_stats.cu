@@ -89,7 +89,8 @@ constexpr int kStatStageBytes = (256 / kLeafLanes) * 128 * 2;  // one CTA's pixe
 // ring, its barriers, the A / B energy tables; screened windows add (sum std~, sum bound) per
 // candidate and warp (kStatRed per candidate).  ~21 KB at spec 8: a scan CTA fits on an SM
 // next to a resident carve-pass CTA.
-constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatStages + 2 * 256 * sizeof(double);
+constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatStages + 2 * 256 * sizeof(double) +
+                             kScanMaxL * sizeof(double);  // (+ the screened body's 1 / n table)
 constexpr size_t kStatRed = 16 * sizeof(double);
 
 // numpy's leaf sum (pairwise_sum, n <= 128): r[j] = a[j] + a[j+8] + ... (sequential), then
@@ -311,6 +312,304 @@ __device__ __forceinline__ void window_stats_body(const uint16_t* __restrict__ c
   }
 }
 
+// ------------------------------------------------------------ device: screened windows
+// The screened (APPROX) evaluation of a window does not need numpy's summation tree: only
+// S and Q per pixel are exact (they are the checkpoint); sum(std~) and sum(bound) may be
+// added in any order (their f32 roundings are part of scan_step_kernel's margin).  So this
+// body drops the leaf layout: a CTA owns `chunk` consecutive pixels (a multiple of 8, sized so
+// the grid is a whole number of waves), thread t the pixel pairs 2 (t + 256 k), k = 0..3 --
+// one 32-bit shared-memory load per pair and frame, one 16-byte checkpoint load / store per
+// pair, no per-pixel branches (warps skip whole k slots past the chunk; only the one warp on
+// the chunk's edge runs the masked variant).  Per pixel and candidate: 2 I2F, 9 fp64
+// operations (e, S, Q, m, Q/n, var), F2F, MUFU.RSQ and 5 f32 operations.
+//   * the clamp min(e, 255) is a no-op when wm, wg >= 0 and fl(fl(255 wm) + fl(255 wg)) <= 255
+//     (rounding is monotone, so every e is <= that value): CLAMP = false drops it;
+//   * a pure-gradient frame (the clip's first, energy.py:79-80) is wm = 0, wg = 1 (exact);
+//   * the bound min(sqrt(delta), delta * rs) is accumulated as min(1 / sqrt(delta), rs) and
+//     scaled by delta once per CTA: kScrCap * kScanDelta == kScanSqrtDelta, and the f32 sums'
+//     relative rounding (< 2e-6) is far inside kScanDelta's factor 2 over the proven bound.
+constexpr int kScrPairs = 4;                          // pixel pairs per thread
+constexpr int kScrMaxChunk = 256 * 2 * kScrPairs;     // 2048 pixels per CTA at most
+constexpr float kScrCap = 70715.0f;                   // kScanSqrtDelta / kScanDelta
+// The screened body's ring holds a whole default window (8 candidates + the initial frame start
+// with every copy in flight): the kernel is bound by memory latency, not by a pipe (ncu round
+// 2d: SMs active 75% of the time, issue slots 50%, DRAM 18%), so nothing waits on a refill.
+constexpr int kScrStages = 8;
+constexpr size_t kScrSmem = (size_t)kScrStages * kStatStageBytes + 8 * kScrStages + kScanMaxL * 8 * 2 * sizeof(float) +
+                            kScanMaxL * sizeof(double);
+static_assert(kScrMaxChunk * 2 <= kStatStageBytes, "a chunk's codes of one frame fit a ring stage");
+
+// CTAs' pixels for a frame of N pixels: the smallest whole number of waves (4 CTAs per SM)
+// that keeps a chunk within kScrMaxChunk; a multiple of 8 pixels (16-byte bulk copies)
+int screen_chunk(long N, int num_sms) {
+  const long wave = (long)std::max(1, num_sms) * 4;
+  long g = wave;
+  while (cdiv(N, g) > kScrMaxChunk) g += wave;
+  long chunk = cdiv(N, g);
+  chunk = (chunk + 7) & ~7L;
+  return (int)std::min<long>(kScrMaxChunk, std::max<long>(512, chunk));
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// Integer -> double and double -> float without the conversion unit: the window kernel was
+// bound by the XU pipe (I2F.F64, F2F.F32.F64 and MUFU share it: 68% busy, ncu round 2d) while
+// the fp64 pipe idled.  u8_f64: 2^52 + k is exact in the low mantissa bits, minus 2^52 (exact).
+// f64_f32_floor: max(var, ~1e-30) on the high word (doubles order like sign-magnitude integers,
+// a negative variance has the sign bit set), then the f32 bit pattern by re-biasing the exponent
+// and a funnel shift: truncation instead of rounding, a relative error < 2^-23 that is part of
+// the decision's relative margin (see below).
+__device__ __forceinline__ double u8_f64(uint32_t k) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)k), 4503599627370496.0);
+}
+__device__ __forceinline__ float f64_f32_floor(double var) {
+  const int hi = max(__double2hiint(var), 0x39B4484B);  // high word of 1e-30
+  return __uint_as_float(__funnelshift_l((uint32_t)__double2loint(var), (uint32_t)(hi - 0x38000000), 3));
+}
+
+// Relative f32 errors of one pixel's std~ and of the sums: truncation 2^-23, rsqrt.approx 2^-20
+// (budget), the fused multiply-add, the 8-term per-lane sum, 5 shuffle adds -- < 2e-6 in total;
+// scan_decide_plan budgets 8e-6.
+template <bool CLAMP>
+__device__ __forceinline__ void screen_px(uint32_t d, uint32_t g, double wm, double wg, double rn, double& S,
+                                          double& Q, float& as, float& ab, float mask, bool masked) {
+  double e = __dadd_rn(__dmul_rn(wm, u8_f64(d)), __dmul_rn(wg, u8_f64(g)));
+  if (CLAMP) e = e > 255.0 ? 255.0 : e;  // (never NaN)
+  S = __dadd_rn(S, e);
+  Q = __dadd_rn(Q, __dmul_rn(e, e));
+  const double m = __dmul_rn(S, rn);
+  const double var = __fma_rn(-m, m, __dmul_rn(Q, rn));
+  // std~ = v * rsqrt(v) (v > 0, so no 0 * inf); a variance <= 0 gives std~ ~ 1e-15 and the
+  // bound sqrt(delta), which covers the reference's std <= sqrt(delta) there
+  const float v = f64_f32_floor(var);
+  float rs;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(v));
+  if (masked) {
+    as = __fmaf_rn(__fmul_rn(v, rs), mask, as);
+    ab = __fmaf_rn(fminf(kScrCap, rs), mask, ab);
+  } else {
+    as = __fmaf_rn(v, rs, as);
+    ab = __fadd_rn(ab, fminf(kScrCap, rs));
+  }
+}
+
+// Every CTA of a window launch checks in once its sums (or leaf sums) are written -- also the
+// CTAs with nothing to do for this window's layout, so that no CTA can read the scan state
+// after it has been advanced.  True (block-uniform) for the last CTA of the grid.
+__device__ __forceinline__ bool scan_window_arrive(ScanState* S) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&S->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
+// one candidate frame for this thread's K full pixel pairs (no masks)
+template <bool CLAMP, int K>
+__device__ __forceinline__ void screen_frame_full(uint32_t a, double wm, double wg, double rn, double (&S)[8],
+                                                  double (&Q)[8], float& as, float& ab) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t w = lds_u32(a + 1024 * k);
+    screen_px<CLAMP>(__byte_perm(w, 0u, 0x4441), w & 255u, wm, wg, rn, S[2 * k], Q[2 * k], as, ab, 1.f, false);
+    screen_px<CLAMP>(w >> 24, __byte_perm(w, 0u, 0x4442), wm, wg, rn, S[2 * k + 1], Q[2 * k + 1], as, ab, 1.f, false);
+  }
+}
+
+template <bool CLAMP>
+__device__ __forceinline__ bool window_screen_body(const uint16_t* __restrict__ codes, long N, int chunk, int s,
+                                                   int n_acc, int L, int init, double wm0, double wg0,
+                                                   const double* ckS, const double* ckQ, double* ckSo,
+                                                   double* ckQo, double* asum, double* bsum, ScanState* Sg) {
+  extern __shared__ __align__(128) uint8_t st_ring[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(st_ring + kScrStages * kStatStageBytes);
+  float* red = reinterpret_cast<float*>(bars + kScrStages);             // [L][8 warps][2]
+  double* rns = reinterpret_cast<double*>(red + kScanMaxL * 8 * 2);      // [L]: RN(1 / n)
+  const long p0 = (long)blockIdx.x * chunk;
+  if (p0 >= N) return scan_window_arrive(Sg);
+  const int npx = (int)min((long)chunk, N - p0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // slot k of this warp covers chunk pixels [512 k + 64 warp, + 64): nfull slots are entirely
+  // inside the chunk (warp-uniform: 4 or 3 of them run the unmasked code), the next one may be
+  // partly inside (edge: masked), the rest are skipped
+  const int wb = 64 * warp;
+  const int nfull = npx >= wb + 64 ? min(kScrPairs, (npx - wb - 64) / 512 + 1) : 0;
+  const bool edge = nfull < kScrPairs && 512 * nfull + wb < npx;
+  const int i0e = 512 * nfull + 2 * (int)threadIdx.x - 64 * warp + wb;  // this thread's first edge-slot pixel
+  const float mk0 = edge && i0e < npx ? 1.f : 0.f, mk1 = edge && i0e + 1 < npx ? 1.f : 0.f;
+  auto slot_on = [&](int k) { return k < nfull || (k == nfull && edge); };
+  auto px_on = [&](int k, int u) { return k < nfull || (k == nfull && (u ? mk1 : mk0) != 0.f); };
+  const bool vec = ((N & 1) == 0) && ((reinterpret_cast<uintptr_t>(ckS) | reinterpret_cast<uintptr_t>(ckQ) |
+                                       reinterpret_cast<uintptr_t>(ckSo) | reinterpret_cast<uintptr_t>(ckQo)) &
+                                      15) == 0;
+  double S[2 * kScrPairs], Q[2 * kScrPairs];
+  // the checkpoint first: its loads are in flight while the ring is set up
+  if (!init) {
+#pragma unroll
+    for (int k = 0; k < kScrPairs; ++k) {
+      S[2 * k] = S[2 * k + 1] = Q[2 * k] = Q[2 * k + 1] = 0.0;
+      if (!slot_on(k)) continue;
+      const long p = p0 + 512 * k + 2 * (int)threadIdx.x;
+      if (k < nfull && vec) {
+        const double2 sv = *reinterpret_cast<const double2*>(ckS + p);
+        const double2 qv = *reinterpret_cast<const double2*>(ckQ + p);
+        S[2 * k] = sv.x, S[2 * k + 1] = sv.y, Q[2 * k] = qv.x, Q[2 * k + 1] = qv.y;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (px_on(k, u)) S[2 * k + u] = ckS[p + u], Q[2 * k + u] = ckQ[p + u];
+      }
+    }
+  }
+
+  const uint32_t bytes = (uint32_t)((npx * 2 + 15) & ~15);
+  const bool bulk = (N & 7) == 0;  // frame rows 16-byte aligned (chunk starts are multiples of 8)
+  const int M = L + (init ? 1 : 0);  // frames read: [s if init], s+n_acc .. s+n_acc+L-1
+  auto frame_of = [&](int i) { return init ? (i == 0 ? s : s + n_acc + i - 1) : s + n_acc + i; };
+  for (int c = threadIdx.x; c < L; c += blockDim.x) rns[c] = __ddiv_rn(1.0, (double)(n_acc + c + 1));
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kScrStages; ++k) mbar_init(&bars[k], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < M && i < kScrStages; ++i) {
+        mbar_arrive_tx(&bars[i], bytes);
+        bulk_g2s(st_ring + i * kStatStageBytes, codes + (size_t)frame_of(i) * N + p0, bytes, &bars[i]);
+      }
+    }
+  } else {
+    __syncthreads();
+  }
+  const uint32_t ring_s = smem_u32(st_ring) + 4 * threadIdx.x;
+  auto acquire = [&](int i) -> uint32_t {  // this thread's first pair in stage i
+    const int slot = i % kScrStages;
+    if (bulk) {
+      mbar_wait(&bars[slot], (uint32_t)(i / kScrStages) & 1u);
+    } else {
+      const uint16_t* src = codes + (size_t)frame_of(i) * N + p0;
+      uint16_t* st = reinterpret_cast<uint16_t*>(st_ring + slot * kStatStageBytes);
+      for (int q = threadIdx.x; q < npx; q += blockDim.x) st[q] = src[q];
+      __syncthreads();
+    }
+    return ring_s + slot * kStatStageBytes;
+  };
+  // stage i consumed.  A block barrier is only needed when the slot is refilled (windows longer
+  // than the ring): otherwise the warps run through the window's frames on their own, waiting
+  // only on the frames' copies.  (Plain fills: a thread refilling slot i has passed the barrier
+  // of acquire(i + kScrStages - 1), which every thread reaches after its frame i.)
+  auto release = [&](int i) {
+    if (bulk && i + kScrStages < M) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int j = i + kScrStages;
+        mbar_arrive_tx(&bars[j % kScrStages], bytes);
+        bulk_g2s(st_ring + (j % kScrStages) * kStatStageBytes, codes + (size_t)frame_of(j) * N + p0, bytes,
+                 &bars[j % kScrStages]);
+      }
+    }
+  };
+
+  int ci = 0;  // next stage
+  if (init) {
+    const uint32_t a = acquire(ci);
+    const bool pure0 = s == 0;  // (the clip's first frame is pure gradient: wm = 0, wg = 1)
+    const double wm = pure0 ? 0.0 : wm0, wg = pure0 ? 1.0 : wg0;
+#pragma unroll
+    for (int k = 0; k < kScrPairs; ++k) {
+      S[2 * k] = S[2 * k + 1] = Q[2 * k] = Q[2 * k + 1] = 0.0;
+      if (!slot_on(k)) continue;
+      const uint32_t w = lds_u32(a + 1024 * k);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t c16 = u ? w >> 16 : w & 0xffffu;
+        double e = __dadd_rn(__dmul_rn(wm, (double)(c16 >> 8)), __dmul_rn(wg, (double)(c16 & 255u)));
+        e = e > 255.0 ? 255.0 : e;
+        S[2 * k + u] = e;
+        Q[2 * k + u] = __dmul_rn(e, e);
+      }
+    }
+    release(ci++);
+  }
+
+  // (a candidate is never the clip's first frame: the scan state keeps n_acc >= 1, so the
+  // pure-gradient frame 0 only ever enters as a run's initial frame above)
+  SCPL_DCHECK(s + n_acc >= 1, "screened candidate at frame 0");
+  const double wm = wm0, wg = wg0;
+  const int path = nfull == kScrPairs ? 0 : (nfull == kScrPairs - 1 && !edge ? 1 : 2);
+  for (int c = 0; c < L; ++c, ++ci) {
+    const uint32_t a = acquire(ci);
+    const double rn = rns[c];
+    float as = 0.f, ab = 0.f;
+    if (path == 0) {
+      screen_frame_full<CLAMP, kScrPairs>(a, wm, wg, rn, S, Q, as, ab);
+    } else if (path == 1) {
+      screen_frame_full<CLAMP, kScrPairs - 1>(a, wm, wg, rn, S, Q, as, ab);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kScrPairs; ++k) {
+        if (!slot_on(k)) continue;
+        const uint32_t w = lds_u32(a + 1024 * k);
+        const bool m = k >= nfull;
+        screen_px<CLAMP>(__byte_perm(w, 0u, 0x4441), w & 255u, wm, wg, rn, S[2 * k], Q[2 * k], as, ab,
+                         m ? mk0 : 1.f, true);
+        screen_px<CLAMP>(w >> 24, __byte_perm(w, 0u, 0x4442), wm, wg, rn, S[2 * k + 1], Q[2 * k + 1], as, ab,
+                         m ? mk1 : 1.f, true);
+      }
+    }
+    release(ci);
+    // warp sums of (as, ab): lanes 0-15 fold as, lanes 16-31 fold ab
+    const bool hi = (lane & 16) != 0;
+    float x = hi ? ab : as;
+    const float y = hi ? as : ab;
+    x = __fadd_rn(x, __shfl_xor_sync(0xffffffffu, y, 16));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if ((lane & 15) == 0) red[(c * 8 + warp) * 2 + (lane >> 4)] = x;
+  }
+
+  __syncthreads();
+  for (int c = threadIdx.x; c < L; c += blockDim.x) {
+    double ds = 0.0, db = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      ds += (double)red[(c * 8 + w) * 2];
+      db += (double)red[(c * 8 + w) * 2 + 1];
+    }
+    atomicAdd(&asum[c], ds);
+    atomicAdd(&bsum[c], db * (double)kScanDelta);
+  }
+  // this CTA's sums are in: check in before the checkpoint stores (the deciding CTA only needs
+  // the sums; the stores are ordered before the next window by the kernel boundary)
+  const bool last = scan_window_arrive(Sg);
+  // checkpoint S,Q after n_acc + L frames
+#pragma unroll
+  for (int k = 0; k < kScrPairs; ++k) {
+    if (!slot_on(k)) continue;
+    const long p = p0 + 512 * k + 2 * (int)threadIdx.x;
+    if (k < nfull && vec) {
+      *reinterpret_cast<double2*>(ckSo + p) = make_double2(S[2 * k], S[2 * k + 1]);
+      *reinterpret_cast<double2*>(ckQo + p) = make_double2(Q[2 * k], Q[2 * k + 1]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (px_on(k, u)) ckSo[p + u] = S[2 * k + u], ckQo[p + u] = Q[2 * k + u];
+    }
+  }
+  return last;
+}
+
+__device__ __forceinline__ bool screen_noclamp(double wm, double wg) {
+  return wm >= 0.0 && wg >= 0.0 && __dadd_rn(__dmul_rn(wm, 255.0), __dmul_rn(wg, 255.0)) <= 255.0;
+}
+
 __global__ void __launch_bounds__(256, 3) window_stats_kernel(const uint16_t* __restrict__ codes, long N,
                                                            const int2* __restrict__ leaves, int nleaves,
                                                            int s, int n_acc, int L, int first_pure, int init,
@@ -321,17 +620,54 @@ __global__ void __launch_bounds__(256, 3) window_stats_kernel(const uint16_t* __
                            leafsum, nullptr, nullptr);
 }
 
-// Scan variant: the window comes from the device-side scan state (no host round trip).
+// Scan variant: the window comes from the device-side scan state (no host round trip).  The grid
+// covers both layouts (scan_grid): exact windows by leaves, screened windows by pixel chunks.
+__device__ void scan_window_finish(ScanState* S, int nleaves, const PwVnode* __restrict__ vnodes,
+                                   cudaGraphConditionalHandle loop, int in_graph, double* scratch);
 __global__ void __launch_bounds__(256, 4) window_stats_scan_kernel(ScanState* S,
-                                                                const int2* __restrict__ leaves, int nleaves) {
-  const int L = S->L;
+                                                                const int2* __restrict__ leaves, int nleaves,
+                                                                int chunk, const PwVnode* __restrict__ vnodes,
+                                                                cudaGraphConditionalHandle loop, int in_graph) {
+  extern __shared__ __align__(128) uint8_t st_ring[];
+  // the window, read once up front (one round trip; the deciding CTA rewrites the state only
+  // after every CTA of the grid has checked in)
+  const int L = S->L, approx = S->approx, exact = S->exact, s = S->s, n_acc = S->n_acc, init = S->init;
+  const long N = S->N;
+  const double wm = S->wm, wg = S->wg;
+  const uint16_t* codes = S->codes;
+  double *ckS = S->ckS, *ckQ = S->ckQ, *ckS2 = S->ckS2, *ckQ2 = S->ckQ2;
   if (L <= 0) return;
-  if (!S->approx || S->exact)
-    window_stats_body<false>(S->codes, S->N, leaves, nleaves, S->s, S->n_acc, L, 1, S->init, S->wm, S->wg, S->ckS,
-                             S->ckQ, S->ckS2, S->ckQ2, S->leafsum, nullptr, nullptr);
-  else
-    window_stats_body<true>(S->codes, S->N, leaves, nleaves, S->s, S->n_acc, L, 1, S->init, S->wm, S->wg, S->ckS,
-                            S->ckQ, S->ckS2, S->ckQ2, nullptr, S->asum, S->bsum);
+  const bool by_leaf = (long)blockIdx.x * (blockDim.x / kLeafLanes) < nleaves;
+  bool last;
+  if (!approx || exact) {
+    if (by_leaf)
+      window_stats_body<false>(codes, N, leaves, nleaves, s, n_acc, L, 1, init, wm, wg, ckS, ckQ, ckS2, ckQ2,
+                               S->leafsum, nullptr, nullptr);
+    last = scan_window_arrive(S);
+  } else if (chunk <= 0) {  // (SCPL_SCAN_LEAF_SCREEN=1: the leaf-layout screening body)
+    if (by_leaf)
+      window_stats_body<true>(codes, N, leaves, nleaves, s, n_acc, L, 1, init, wm, wg, ckS, ckQ, ckS2, ckQ2,
+                              nullptr, S->asum, S->bsum);
+    last = scan_window_arrive(S);
+  } else if (screen_noclamp(wm, wg)) {
+    last = window_screen_body<false>(codes, N, chunk, s, n_acc, L, init, wm, wg, ckS, ckQ, ckS2, ckQ2, S->asum,
+                                     S->bsum, S);
+  } else {
+    last = window_screen_body<true>(codes, N, chunk, s, n_acc, L, init, wm, wg, ckS, ckQ, ckS2, ckQ2, S->asum,
+                                    S->bsum, S);
+  }
+  if (last) scan_window_finish(S, nleaves, vnodes, loop, in_graph, reinterpret_cast<double*>(st_ring));
+}
+
+// grid of a scan window launch and the screened body's chunk (0: leaf-layout screening)
+static int scan_grid(long N, int nleaves, int& chunk) {
+  static const bool leaf_screen = getenv("SCPL_SCAN_LEAF_SCREEN") != nullptr;  // (experiments)
+  int dev = 0, sms = 0;
+  SCPL_CUDA(cudaGetDevice(&dev));
+  SCPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  chunk = leaf_screen ? 0 : screen_chunk(N, sms);
+  const int by_leaves = cdiv((long)nleaves * kLeafLanes, 256);
+  return chunk > 0 ? std::max(by_leaves, (int)cdiv(N, (long)chunk)) : by_leaves;
 }
 
 static void stats_smem_attr() {
@@ -346,7 +682,7 @@ static void stats_smem_attr() {
 // candidate each fold one complete subtree of depth kPwDepth - kPwTop to a partial; the
 // root folds the kPwFoldCtas partials (again a complete tree, so the bracketing is numpy's).
 __device__ double pw_eval(long n, const double* __restrict__ ls, int& li) {
-  if (n <= 128) return ls[li++];
+  if (n <= 128) return __ldcg(&ls[li++]);  // (L2: the fused tail reads other CTAs' leaf sums)
   long h = n / 2;
   h -= h % 8;
   double a = pw_eval(h, ls, li);
@@ -356,19 +692,10 @@ __device__ double pw_eval(long n, const double* __restrict__ ls, int& li) {
 
 constexpr int kPwSub = (1 << kPwDepth) / kPwFoldCtas;  // vnodes per CTA
 
-// grid (kPwFoldCtas, L or max L); Lp (device) overrides the candidate count when given
-__global__ void __launch_bounds__(256) fold_partial_kernel(const double* leafsum, int nleaves,
-                                                           const PwVnode* __restrict__ vnodes, double* partial,
-                                                           const ScanState* Sp) {
-  __shared__ double v[kPwSub];
-  const int c = blockIdx.y;
-  if (Sp != nullptr) {
-    if (c >= Sp->L || (Sp->approx && !Sp->exact)) return;  // a screened window needs no fold
-    leafsum = Sp->leafsum;
-    partial = Sp->partial;
-  }
-  const double* ls = leafsum + (size_t)c * nleaves;
-  const int v0 = blockIdx.x * kPwSub;
+// one subtree (fold CTA index b) of candidate sums ls folded in v[kPwSub] (shared); returns the
+// subtree's sum in v[0] (valid for thread 0 after the last barrier)
+__device__ __forceinline__ void fold_subtree(const double* ls, const PwVnode* __restrict__ vnodes, int b, double* v) {
+  const int v0 = b * kPwSub;
   for (int t = threadIdx.x; t < kPwSub; t += blockDim.x) {
     PwVnode vn = vnodes[v0 + t];
     double x = 0.0;
@@ -385,6 +712,14 @@ __global__ void __launch_bounds__(256) fold_partial_kernel(const double* leafsum
       v[2 * t * s] = __dadd_rn(v[2 * t * s], v[2 * t * s + s]);
     __syncthreads();
   }
+}
+
+// grid (kPwFoldCtas, L)
+__global__ void __launch_bounds__(256) fold_partial_kernel(const double* leafsum, int nleaves,
+                                                           const PwVnode* __restrict__ vnodes, double* partial) {
+  __shared__ double v[kPwSub];
+  const int c = blockIdx.y;
+  fold_subtree(leafsum + (size_t)c * nleaves, vnodes, blockIdx.x, v);
   if (threadIdx.x == 0) partial[(size_t)c * kPwFoldCtas + blockIdx.x] = v[0];
 }
 
@@ -406,7 +741,7 @@ __global__ void fold_root_kernel(const double* __restrict__ partial, int L, long
 
 void launch_pairwise_fold(const double* leafsum, int nleaves, const PwVnode* vnodes, long N, int L,
                           double* partial, double* out, cudaStream_t st) {
-  fold_partial_kernel<<<dim3(kPwFoldCtas, L), 256, 0, st>>>(leafsum, nleaves, vnodes, partial, nullptr);
+  fold_partial_kernel<<<dim3(kPwFoldCtas, L), 256, 0, st>>>(leafsum, nleaves, vnodes, partial);
   SCPL_CHECK_LAUNCH();
   fold_root_kernel<<<cdiv(L, 64), 64, 0, st>>>(partial, L, N, out);
   SCPL_CHECK_LAUNCH();
@@ -465,16 +800,12 @@ __device__ void scan_plan(ScanState* S) {
   S->L = 0;
 }
 
-// One thread per candidate folds its root; thread 0 then decides and plans the next window.
-__global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, int decide, int in_graph) {
-  __shared__ double asde[kScanMaxL];
+// Thread 0 of the deciding CTA: consume the window's results (asde[c]: exact ASDEs of an exact
+// window), decide, plan the next window and set the loop condition.
+__device__ void scan_decide_plan(ScanState* S, const double* asde, cudaGraphConditionalHandle loop, int decide,
+                                 int in_graph) {
   const int L = S->L;
   const bool exact = !S->approx || S->exact;
-  if (decide && L > 0 && exact) {
-    for (int c = threadIdx.x; c < L; c += blockDim.x) asde[c] = fold_root(S->partial, c, S->N);
-    __syncthreads();
-  }
-  if (threadIdx.x != 0) return;
   if (decide && L > 0) {
     int breach = -1;
     if (exact) {
@@ -489,11 +820,14 @@ __global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, 
       // |asde~ - asde| <= marg (kScanDelta's per-pixel bounds, the relative f32 roundings of
       // std~ with a 5x margin, and the reference's own fp64 rounding) the test is settled
       // when asde~ + marg < phi or asde~ - marg > phi.  Otherwise re-run the window exactly.
+      // (asum / bsum: other CTAs' atomics, read past L1)
+      const volatile double* asum = S->asum;
+      const volatile double* bsum = S->bsum;
       const double invN = 1.0 / (double)S->N;
       bool unsure = S->force_fallback != 0;
       for (int c = 0; c < L && !unsure; ++c) {
-        const double a = S->asum[c] * invN;
-        const double marg = 2.0 * S->bsum[c] * invN + 8e-6 * a + 1e-9;
+        const double a = asum[c] * invN;
+        const double marg = 2.0 * bsum[c] * invN + 8e-6 * a + 1e-9;
         const double phi = S->phi[S->n_acc + c + 1];
         if (a + marg < phi) continue;
         if (a - marg > phi) {
@@ -535,22 +869,51 @@ __global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, 
   if (in_graph) cudaGraphSetConditional(loop, S->L > 0 ? 1u : 0u);
 }
 
+// The head of a scan launch: plan the first window of the chunk.
+__global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, int in_graph) {
+  if (threadIdx.x == 0) scan_decide_plan(S, nullptr, loop, 0, in_graph);
+}
+
+// The deciding CTA of a window launch (scan_window_arrive): folds an exact window's leaf sums
+// (one CTA: exact windows are the rare fallback), decides and plans -- the loop body is ONE
+// kernel, no fold / step launches per window.
+__device__ void scan_window_finish(ScanState* S, int nleaves, const PwVnode* __restrict__ vnodes,
+                                   cudaGraphConditionalHandle loop, int in_graph, double* scratch) {
+  __shared__ double asde[kScanMaxL];
+  __syncthreads();  // (the ring is free: scratch)
+  __threadfence();
+  const int L = S->L;
+  if (!S->approx || S->exact) {
+    for (int c = 0; c < L; ++c)
+      for (int b = 0; b < kPwFoldCtas; ++b) {
+        fold_subtree(S->leafsum + (size_t)c * nleaves, vnodes, b, scratch);
+        if (threadIdx.x == 0) S->partial[(size_t)c * kPwFoldCtas + b] = scratch[0];
+        __syncthreads();
+      }
+    for (int c = threadIdx.x; c < L; c += blockDim.x) asde[c] = fold_root(S->partial, c, S->N);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    S->ticket = 0;
+    scan_decide_plan(S, asde, loop, 1, in_graph);
+  }
+}
+
 __global__ void scan_reset_kernel(ScanState* S, ScanState init) { *S = init; }
 __global__ void scan_avail_kernel(ScanState* S, int avail) { S->avail = avail; }
 
-// graph: step(plan) -> while (L > 0) { stats -> fold partials -> step(decide + plan) }
-cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes,
-                                 int spec) {
+// graph: step(plan) -> while (L > 0) { window statistics; its last CTA decides and plans }
+cudaGraphExec_t build_scan_graph(ScanState* S, long N, const int2* leaves, int nleaves, const PwVnode* vnodes,
+                                 int spec, int prio) {
   SCPL_ARG(spec >= 1 && spec <= 64, "spec_len must be in 1..64");
   cudaGraph_t g;
   SCPL_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
   SCPL_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-  cudaStream_t cs;
-  SCPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaStream_t cs = capture_stream(prio);
   // head: plan
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 0, 1);
+  scan_step_kernel<<<1, 32, 0, cs>>>(S, h, 1);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   SCPL_CUDA(cudaStreamEndCapture(cs, &g));
   cudaGraphNode_t head;
@@ -566,14 +929,14 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   stats_smem_attr();
-  window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem + spec * kStatRed, cs>>>(
-      S, leaves, nleaves);
-  SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
-  fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, cs>>>(nullptr, nleaves, vnodes, nullptr, S);
-  SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
-  scan_step_kernel<<<1, 64, 0, cs>>>(S, h, 1, 1);
+  int chunk = 0;
+  const int grid = scan_grid(N, nleaves, chunk);
+  const size_t smem = std::max(kStatSmem + spec * kStatRed, kScrSmem);
+  window_stats_scan_kernel<<<grid, 256, smem, cs>>>(S, leaves, nleaves, chunk, vnodes, h, 1);
   SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
+  graph_set_priority(g, prio);
+  graph_set_priority(body, prio);
   cudaGraphExec_t ex;
   SCPL_CUDA(cudaGraphInstantiate(&ex, g, 0));
   cudaGraphDestroy(g);
@@ -583,22 +946,20 @@ cudaGraphExec_t build_scan_graph(ScanState* S, const int2* leaves, int nleaves, 
 
 // Host-driven equivalent of one scan graph launch (SCPL_HOST_LOOPS: profiling, where the
 // conditional graph would hide the kernels from the profiler): the host reads L back.
-void run_scan_host(ScanState* S, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec, int* h_L,
+void run_scan_host(ScanState* S, long N, const int2* leaves, int nleaves, const PwVnode* vnodes, int spec, int* h_L,
                    cudaStream_t st) {
-  scan_step_kernel<<<1, 64, 0, st>>>(S, 0, 0, 0);
+  scan_step_kernel<<<1, 32, 0, st>>>(S, 0, 0);
   SCPL_CHECK_LAUNCH();
   stats_smem_attr();
+  int chunk = 0;
+  const int grid = scan_grid(N, nleaves, chunk);
+  const size_t smem = std::max(kStatSmem + spec * kStatRed, kScrSmem);
   while (true) {
     SCPL_CUDA(cudaMemcpyAsync(h_L, reinterpret_cast<uint8_t*>(S) + offsetof(ScanState, L), sizeof(int),
                               cudaMemcpyDeviceToHost, st));
     SCPL_CUDA(cudaStreamSynchronize(st));
     if (*h_L <= 0) break;
-    window_stats_scan_kernel<<<cdiv((long)nleaves * kLeafLanes, 256), 256, kStatSmem + spec * kStatRed, st>>>(
-        S, leaves, nleaves);
-    SCPL_CHECK_LAUNCH();
-    fold_partial_kernel<<<dim3(kPwFoldCtas, spec), 256, 0, st>>>(nullptr, nleaves, vnodes, nullptr, S);
-    SCPL_CHECK_LAUNCH();
-    scan_step_kernel<<<1, 64, 0, st>>>(S, 0, 1, 0);
+    window_stats_scan_kernel<<<grid, 256, smem, st>>>(S, leaves, nleaves, chunk, vnodes, 0, 0);
     SCPL_CHECK_LAUNCH();
   }
 }
