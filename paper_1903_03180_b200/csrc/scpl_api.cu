@@ -1034,7 +1034,9 @@ void retarget_jobs(scpl_ctx* ctx, std::vector<ClipJob>& jobs, int T, int h, int 
   // chunks of 16 frames: a host clip's copies overlap its codes and scan, and a single clip's
   // runs reach the carve while its scan goes on; a batch of device clips is scanned clip by clip
   // in one piece (other clips' runs keep the carve busy; a chunk costs host API calls per clip)
-  const int chunk = (njobs > 1 && !host_in) ? std::max(T, 1) : 16;
+  // SCPL_CHUNK=N (experiments): frames per chunk of a single / host clip
+  static const int chunk_env = getenv("SCPL_CHUNK") ? std::max(1, atoi(getenv("SCPL_CHUNK"))) : 0;
+  const int chunk = (njobs > 1 && !host_in) ? std::max(T, 1) : (chunk_env > 0 ? std::min(chunk_env, std::max(T, 1)) : 16);
   const int nchunk = (T + chunk - 1) / chunk;
   if (buffered && !given) upload_phi(ctx, P);
 

@@ -13,6 +13,7 @@
 // candidates.  A second kernel folds the leaf sums with the same tree (one CTA per
 // candidate).  The per-pixel S,Q after the chunk are checkpointed so the next chunk of
 // the same run resumes without re-reading earlier frames.
+#include <cmath>
 #include <cstddef>
 #include <vector>
 
@@ -607,7 +608,8 @@ __device__ __forceinline__ bool window_screen_body(const uint16_t* __restrict__ 
 }
 
 __device__ __forceinline__ bool screen_noclamp(double wm, double wg) {
-  return wm >= 0.0 && wg >= 0.0 && __dadd_rn(__dmul_rn(wm, 255.0), __dmul_rn(wg, 255.0)) <= 255.0;
+  return __double2hiint(wm) >= 0 && __double2hiint(wg) >= 0 &&
+         __dadd_rn(__dmul_rn(wm, 255.0), __dmul_rn(wg, 255.0)) <= 255.0;  // (false for NaN weights)
 }
 
 __global__ void __launch_bounds__(256, 3) window_stats_kernel(const uint16_t* __restrict__ codes, long N,
@@ -1020,8 +1022,13 @@ __device__ __forceinline__ double energy_fp64(uint32_t code, bool pure, double w
   if (pure) return (double)g;
   return fmin(__dadd_rn(__dmul_rn(wm, (double)(code >> 8)), __dmul_rn(wg, (double)g)), 255.0);
 }
+// CLAMP = false (wm, wg non-negative with fl(fl(255 wm) + fl(255 wg)) <= 255, uniform_noclamp):
+// min(e, 255) is a no-op and every e is >= +0.0, so the sum may start from +0.0 (0 + e == e bit
+// for bit); bytes become doubles on the fp64 pipe (u8_f64) -- 8 instructions per pixel and
+// frame instead of 16.  A pure-gradient frame (the clip's first) is wm = 0, wg = 1.
+template <bool CLAMP>
 __global__ void __launch_bounds__(256, 4) uniform_vec_kernel(const uint16_t* __restrict__ codes, int H, int W, int s,
-                                                          int n, int first_pure, double wm, double wg,
+                                                          int n, int first_pure, double wm0, double wg0,
                                                           double* __restrict__ out, int pitch) {
   const long N = (long)H * W;
   const long q = blockIdx.x * (long)blockDim.x + threadIdx.x;  // 8-pixel group
@@ -1030,6 +1037,8 @@ __global__ void __launch_bounds__(256, 4) uniform_vec_kernel(const uint16_t* __r
   const uint4* src = reinterpret_cast<const uint4*>(codes + (size_t)s * N + p);
   const size_t fstride = (size_t)N / kUniPx;  // uint4 per frame
   double acc[kUniPx];
+#pragma unroll
+  for (int k = 0; k < kUniPx; ++k) acc[k] = 0.0;
   // frames in chunks of 4 with every load of a chunk in flight (a short run is one or two round
   // trips), then the sequential fp64 sum in frame order (buffering.py:69-71)
   const bool pure0 = first_pure && s == 0;
@@ -1043,10 +1052,22 @@ __global__ void __launch_bounds__(256, 4) uniform_vec_kernel(const uint16_t* __r
       if (t0 + u >= n) break;
       const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
       const bool pure = pure0 && t0 + u == 0;
+      if (CLAMP) {
 #pragma unroll
-      for (int k = 0; k < kUniPx; ++k) {
-        const double e = energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, pure, wm, wg);
-        acc[k] = t0 + u == 0 ? e : __dadd_rn(acc[k], e);
+        for (int k = 0; k < kUniPx; ++k) {
+          const double e = energy_fp64((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu, pure, wm0, wg0);
+          acc[k] = t0 + u == 0 ? e : __dadd_rn(acc[k], e);
+        }
+      } else {
+        const double wm = pure ? 0.0 : wm0, wg = pure ? 1.0 : wg0;
+#pragma unroll
+        for (int k = 0; k < kUniPx; k += 2) {
+          const uint32_t w = w4[k >> 1];
+          const double e0 = __dadd_rn(__dmul_rn(wm, u8_f64(__byte_perm(w, 0u, 0x4441))), __dmul_rn(wg, u8_f64(w & 255u)));
+          const double e1 = __dadd_rn(__dmul_rn(wm, u8_f64(w >> 24)), __dmul_rn(wg, u8_f64(__byte_perm(w, 0u, 0x4442))));
+          acc[k] = __dadd_rn(acc[k], e0);
+          acc[k + 1] = __dadd_rn(acc[k + 1], e1);
+        }
       }
     }
   }
@@ -1057,13 +1078,25 @@ __global__ void __launch_bounds__(256, 4) uniform_vec_kernel(const uint16_t* __r
   for (int k = 0; k < kUniPx; k += 2) o[k / 2] = make_double2(__ddiv_rn(acc[k], dn), __ddiv_rn(acc[k + 1], dn));
 }
 
+// wm, wg with a clear sign bit and fl(fl(255 wm) + fl(255 wg)) <= 255 (separate roundings, as the
+// device computes e): rounding is monotone, so no e exceeds 255 and none is -0.0
+static bool uniform_noclamp(double wm, double wg) {
+  if (std::signbit(wm) || std::signbit(wg) || !(wm == wm) || !(wg == wg)) return false;
+  volatile double a = wm * 255.0, b = wg * 255.0;
+  volatile double c = a + b;
+  return c <= 255.0;
+}
+
 void launch_uniform(const uint16_t* codes, int H, int W, int s, int n, int first_pure, double wm, double wg,
                     int transposed, double* out, cudaStream_t st, int pitch) {
   if (pitch <= 0) pitch = transposed ? H : W;
   const long N = (long)H * W;
   if (!transposed && W % kUniPx == 0 && pitch % 2 == 0 && (reinterpret_cast<uintptr_t>(codes) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-    uniform_vec_kernel<<<cdiv(N / kUniPx, 256), 256, 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, out, pitch);
+    if (uniform_noclamp(wm, wg))
+      uniform_vec_kernel<false><<<cdiv(N / kUniPx, 256), 256, 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, out, pitch);
+    else
+      uniform_vec_kernel<true><<<cdiv(N / kUniPx, 256), 256, 0, st>>>(codes, H, W, s, n, first_pure, wm, wg, out, pitch);
     SCPL_CHECK_LAUNCH();
     return;
   }
