@@ -276,9 +276,11 @@ void scan_start(scpl_ctx* ctx, ScanStream& S, ScanLane& lane, const uint16_t* co
                 const scpl_video_params& P, cudaStream_t st) {
   const long N = (long)H * W;
   const PwPlan& plan = plan_for(ctx, N);
-  // candidates per scan window (speculation length): params, else SCPL_SPEC (experiments), else 8
+  // candidates per scan window (speculation length): params, else SCPL_SPEC (experiments), else 16
+  // (a window's fixed cost -- launch, checkpoint, decision -- is ~7 candidates' worth of work; a
+  // run's first window is still capped by the previous run's length)
   static const int spec_env = getenv("SCPL_SPEC") ? atoi(getenv("SCPL_SPEC")) : 0;
-  const int spec = P.spec_len > 0 ? P.spec_len : (spec_env > 0 ? spec_env : 8);
+  const int spec = P.spec_len > 0 ? P.spec_len : (spec_env > 0 ? spec_env : 16);
   SCPL_ARG(spec <= 64, "spec_len must be <= 64");
   if (!lane.scan) SCPL_CUDA(cudaMalloc(&lane.scan, sizeof(ScanState)));
   auto key = std::make_tuple(N, spec, (const void*)lane.scan);

@@ -802,10 +802,23 @@ __device__ void scan_plan(ScanState* S) {
   S->L = 0;
 }
 
+// Screened window, candidate c: the reference accepts it iff asde(c) <= phi; with
+// |asde~ - asde| <= marg (kScanDelta's per-pixel bounds, the relative f32 roundings of std~
+// with a 4x margin, and the reference's own fp64 rounding) the test is settled when
+// asde~ + marg < phi (0: accepted) or asde~ - marg > phi (1: breach); otherwise 2 (the window
+// is re-run exactly).  asum / bsum are other CTAs' atomics, read past L1.
+__device__ __forceinline__ int scan_screen_status(const ScanState* S, int c) {
+  const double invN = 1.0 / (double)S->N;
+  const double a = *(const volatile double*)&S->asum[c] * invN;
+  const double marg = 2.0 * *(const volatile double*)&S->bsum[c] * invN + 8e-6 * a + 1e-9;
+  const double phi = S->phi[S->n_acc + c + 1];
+  return a + marg < phi ? 0 : (a - marg > phi ? 1 : 2);
+}
+
 // Thread 0 of the deciding CTA: consume the window's results (asde[c]: exact ASDEs of an exact
 // window), decide, plan the next window and set the loop condition.
-__device__ void scan_decide_plan(ScanState* S, const double* asde, cudaGraphConditionalHandle loop, int decide,
-                                 int in_graph) {
+__device__ void scan_decide_plan(ScanState* S, const double* asde, const int* status,
+                                 cudaGraphConditionalHandle loop, int decide, int in_graph) {
   const int L = S->L;
   const bool exact = !S->approx || S->exact;
   if (decide && L > 0) {
@@ -818,21 +831,12 @@ __device__ void scan_decide_plan(ScanState* S, const double* asde, cudaGraphCond
         }
       }
     } else {
-      // screened window: the reference accepts candidate c iff asde(c) <= phi; with
-      // |asde~ - asde| <= marg (kScanDelta's per-pixel bounds, the relative f32 roundings of
-      // std~ with a 5x margin, and the reference's own fp64 rounding) the test is settled
-      // when asde~ + marg < phi or asde~ - marg > phi.  Otherwise re-run the window exactly.
-      // (asum / bsum: other CTAs' atomics, read past L1)
-      const volatile double* asum = S->asum;
-      const volatile double* bsum = S->bsum;
-      const double invN = 1.0 / (double)S->N;
+      // screened window: status[c] (scan_screen_status, evaluated by the CTA's threads in
+      // parallel) is 0 = accepted, 1 = breach, 2 = the bound cannot settle the threshold test
       bool unsure = S->force_fallback != 0;
       for (int c = 0; c < L && !unsure; ++c) {
-        const double a = asum[c] * invN;
-        const double marg = 2.0 * bsum[c] * invN + 8e-6 * a + 1e-9;
-        const double phi = S->phi[S->n_acc + c + 1];
-        if (a + marg < phi) continue;
-        if (a - marg > phi) {
+        if (status[c] == 0) continue;
+        if (status[c] == 1) {
           breach = c;
           break;
         }
@@ -873,7 +877,7 @@ __device__ void scan_decide_plan(ScanState* S, const double* asde, cudaGraphCond
 
 // The head of a scan launch: plan the first window of the chunk.
 __global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, int in_graph) {
-  if (threadIdx.x == 0) scan_decide_plan(S, nullptr, loop, 0, in_graph);
+  if (threadIdx.x == 0) scan_decide_plan(S, nullptr, nullptr, loop, 0, in_graph);
 }
 
 // The deciding CTA of a window launch (scan_window_arrive): folds an exact window's leaf sums
@@ -882,6 +886,7 @@ __global__ void scan_step_kernel(ScanState* S, cudaGraphConditionalHandle loop, 
 __device__ void scan_window_finish(ScanState* S, int nleaves, const PwVnode* __restrict__ vnodes,
                                    cudaGraphConditionalHandle loop, int in_graph, double* scratch) {
   __shared__ double asde[kScanMaxL];
+  __shared__ int status[kScanMaxL];
   __syncthreads();  // (the ring is free: scratch)
   __threadfence();
   const int L = S->L;
@@ -893,11 +898,13 @@ __device__ void scan_window_finish(ScanState* S, int nleaves, const PwVnode* __r
         __syncthreads();
       }
     for (int c = threadIdx.x; c < L; c += blockDim.x) asde[c] = fold_root(S->partial, c, S->N);
-    __syncthreads();
+  } else {  // one thread per candidate: the loads of the sums and thresholds in parallel
+    for (int c = threadIdx.x; c < L; c += blockDim.x) status[c] = scan_screen_status(S, c);
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     S->ticket = 0;
-    scan_decide_plan(S, asde, loop, 1, in_graph);
+    scan_decide_plan(S, asde, status, loop, 1, in_graph);
   }
 }
 
