@@ -91,7 +91,7 @@ constexpr int kStatStageBytes = (256 / kLeafLanes) * 128 * 2;  // one CTA's pixe
 // candidate and warp (kStatRed per candidate).  ~21 KB at spec 8: a scan CTA fits on an SM
 // next to a resident carve-pass CTA.
 constexpr size_t kStatSmem = (size_t)kStatStages * kStatStageBytes + 8 * kStatStages + 2 * 256 * sizeof(double) +
-                             kScanMaxL * sizeof(double);  // (+ the screened body's 1 / n table)
+                             kScanMaxL * sizeof(double) + 64;  // (+ slot / window counters)  // (+ the screened body's 1 / n table)
 constexpr size_t kStatRed = 16 * sizeof(double);
 
 // numpy's leaf sum (pairwise_sum, n <= 128): r[j] = a[j] + a[j+8] + ... (sequential), then
@@ -337,7 +337,7 @@ constexpr float kScrCap = 70715.0f;                   // kScanSqrtDelta / kScanD
 // 2d: SMs active 75% of the time, issue slots 50%, DRAM 18%), so nothing waits on a refill.
 constexpr int kScrStages = 8;
 constexpr size_t kScrSmem = (size_t)kScrStages * kStatStageBytes + 8 * kScrStages + kScanMaxL * 8 * 2 * sizeof(float) +
-                            kScanMaxL * sizeof(double);
+                            kScanMaxL * sizeof(double) + 64;  // (+ slot / window counters)
 static_assert(kScrMaxChunk * 2 <= kStatStageBytes, "a chunk's codes of one frame fit a ring stage");
 
 // CTAs' pixels for a frame of N pixels: the smallest whole number of waves (4 CTAs per SM)
@@ -412,6 +412,8 @@ __device__ __forceinline__ bool scan_window_arrive(ScanState* S) {
   return s_last != 0;
 }
 
+__device__ void scan_screen_finish_warp(ScanState* S, cudaGraphConditionalHandle loop, int in_graph);
+
 // one candidate frame for this thread's K full pixel pairs (no masks)
 template <bool CLAMP, int K>
 __device__ __forceinline__ void screen_frame_full(uint32_t a, double wm, double wg, double rn, double (&S)[8],
@@ -428,11 +430,14 @@ template <bool CLAMP>
 __device__ __forceinline__ bool window_screen_body(const uint16_t* __restrict__ codes, long N, int chunk, int s,
                                                    int n_acc, int L, int init, double wm0, double wg0,
                                                    const double* ckS, const double* ckQ, double* ckSo,
-                                                   double* ckQo, double* asum, double* bsum, ScanState* Sg) {
+                                                   double* ckQo, double* asum, double* bsum, ScanState* Sg,
+                                                   cudaGraphConditionalHandle loop, int in_graph) {
   extern __shared__ __align__(128) uint8_t st_ring[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(st_ring + kScrStages * kStatStageBytes);
   float* red = reinterpret_cast<float*>(bars + kScrStages);             // [L][8 warps][2]
   double* rns = reinterpret_cast<double*>(red + kScanMaxL * 8 * 2);      // [L]: RN(1 / n)
+  int* cnt = reinterpret_cast<int*>(rns + kScanMaxL);                    // [stages]: warps done with a slot
+  int* done = cnt + kScrStages;                                          // warps done with the window
   const long p0 = (long)blockIdx.x * chunk;
   if (p0 >= N) return scan_window_arrive(Sg);
   const int npx = (int)min((long)chunk, N - p0);
@@ -475,6 +480,7 @@ __device__ __forceinline__ bool window_screen_body(const uint16_t* __restrict__ 
   const int M = L + (init ? 1 : 0);  // frames read: [s if init], s+n_acc .. s+n_acc+L-1
   auto frame_of = [&](int i) { return init ? (i == 0 ? s : s + n_acc + i - 1) : s + n_acc + i; };
   for (int c = threadIdx.x; c < L; c += blockDim.x) rns[c] = __ddiv_rn(1.0, (double)(n_acc + c + 1));
+  if (threadIdx.x <= kScrStages) cnt[threadIdx.x] = 0;  // (cnt[kScrStages] is `done`)
   if (bulk) {
     if (threadIdx.x == 0) {
       for (int k = 0; k < kScrStages; ++k) mbar_init(&bars[k], 1);
@@ -503,18 +509,26 @@ __device__ __forceinline__ bool window_screen_body(const uint16_t* __restrict__ 
     }
     return ring_s + slot * kStatStageBytes;
   };
-  // stage i consumed.  A block barrier is only needed when the slot is refilled (windows longer
-  // than the ring): otherwise the warps run through the window's frames on their own, waiting
-  // only on the frames' copies.  (Plain fills: a thread refilling slot i has passed the barrier
-  // of acquire(i + kScrStages - 1), which every thread reaches after its frame i.)
+  // stage i consumed.  No block barrier anywhere in the window: a slot that is needed again
+  // (windows longer than the ring) is refilled by the LAST warp to finish with it (a shared
+  // counter per slot), so the warps run through the window's frames on their own, waiting only
+  // on the frames' copies.  (Plain fills: a thread refilling slot i has passed the barrier of
+  // acquire(i + kScrStages - 1), which every thread reaches after its frame i.)
+  const int nwarps = (int)(blockDim.x >> 5);
   auto release = [&](int i) {
     if (bulk && i + kScrStages < M) {
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int j = i + kScrStages;
-        mbar_arrive_tx(&bars[j % kScrStages], bytes);
-        bulk_g2s(st_ring + (j % kScrStages) * kStatStageBytes, codes + (size_t)frame_of(j) * N + p0, bytes,
-                 &bars[j % kScrStages]);
+      __syncwarp();
+      if (lane == 0) {
+        const int slot = i % kScrStages;
+        __threadfence_block();
+        if (atomicAdd(&cnt[slot], 1) == nwarps - 1) {
+          cnt[slot] = 0;
+          __threadfence_block();
+          fence_proxy_async();  // (the warps' reads of the slot before the async refill)
+          const int j = i + kScrStages;
+          mbar_arrive_tx(&bars[slot], bytes);
+          bulk_g2s(st_ring + slot * kStatStageBytes, codes + (size_t)frame_of(j) * N + p0, bytes, &bars[slot]);
+        }
       }
     }
   };
@@ -577,19 +591,37 @@ __device__ __forceinline__ bool window_screen_body(const uint16_t* __restrict__ 
     if ((lane & 15) == 0) red[(c * 8 + warp) * 2 + (lane >> 4)] = x;
   }
 
-  __syncthreads();
-  for (int c = threadIdx.x; c < L; c += blockDim.x) {
-    double ds = 0.0, db = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      ds += (double)red[(c * 8 + w) * 2];
-      db += (double)red[(c * 8 + w) * 2 + 1];
-    }
-    atomicAdd(&asum[c], ds);
-    atomicAdd(&bsum[c], db * (double)kScanDelta);
+  // The last warp of the CTA to finish the window adds the CTA's sums to the global ones and
+  // checks the CTA in (scan_window_arrive's ticket); every warp then stores its checkpoint (the
+  // deciding warp only needs the sums; the stores are ordered before the next window by the
+  // kernel boundary).  The last warp of the last CTA decides and plans.
+  __syncwarp();
+  int flag = 0;
+  if (lane == 0) {
+    __threadfence_block();
+    flag = atomicAdd(done, 1) == nwarps - 1;
   }
-  // this CTA's sums are in: check in before the checkpoint stores (the deciding CTA only needs
-  // the sums; the stores are ordered before the next window by the kernel boundary)
-  const bool last = scan_window_arrive(Sg);
+  const bool cta_last = __shfl_sync(0xffffffffu, flag, 0) != 0;
+  bool grid_last = false;
+  if (cta_last) {
+    __threadfence_block();
+    for (int c = lane; c < L; c += 32) {
+      double ds = 0.0, db = 0.0;
+      for (int w = 0; w < nwarps; ++w) {
+        ds += (double)red[(c * 8 + w) * 2];
+        db += (double)red[(c * 8 + w) * 2 + 1];
+      }
+      atomicAdd(&asum[c], ds);
+      atomicAdd(&bsum[c], db * (double)kScanDelta);
+    }
+    __syncwarp();
+    flag = 0;
+    if (lane == 0) {
+      __threadfence();
+      flag = atomicAdd(&Sg->ticket, 1u) == gridDim.x - 1;
+    }
+    grid_last = __shfl_sync(0xffffffffu, flag, 0) != 0;
+  }
   // checkpoint S,Q after n_acc + L frames
 #pragma unroll
   for (int k = 0; k < kScrPairs; ++k) {
@@ -604,7 +636,8 @@ __device__ __forceinline__ bool window_screen_body(const uint16_t* __restrict__ 
         if (px_on(k, u)) ckSo[p + u] = S[2 * k + u], ckQo[p + u] = Q[2 * k + u];
     }
   }
-  return last;
+  if (grid_last) scan_screen_finish_warp(Sg, loop, in_graph);
+  return false;  // (decided here if this was the last CTA)
 }
 
 __device__ __forceinline__ bool screen_noclamp(double wm, double wg) {
@@ -653,10 +686,10 @@ __global__ void __launch_bounds__(256, 4) window_stats_scan_kernel(ScanState* S,
     last = scan_window_arrive(S);
   } else if (screen_noclamp(wm, wg)) {
     last = window_screen_body<false>(codes, N, chunk, s, n_acc, L, init, wm, wg, ckS, ckQ, ckS2, ckQ2, S->asum,
-                                     S->bsum, S);
+                                     S->bsum, S, loop, in_graph);
   } else {
     last = window_screen_body<true>(codes, N, chunk, s, n_acc, L, init, wm, wg, ckS, ckQ, ckS2, ckQ2, S->asum,
-                                    S->bsum, S);
+                                    S->bsum, S, loop, in_graph);
   }
   if (last) scan_window_finish(S, nleaves, vnodes, loop, in_graph, reinterpret_cast<double*>(st_ring));
 }
@@ -905,6 +938,20 @@ __device__ void scan_window_finish(ScanState* S, int nleaves, const PwVnode* __r
   if (threadIdx.x == 0) {
     S->ticket = 0;
     scan_decide_plan(S, asde, status, loop, 1, in_graph);
+  }
+}
+
+// The same for a screened window decided by ONE warp (the last warp of the last CTA to finish:
+// window_screen_body has no block barriers): a lane per candidate evaluates the threshold tests.
+__device__ void scan_screen_finish_warp(ScanState* S, cudaGraphConditionalHandle loop, int in_graph) {
+  __shared__ int status[kScanMaxL];
+  __threadfence();
+  const int L = S->L;
+  for (int c = threadIdx.x & 31; c < L; c += 32) status[c] = scan_screen_status(S, c);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    S->ticket = 0;
+    scan_decide_plan(S, nullptr, status, loop, 1, in_graph);
   }
 }
 

@@ -193,3 +193,24 @@ JITTER_CASES = {  # name -> (small_clip kwargs, window)
     "j_gray": (dict(seed=44, t=7, gray=True), 3),
     "j_long": (dict(seed=45, t=40, h=30, w=50), 5),
 }
+
+
+# Motion / gradient weight pairs (w_motion, w_grad): (0.08, 0.92) and (0.46, 0.54) give
+# fl(fl(255 wm) + fl(255 wg)) > 255, so the energy clamp min(e, 255) is live for them.
+WEIGHT_CASES = [(0.6, 0.4), (0.08, 0.92), (0.46, 0.54), (1.0, 0.0), (0.0, 1.0), (0.25, 0.75)]
+
+
+def weights_clip(wm):
+    """14 frames 40x72: slow drift, one cut, saturated patches (energies at the 255 end), a noisy row."""
+    rng = np.random.default_rng(int(wm * 1000) + 17)
+    T, H, W = 14, 40, 72
+    base = rng.integers(0, 256, (H, W, 3), dtype=np.uint8)
+    frames = []
+    for t in range(T):
+        f = np.roll(base, (t // 3, t // 2), axis=(0, 1)).copy()
+        if t >= 9:
+            f = 255 - f
+        f[:6, :8] = 255 * (t & 1)
+        f[(t * 2) % H, :, :] = rng.integers(0, 256, (W, 3), dtype=np.uint8)
+        frames.append(f)
+    return frames, W - 13

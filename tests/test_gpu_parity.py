@@ -227,6 +227,30 @@ def test_size_cases_vs_oracle(P, i):
     assert np.array_equal(dev.cpu().numpy(), np.stack(ref.frames))
 
 
+@pytest.mark.parametrize("wm,wg", cases.WEIGHT_CASES)
+def test_energy_weights_golden(P, wm, wg):
+    """Motion / gradient weight pairs through the scan, the uniform map and the carve against the
+    reference's own outputs (tests/golden/weights.json, make_weights_golden.py) and the oracle:
+    (0.08, 0.92) and (0.46, 0.54) give fl(fl(255 wm) + fl(255 wg)) > 255, so those clips take the
+    clamped kernel variants, the others the clamp-free ones (energy.py:86-87)."""
+    import torch
+    from oracle import scpl_oracle as O
+    with open(os.path.join(os.path.dirname(__file__), "golden", "weights.json")) as fh:
+        g = json.load(fh)[f"{wm}/{wg}"]
+    assert ((np.float64(wm) * 255.0) + (np.float64(wg) * 255.0) > 255.0) == ((wm, wg) in [(0.08, 0.92), (0.46, 0.54)])
+    frames, tw = cases.weights_clip(wm)
+    cfg = dict(target_width=tw, mode="buffered", w_motion=wm, w_grad=wg)
+    out, m = P.retarget_video(frames, P.RetargetConfig(**cfg))
+    assert [list(r) for r in m.runs] == g["runs"]
+    assert m.dp_passes == g["dp_passes"]
+    assert [sha(f) for f in out] == g["frames"]
+    ref = O.retarget_video(frames, **cfg)
+    for a, b in zip(out, ref.frames):
+        assert np.array_equal(a, b)
+    dev, m2 = P.retarget_video_tensor(torch.from_numpy(np.stack(frames)).cuda(), P.RetargetConfig(**cfg))
+    assert [sha(f) for f in dev.cpu().numpy()] == g["frames"]
+
+
 def test_pipeline_errors(P):
     with pytest.raises(ValueError, match="exceeds"):
         P.retarget_image(np.zeros((8, 8), np.uint8), P.RetargetConfig(target_width=9))

@@ -141,3 +141,16 @@ def test_pipeline_C1_golden():
     assert res.dp_passes == g["dp_passes"]
     assert [[[_batch_rec(b, labels=True) for b in ph] for ph in rb] for rb in res.batches] == g["batches"]
     assert [sha(f) for f in res.frames] == g["frames_sha"]
+
+
+@pytest.mark.parametrize("wm,wg", cases.WEIGHT_CASES)
+def test_pipeline_weights_golden(wm, wg):
+    """Non-default motion / gradient weights (two pairs with a live 255 clamp): the oracle against
+    the reference's outputs (tests/golden/make_weights_golden.py)."""
+    with open(os.path.join(GOLD, "weights.json")) as fh:
+        g = json.load(fh)[f"{wm}/{wg}"]
+    frames, tw = cases.weights_clip(wm)
+    ref = O.retarget_video(frames, target_width=tw, mode="buffered", w_motion=wm, w_grad=wg)
+    assert [list(r) for r in ref.runs] == g["runs"]
+    assert ref.dp_passes == g["dp_passes"]
+    assert [sha(f) for f in ref.frames] == g["frames"]
