@@ -62,8 +62,13 @@ void smem_optin(const void* kernel) {
                                  optin - (int)fa.sharedSizeBytes));
   done.insert({dev, kernel});
 }
+// SCPL_GRAPH_PRIO=1 (experiments): the kernel nodes of the scan / carve loop graphs carry the
+// priority of the stream they are launched into (captured nodes otherwise run at the capture
+// stream's default priority).  Measured: no gain on any config, and the carve loops' pool then
+// holds one graph per (shape, priority), so a C4 batch step now and then instantiates graphs
+// (52 -> 96 ms outliers); off by default.
 static bool graph_prio_on() {
-  static const bool on = !(getenv("SCPL_GRAPH_PRIO") && atoi(getenv("SCPL_GRAPH_PRIO")) == 0);
+  static const bool on = getenv("SCPL_GRAPH_PRIO") && atoi(getenv("SCPL_GRAPH_PRIO")) != 0;
   return on;
 }
 void graph_set_priority(cudaGraph_t g, int prio) {
@@ -567,7 +572,7 @@ void carve_launch(scpl_ctx* ctx, CarveSet& S, void* h_state, cudaStream_t st) {
   }
   S.ctx = ctx;
   int prio = 0;  // the loop's kernel nodes carry the group stream's priority (part of the pool key)
-  SCPL_CUDA(cudaStreamGetPriority(st, &prio));
+  if (graph_prio_on()) SCPL_CUDA(cudaStreamGetPriority(st, &prio));
   S.loop_key = {nb, S.rows, S.pitch, S.cols, S.cl, S.cols - S.target + 1, S.max_fr,
                 (int)S.reaverage + 2 * graph + 4 * S.kc + 64 * (int)S.has_uniform + 128 * S.kc_first +
                     2048 * S.cl_first + 65536 * (int)S.fused + (1 << 20) * (prio & 15)};

@@ -57,9 +57,10 @@ void smem_optin(const void* kernel);
 // true the first time (current device, key) is seen (per-device one-time attribute setup)
 bool once_per_device(const void* key);
 // Kernel nodes of a captured graph run at the priority recorded in the node, not at the
-// priority of the stream the graph is launched into: give every kernel node of g this one.
+// priority of the stream the graph is launched into: give every kernel node of g this one
+// (SCPL_GRAPH_PRIO=1; see scpl_api.cu).
 void graph_set_priority(cudaGraph_t g, int prio);
-// the capture stream for a graph whose kernels should run at prio (SCPL_GRAPH_PRIO=0: default)
+// the capture stream for a graph whose kernels should run at prio (only with SCPL_GRAPH_PRIO=1)
 cudaStream_t capture_stream(int prio);
 
 // ---------------------------------------------------------------- exact arithmetic
