@@ -2214,7 +2214,12 @@ __global__ void carve_check_kernel(const CarveRun* __restrict__ runs, int nruns,
 }
 
 static void launch_carve_check(CarveRun* runs_d, int nruns, int max_iters, int* iters_d,
-                               cudaGraphConditionalHandle h, cudaStream_t cs) {
+                               cudaGraphConditionalHandle h, cudaStream_t cs, bool pdl = true) {
+  if (!pdl) {
+    carve_check_kernel<<<1, 256, 0, cs>>>((const CarveRun*)runs_d, nruns, max_iters, iters_d, h);
+    SCPL_CUDA(cudaGetLastError());
+    return;
+  }
   cudaLaunchAttribute pa[1];
   pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pa[0].val.programmaticStreamSerializationAllowed = 1;
@@ -2261,6 +2266,13 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   else
     SCPL_CUDA(cudaLaunchKernelEx(&cfg, carve_pass_kernel, runs_d, cl, f64 ? 1 : 0));
   SCPL_CHECK_LAUNCH();
+  const bool fork = loop && loop->side && !fused && !reaverage;
+  if (fork) {  // the widths are final once the pass is done: the loop condition on a side branch
+    SCPL_CUDA(cudaEventRecord(loop->e_fork, st));
+    SCPL_CUDA(cudaStreamWaitEvent(loop->side, loop->e_fork, 0));
+    launch_carve_check(runs_d, nruns, loop->max_iters, loop->counters, loop->handle, loop->side, false);
+    SCPL_CUDA(cudaEventRecord(loop->e_join, loop->side));
+  }
   if (fused) {  // the next pass's producers remove this batch: no row kernels
     if (reaverage) launch_carve_mean(runs_d, nruns, rows, st);
     if (loop) launch_carve_check(runs_d, nruns, loop->max_iters, loop->counters, loop->handle, st);
@@ -2286,7 +2298,10 @@ void launch_carve_iteration(CarveRun* runs_d, int nruns, int rows, int pitch, in
   SCPL_CUDA(cudaLaunchKernelEx(&rc, carve_dirty_kernel, runs_d));
   SCPL_CHECK_LAUNCH();
   if (reaverage) launch_carve_mean(runs_d, nruns, rows, st);
-  if (loop) launch_carve_check(runs_d, nruns, loop->max_iters, loop->counters, loop->handle, st);
+  if (fork)
+    SCPL_CUDA(cudaStreamWaitEvent(st, loop->e_join, 0));
+  else if (loop)
+    launch_carve_check(runs_d, nruns, loop->max_iters, loop->counters, loop->handle, st);
 }
 
 // Word copy by the SMs.  Small control transfers between device memory and mapped pinned
@@ -2341,10 +2356,22 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   SCPL_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   {
-    const RowsLoop lp{max_iters, iters_d, h};
+    // the loop condition on a side branch of the body (SCPL_CHECK_FORK=0: after the row kernels)
+    static const bool check_fork = !(getenv("SCPL_CHECK_FORK") && atoi(getenv("SCPL_CHECK_FORK")) == 0);
+    RowsLoop lp{max_iters, iters_d, h};
+    if (check_fork) {
+      SCPL_CUDA(cudaStreamCreateWithFlags(&lp.side, cudaStreamNonBlocking));
+      SCPL_CUDA(cudaEventCreateWithFlags(&lp.e_fork, cudaEventDisableTiming));
+      SCPL_CUDA(cudaEventCreateWithFlags(&lp.e_join, cudaEventDisableTiming));
+    }
     launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false, &lp, fused);
+    SCPL_CUDA(cudaStreamEndCapture(cs, &body));
+    if (check_fork) {
+      cudaEventDestroy(lp.e_fork);
+      cudaEventDestroy(lp.e_join);
+      cudaStreamDestroy(lp.side);
+    }
   }
-  SCPL_CUDA(cudaStreamEndCapture(cs, &body));
   graph_set_priority(g, prio);
   graph_set_priority(body, prio);
   g_launches.store(before);  // counted per executed iteration by the caller

@@ -119,6 +119,10 @@ struct RowsLoop {
   int max_iters;
   int* counters;
   cudaGraphConditionalHandle handle;
+  // loop body only: the loop condition is evaluated on a side branch right after the pass (which
+  // writes the widths), next to the row kernels instead of after them (SCPL_CHECK_FORK=0: after)
+  cudaStream_t side = nullptr;
+  cudaEvent_t e_fork = nullptr, e_join = nullptr;
 };
 // one carve iteration of some DP window variant (the fp64 first pass may use another variant)
 using FirstIter = void (*)(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
