@@ -109,6 +109,10 @@ cudaStream_t capture_stream(int prio) {
   return cs;
 }
 std::atomic<long> g_launches{0};
+int carve_unroll() {
+  static const int u = getenv("SCPL_CARVE_UNROLL") ? std::min(8, std::max(1, atoi(getenv("SCPL_CARVE_UNROLL")))) : 4;
+  return u;
+}
 }  // namespace scpl
 
 struct PwPlan {
@@ -629,8 +633,10 @@ void carve_finish(CarveSet& S) {
   const int nruns = (int)S.runs.size();
   if (nruns == 0) return;
   std::memcpy(S.runs.data(), S.h_runs, sizeof(CarveRun) * nruns);
-  g_launches.fetch_add((long)(S.fused ? 2 : kc6::carve_kernels_per_iteration(S.reaverage)) * *S.h_iters,
-                       std::memory_order_relaxed);
+  {  // kernels per executed loop body: the unrolled iterations' kernels + one condition kernel
+    const long per_iter = (S.fused ? 2 : kc6::carve_kernels_per_iteration(S.reaverage)) - 1;
+    g_launches.fetch_add((per_iter * carve_unroll() + 1) * *S.h_iters, std::memory_order_relaxed);
+  }
   for (auto& R : S.runs)
     if (R.width > R.target) throw Error{2, "carve loop stopped before every run reached its target"};
   long long best = -1;

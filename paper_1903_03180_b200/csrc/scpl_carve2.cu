@@ -2364,7 +2364,12 @@ cudaGraphExec_t build_carve_loop(CarveRun* runs_d, int nruns, int rows, int pitc
       SCPL_CUDA(cudaEventCreateWithFlags(&lp.e_fork, cudaEventDisableTiming));
       SCPL_CUDA(cudaEventCreateWithFlags(&lp.e_join, cudaEventDisableTiming));
     }
-    launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false, &lp, fused);
+    // (unrolled bodies: the loop's re-evaluation is paid once per carve_unroll() iterations; only
+    // the last one carries the condition kernel)
+    const int unroll = carve_unroll();
+    for (int u = 0; u < unroll; ++u)
+      launch_carve_iteration(runs_d, nruns, rows, pitch, width, cl, cs, max_fr, reaverage, false,
+                             u == unroll - 1 ? &lp : nullptr, fused);
     SCPL_CUDA(cudaStreamEndCapture(cs, &body));
     if (check_fork) {
       cudaEventDestroy(lp.e_fork);

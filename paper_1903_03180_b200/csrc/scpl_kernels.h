@@ -124,6 +124,9 @@ struct RowsLoop {
   cudaStream_t side = nullptr;
   cudaEvent_t e_fork = nullptr, e_join = nullptr;
 };
+// carve iterations per execution of the device-side loop's body (SCPL_CARVE_UNROLL; runs that are
+// done skip every kernel, so the extra iterations of the last body are no-ops)
+int carve_unroll();
 // one carve iteration of some DP window variant (the fp64 first pass may use another variant)
 using FirstIter = void (*)(CarveRun* runs_d, int nruns, int rows, int pitch, int width, int cl, cudaStream_t st,
                            int max_fr, bool reaverage, bool f64, const RowsLoop* loop, bool fused);
