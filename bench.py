@@ -49,6 +49,9 @@ METRIC = "retargeted frames/sec (1080p, width -25%)"
 UNIT = "frames/s"
 
 
+PRIME_CALLS = 3  # untimed calls before the warm-up steps (graph-pool initialisation)
+
+
 def metric_for(name: str) -> str:
     """BASELINE.json's metric on its own workload (C2); the other configs name theirs."""
     if name == "C2":
@@ -422,6 +425,10 @@ def main():
     def all_runs(m):
         return sum(len(x[1].runs) for x in m) if batch else len(m.runs)
 
+    # initialisation: the library instantiates its pooled CUDA graphs (one per group shape in
+    # flight) on first use; a few untimed calls fill the pool before the W warm-up steps
+    for _ in range(PRIME_CALLS):
+        step(devs)
     for _ in range(a.warmup):
         out, m = step(devs)
     torch.cuda.synchronize()
@@ -464,7 +471,7 @@ def main():
                 host_outs[0].copy_(res, non_blocking=True)
             return host_outs[0], m_
 
-        for _ in range(1):
+        for _ in range(max(1, min(a.warmup, 3))):
             e2e_step()
         barrier()
         torch.cuda.synchronize()
@@ -531,6 +538,7 @@ def main():
                    "frames_per_step": frames_job, "clips_per_step": len(devs) * (1 if split else world),
                    "runs": all_runs(m), "dp_passes": total_dp(m),
                    "l2": f"inputs ({sum(h.numel() for h in host_clips) / 1e9:.2f} GB per rank) larger than L2",
+                   "init": f"{PRIME_CALLS} untimed calls before the warm-up steps (pooled CUDA graphs instantiated)",
                    "parallelism": (f"one clip, runs split over {world} GPUs ("
                                    + ("rank 0 scans, runs dealt LPT-first" if a.scan_once else "every rank scans")
                                    + "; outputs exchanged by NCCL broadcasts)") if split else
