@@ -13,7 +13,9 @@
 // candidates.  A second kernel folds the leaf sums with the same tree (one CTA per
 // candidate).  The per-pixel S,Q after the chunk are checkpointed so the next chunk of
 // the same run resumes without re-reading earlier frames.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstddef>
 #include <vector>
 
@@ -988,8 +990,14 @@ cudaGraphExec_t build_scan_graph(ScanState* S, long N, const int2* leaves, int n
   int chunk = 0;
   const int grid = scan_grid(N, nleaves, chunk);
   const size_t smem = std::max(kStatSmem + spec * kStatRed, kScrSmem);
-  window_stats_scan_kernel<<<grid, 256, smem, cs>>>(S, leaves, nleaves, chunk, vnodes, h, 1);
-  SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
+  // SCPL_SCAN_UNROLL=n (experiments): n windows per execution of the loop body (a window kernel
+  // that finds nothing planned, L == 0, returns at once).  Unlike the carve loop's unrolling this
+  // gains nothing (the kernels that find no window cost what the loop's re-evaluation saves): 1
+  static const int unroll = getenv("SCPL_SCAN_UNROLL") ? std::min(8, std::max(1, atoi(getenv("SCPL_SCAN_UNROLL")))) : 1;
+  for (int u = 0; u < unroll; ++u) {
+    window_stats_scan_kernel<<<grid, 256, smem, cs>>>(S, leaves, nleaves, chunk, vnodes, h, 1);
+    SCPL_CUDA(cudaGetLastError());  // captured, counted per graph launch
+  }
   SCPL_CUDA(cudaStreamEndCapture(cs, &body));
   graph_set_priority(g, prio);
   graph_set_priority(body, prio);
